@@ -1,0 +1,174 @@
+/*
+ * mpdp.h — C ABI of the B200-native MPDP exact join-order optimiser.
+ *
+ * What it computes: the minimum-C_out bushy join tree without cross products
+ * for a connected query graph G(R, E) (§2.1), by the
+ * level-by-level dynamic program of Alg. mpdp_gpu: for subset size
+ * i = 2..n, unrank all i-subsets, filter the connected ones, evaluate MPDP's
+ * block-based join pairs (Alg. mpdp_generalization), keep the best
+ * pair per set and scatter it into a GPU memo hash table.
+ * Every step runs in CUDA kernels on one B200 (sm_100a); the host only
+ * validates the input, stages it and launches.  There is NO CPU fallback:
+ * without a usable CUDA device every call returns MPDP_ERR_CUDA.
+ *
+ * Conventions (readings R1-R10):
+ *   cost(leaf v) = leaf_costs[v] (0 when leaf_costs == NULL)
+ *   cost(S)      = (cost(L) + cost(R)) + card(S)          (C_out)
+ *   card(S)      = product of cardinalities of S and selectivities of the
+ *                  edges induced by S, multiplied in the canonical order R5
+ *   tie-break    = among equal costs the split with the numerically smaller
+ *                  min(L, R) bitmask wins (R7); costs compare exactly
+ *   counters     = csg_count incl. singletons (R1), unordered ccp_pairs (R2),
+ *                  pairs_evaluated = sum over blocks (2^(b-1) - 1) (R3)
+ *
+ * Threading: a context is used by one host thread at a time.  All pointers
+ * passed in are borrowed for the duration of the call and never retained.
+ */
+#ifndef MPDP_H
+#define MPDP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPDP_ABI_VERSION 1
+#define MPDP_MAX_RELATIONS_EXACT 56   /* exact algorithms: n <= 56 (unranking bound) */
+
+typedef enum {
+    MPDP_OK = 0,
+    MPDP_ERR_INVALID_ARGUMENT = 1,  /* bad pointer/size/value (see mpdp_optimize) */
+    MPDP_ERR_DISCONNECTED = 2,      /* G is not connected: no CP-free plan */
+    MPDP_ERR_CAPACITY = 3,          /* n too large or memo exceeds mem budget      */
+    MPDP_ERR_TIMEOUT = 4,           /* timeout_ms exceeded (checked per level)     */
+    MPDP_ERR_OOM = 5,               /* device allocation failed                    */
+    MPDP_ERR_CUDA = 6,              /* CUDA runtime / no device / kernel fault     */
+    MPDP_ERR_NCCL = 7,              /* NCCL failure (multi-GPU)                    */
+    MPDP_ERR_INTERNAL = 8,          /* device-side consistency check failed        */
+    MPDP_ERR_UNSUPPORTED = 9        /* algorithm not provided by this library      */
+} mpdp_status;
+
+typedef enum {
+    MPDP_ALGO_DPSIZE_REF = 0,      /* the CPU reference: NOT in this library (it is
+                                      the test oracle, oracle/liboracle.so) ->
+                                      MPDP_ERR_UNSUPPORTED                          */
+    MPDP_ALGO_MPDP = 1,            /* exact MPDP on the GPU                        */
+    MPDP_ALGO_IDP2_MPDP = 2,       /* IDP2 with MPDP inner DP, bound k */
+    MPDP_ALGO_UNIONDP_MPDP = 3     /* UnionDP with MPDP inner DP, k    */
+} mpdp_algo;
+
+/* The query graph (host memory).  Relations are 0..n-1, bit v of a set mask
+ * is relation v. */
+typedef struct {
+    uint32_t n;                    /* relations, 1..56 for exact algorithms          */
+    const double* cardinalities;   /* [n], finite, > 0                               */
+    uint32_t n_edges;
+    const uint32_t* edges;         /* [2*n_edges] pairs {u, v}: u < v < n, no dups    */
+    const double* selectivities;   /* [n_edges], in (0, 1]                            */
+    const double* leaf_costs;      /* [n] finite >= 0, or NULL (= 0 for every leaf)   */
+} mpdp_query_graph;
+
+/* One plan node.  Internal nodes satisfy nodes[left].set < nodes[right].set
+ * numerically (tie-break R7). */
+typedef struct {
+    int32_t left, right;           /* child node indices, -1 for leaves              */
+    int32_t relation;              /* leaf: relation index; internal: -1             */
+    uint32_t reserved;
+    uint64_t set;                  /* relation bitmask of the subtree                */
+    double cardinality;            /* card(set)                                      */
+    double cost;                   /* C_out cost of the subtree                      */
+} mpdp_plan_node;
+
+typedef struct {
+    mpdp_plan_node* nodes;         /* caller-owned, capacity >= 2n-1, post-order,
+                                      root last; may be NULL (no plan copied)        */
+    uint32_t capacity;
+    uint32_t n_nodes;              /* out: 2n-1                                       */
+    uint32_t root;                 /* out: n_nodes-1                                  */
+    uint32_t gpu_launches;         /* out: kernels launched by this call              */
+    double cost;                   /* out: optimal cost                               */
+    uint64_t pairs_evaluated;      /* out: R3 units                                   */
+    uint64_t ccp_pairs;            /* out: R2 units                                   */
+    uint64_t csg_count;            /* out: R1 units                                   */
+    uint64_t* level_csg;           /* optional [n+1] per-subset-size breakdowns       */
+    uint64_t* level_ccp;           /* optional [n+1]                                  */
+    uint64_t* level_pairs;         /* optional [n+1]                                  */
+    double time_ms;                /* out: device time of the DP (CUDA events)        */
+    uint64_t probes;               /* out: memo probes of non-singleton sets          */
+    uint64_t h2d_bytes;            /* out: host->device bytes copied by this call     */
+    uint64_t d2h_bytes;            /* out: device->host bytes copied by this call     */
+    double enum_ms;                /* out, MPDP_FLAG_PROFILE_KERNELS: sum of k_enum   */
+    double eval_ms;                /* out, MPDP_FLAG_PROFILE_KERNELS: sum of k_eval   */
+    uint32_t enum_launches;        /* out: k_enum launches                            */
+    uint32_t eval_launches;        /* out: k_eval launches                            */
+} mpdp_result;
+
+typedef struct {
+    int device;                    /* CUDA device ordinal                              */
+    int rank, world;               /* multi-GPU SPMD rank / size (1 process per GPU)   */
+    const void* nccl_unique_id;    /* 128 bytes (mpdp_nccl_get_unique_id on rank 0,
+                                      broadcast by the caller); NULL when world == 1  */
+    void* cuda_stream;             /* cudaStream_t to run on, or NULL (own stream)     */
+    uint64_t mem_budget_bytes;     /* device memory the context may use; 0 = 75% of free */
+    double timeout_ms;             /* 0 = none; checked between levels                 */
+    void* workspace;               /* optional caller-owned device buffer (e.g. a torch
+                                      tensor) the context sub-allocates from; NULL = the
+                                      library allocates mem_budget_bytes itself        */
+    uint64_t workspace_bytes;
+    uint32_t flags;                /* MPDP_FLAG_* (0 for normal use)                   */
+    double load_factor;            /* memo load factor in (0, 0.9]; 0 = default 0.5    */
+} mpdp_ctx_config;
+
+/* flags: use 64-bit set masks even when n <= 32 (exercises the wide kernels) */
+#define MPDP_FLAG_FORCE_WIDE_MASKS 1u
+/* flags: record CUDA events around every level kernel (enum_ms / eval_ms)      */
+#define MPDP_FLAG_PROFILE_KERNELS 2u
+
+typedef struct mpdp_ctx mpdp_ctx;
+
+/* Create a context on cfg->device.  Allocates (or adopts) the workspace and, for
+ * world > 1, initialises the NCCL communicator.  Errors: INVALID_ARGUMENT (NULL
+ * pointers, world < 1, rank out of range, world > 1 without a unique id),
+ * CUDA (no device), OOM, NCCL. */
+mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out);
+mpdp_status mpdp_ctx_destroy(mpdp_ctx* ctx);
+
+/* Optimise one query end to end: validate, copy the graph host->device, run
+ * every level, extract the plan on the device and copy the result back.
+ * Blocks until the result is in *out.
+ *   algo MPDP: k must be 0.  IDP2_MPDP / UNIONDP_MPDP: 2 <= k <= 25.
+ * Errors: INVALID_ARGUMENT (NULL pointers, n == 0, u >= v, v >= n, duplicate
+ * edge, selectivity outside (0,1], cardinality <= 0 or non-finite, negative or
+ * non-finite leaf cost, out->capacity < 2n-1 with out->nodes != NULL, sum of
+ * log10 cardinalities > 300), DISCONNECTED, CAPACITY (n > 56, memo larger than
+ * the budget), TIMEOUT, CUDA, UNSUPPORTED (DPSIZE_REF).  On error *out is left
+ * unspecified and mpdp_last_error() describes it. */
+mpdp_status mpdp_optimize(mpdp_ctx* ctx, const mpdp_query_graph* graph, mpdp_algo algo,
+                          uint32_t k, mpdp_result* out);
+
+/* Split form of mpdp_optimize(MPDP) for device-resident timing:
+ *   mpdp_stage : validate + stage the graph (async H2D on the context stream)
+ *   mpdp_run   : enqueue every level + plan extraction; returns without a host
+ *                sync (single GPU), the memo and the plan stay in device memory
+ *   mpdp_fetch : copy the result back (blocks) and check device status      */
+mpdp_status mpdp_stage(mpdp_ctx* ctx, const mpdp_query_graph* graph);
+mpdp_status mpdp_run(mpdp_ctx* ctx);
+mpdp_status mpdp_fetch(mpdp_ctx* ctx, mpdp_result* out);
+
+/* Thread-local description of the last error on this context (never NULL). */
+const char* mpdp_last_error(const mpdp_ctx* ctx);
+const char* mpdp_status_string(mpdp_status s);
+int mpdp_abi_version(void);
+
+/* Multi-GPU bootstrap: 128-byte NCCL unique id (call on rank 0 only). */
+mpdp_status mpdp_nccl_get_unique_id(void* out128);
+
+/* Contiguous share [lo, hi) of `total` work units for `rank` of `world`
+ * (the per-level partition of the connected-set list). Pure host
+ * arithmetic, exported so multi-process host logic is testable on CPU. */
+void mpdp_share(uint64_t total, int rank, int world, uint64_t* lo, uint64_t* hi);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPDP_H */

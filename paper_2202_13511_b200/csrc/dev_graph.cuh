@@ -1,0 +1,211 @@
+// dev_graph.cuh — the query graph as the level kernels see it (shared memory)
+// and the per-set graph primitives: canonical card(S), grow, connectivity,
+// blocks (biconnected components) and MPDP's join-pair enumeration.
+#pragma once
+#include "dev_common.cuh"
+
+namespace mpdp {
+
+template <typename M> struct MaxN;
+template <> struct MaxN<uint32_t> { static constexpr int value = 32; };
+template <> struct MaxN<uint64_t> { static constexpr int value = kMaxN; };
+
+// Query as staged in global memory (written by the host once per query).
+template <typename M> struct QueryDev {
+    static constexpr int N = MaxN<M>::value;
+    int n, cls, max_depth, pad;
+    M adj[N];            // adjacency bitmaps ("adjacency lists ... as bitmap sets")
+    M desc[N];           // CLS_TREE: vertices of the subtree rooted at v (root = 0)
+    M depth_mask[N];     // CLS_TREE: vertices at depth d
+    double card[N];      // base cardinalities
+    double leaf[N];      // leaf costs (0 for base relations, subplan cost for composites)
+    double sel[N * N];   // sel[u * n + v] for edges, 0 otherwise
+    unsigned long long binom[(N + 1) * (N + 1)];   // C(i, j) at i * (N + 1) + j
+};
+
+// The part every kernel keeps in shared memory (sel compacted to n x n).
+template <typename M> struct SQ {
+    static constexpr int N = MaxN<M>::value;
+    int n, cls, max_depth, pad;
+    M adj[N];
+    M desc[N];
+    M depth_mask[N];
+    double card[N];
+    double leaf[N];
+    double sel[N * N];
+};
+
+template <typename M>
+__device__ __forceinline__ void load_query(SQ<M>& s, const QueryDev<M>* q) {
+    const int n = q->n;
+    if (threadIdx.x == 0) {
+        s.n = n;
+        s.cls = q->cls;
+        s.max_depth = q->max_depth;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        s.adj[i] = q->adj[i];
+        s.desc[i] = q->desc[i];
+        s.depth_mask[i] = q->depth_mask[i];
+        s.card[i] = q->card[i];
+        s.leaf[i] = q->leaf[i];
+    }
+    for (int i = threadIdx.x; i < n * n; i += blockDim.x) s.sel[i] = q->sel[i];
+}
+
+// card(S) in the canonical order of reading R5 (no FMA: only multiplies,
+// and __dmul_rn pins round-to-nearest):
+//   x = 1; for v in S ascending { x *= card[v]; for u in S n adj(v), u < v ascending: x *= sel(u,v) }
+template <typename M>
+__device__ __forceinline__ double card_of(const SQ<M>& q, M S) {
+    double x = 1.0;
+    for (M T = S; T; T &= T - 1) {
+        const int v = ctz(T);
+        x = __dmul_rn(x, q.card[v]);
+        for (M U = S & q.adj[v] & (bitm<M>(v) - 1); U; U &= U - 1)
+            x = __dmul_rn(x, q.sel[ctz(U) * q.n + v]);
+    }
+    return x;
+}
+
+// grow(source, restriction) (Alg. grow): all vertices of the
+// restriction reachable from the source.  Frontier-at-a-time BFS in registers:
+// N = (OR adj[v] over the frontier) & restriction & ~V.
+template <typename M>
+__device__ __forceinline__ M grow(const SQ<M>& q, M source, M restriction) {
+    M V = source, F = source;
+    while (F) {
+        M N = 0;
+        for (M T = F; T; T &= T - 1) N |= q.adj[ctz(T)];
+        N &= restriction & ~V;
+        V |= N;
+        F = N;
+    }
+    return V;
+}
+
+// connected(S) (Alg. connected): grow from the lowest vertex
+// (reading R9), stopping as soon as every vertex is reached.
+template <typename M>
+__device__ __forceinline__ bool connected(const SQ<M>& q, M S) {
+    if (!S) return false;
+    M V = lowbit(S), F = V;
+    while (F) {
+        if (V == S) return true;
+        M N = 0;
+        for (M T = F; T; T &= T - 1) N |= q.adj[ctz(T)];
+        N &= S & ~V;
+        V |= N;
+        F = N;
+    }
+    return V == S;
+}
+
+// 2|E(G[S])|
+template <typename M>
+__device__ __forceinline__ int induced_degree_sum(const SQ<M>& q, M S) {
+    int e2 = 0;
+    for (M T = S; T; T &= T - 1) e2 += popc(q.adj[ctz(T)] & S);
+    return e2;
+}
+
+// Find-Blocks: biconnected components of G[S] by an iterative
+// Hopcroft-Tarjan DFS with a vertex stack; bitmask adjacency, small local arrays.
+template <typename M>
+__device__ int find_blocks(const SQ<M>& q, M S, M* blk) {
+    constexpr int N = MaxN<M>::value;
+    unsigned char disc[N], low[N], par[N], vst[N], dst[N];
+    M rem[N];
+    int vsp = 0, dsp = 0, t = 0, nb = 0;
+    const int r = ctz(S);
+    M visited = bitm<M>(r);
+    disc[r] = low[r] = (unsigned char)t++;
+    par[r] = 0xff;
+    rem[r] = q.adj[r] & S;
+    vst[vsp++] = (unsigned char)r;
+    dst[dsp++] = (unsigned char)r;
+    while (dsp) {
+        const int v = dst[dsp - 1];
+        if (rem[v]) {
+            const int u = ctz(rem[v]);
+            rem[v] &= rem[v] - 1;
+            if (!((visited >> u) & 1)) {
+                visited |= bitm<M>(u);
+                par[u] = (unsigned char)v;
+                disc[u] = low[u] = (unsigned char)t++;
+                rem[u] = q.adj[u] & S;
+                vst[vsp++] = (unsigned char)u;
+                dst[dsp++] = (unsigned char)u;
+            } else if (u != par[v]) {
+                if (disc[u] < low[v]) low[v] = disc[u];
+            }
+        } else {
+            --dsp;
+            if (dsp) {
+                const int p = par[v];
+                if (low[v] < low[p]) low[p] = low[v];
+                if (low[v] >= disc[p]) {          // p separates v's subtree: a block
+                    M B = bitm<M>(p);
+                    int w;
+                    do {
+                        w = vst[--vsp];
+                        B |= bitm<M>(w);
+                    } while (w != v);
+                    blk[nb++] = B;
+                }
+            }
+        }
+    }
+    return nb;
+}
+
+enum SetKind : int { KIND_TREE = 0, KIND_COMPLETE = 1, KIND_BLOCKS = 2 };
+
+// Kind and MPDP join-pair count (reading R3) of one connected set of size k:
+// tree-induced sets have one pair per edge (Alg. mpdp_trees);
+// complete sets are one block with 2^(k-1)-1 splits (Lemma generic:opt);
+// otherwise sum over blocks of 2^(b-1)-1 (Alg. mpdp_generalization).
+template <typename M, int CLS>
+__device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned long long& w) {
+    if (CLS == CLS_TREE) {
+        w = (unsigned long long)(k - 1);
+        return KIND_TREE;
+    }
+    if (CLS == CLS_CLIQUE) {
+        w = (1ull << (k - 1)) - 1;
+        return KIND_COMPLETE;
+    }
+    const int e2 = induced_degree_sum(q, S);
+    if (e2 == 2 * (k - 1)) {
+        w = (unsigned long long)(k - 1);
+        return KIND_TREE;
+    }
+    if (e2 == k * (k - 1)) {
+        w = (1ull << (k - 1)) - 1;
+        return KIND_COMPLETE;
+    }
+    M blk[MaxN<M>::value];
+    const int nb = find_blocks(q, S, blk);
+    unsigned long long s = 0;
+    for (int i = 0; i < nb; i++) s += (1ull << (popc(blk[i]) - 1)) - 1;
+    w = s;
+    return KIND_BLOCKS;
+}
+
+// colex combinadic unrank (reading R10): the r-th k-subset of {0..n-1} has
+// elements c_k > ... > c_1 with r = sum_i C(c_i, i)
+template <typename M>
+__device__ __forceinline__ M unrank_colex(const unsigned long long* binom, int stride, int n, int k,
+                                          unsigned long long r) {
+    M S = 0;
+    int c = n - 1;
+    for (int i = k; i >= 1; i--) {
+        while (binom[c * stride + i] > r) c--;
+        S |= bitm<M>(c);
+        r -= binom[c * stride + i];
+        c--;
+    }
+    return S;
+}
+
+}  // namespace mpdp

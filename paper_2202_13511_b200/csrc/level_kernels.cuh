@@ -1,0 +1,802 @@
+// level_kernels.cuh — the per-level kernels of the MPDP dynamic program
+// (Alg. mpdp_gpu) for sm_100a.
+//
+//   k_enum<M,CLS>    unrank (colex + Gosper) -> connectivity
+//                    filter (grow from the lowest vertex) -> set
+//                    kind + join-pair count -> stream compaction into a light
+//                    list (<= 32 pairs: thread per set) and a heavy list, with
+//                    a single-pass decoupled look-back scan.
+//   k_eval<M,CLS>    evaluate MPDP's join pairs (Alg. mpdp_generalization
+//                    P:531-579), C_out cost with memo probes, per-set
+//                    min (prune fused into evaluate) and scatter into
+//                    the level's open-addressing memo.
+//   k_extract<M>     plan extraction from the memo + counters.
+#pragma once
+#include "dev_graph.cuh"
+#include "../../include/mpdp.h"
+
+namespace mpdp {
+
+struct __align__(16) LevelDesc {
+    unsigned long long n_light, n_heavy;   // compacted connected sets
+    unsigned long long heavy_pairs;        // sum of heavy-set pair counts
+    unsigned long long n_items;            // heavy work items of `item` pairs
+    unsigned long long pairs, ccp;         // counters (R3, R2)
+    unsigned long long probes;             // memo probes of non-singleton sets
+    unsigned long long bucket_off, n_buckets;   // this level's memo table
+    unsigned int tile_ticket, work_ticket, pad0, pad1;
+};
+
+struct __align__(64) TileRec {            // decoupled look-back record (ring slot)
+    unsigned long long flag;               // tile << 24 | epoch22 << 2 | state (1 aggregate, 2 inclusive)
+    unsigned long long agg_l, agg_h, agg_w;
+    unsigned long long inc_l, inc_h, inc_w, pad;
+};
+
+enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u };
+
+struct ResultDev {
+    double cost;
+    unsigned long long csg, ccp, pairs, probes;
+    unsigned int n_nodes, error;
+    unsigned long long lvl_csg[kMaxN + 1], lvl_ccp[kMaxN + 1], lvl_pairs[kMaxN + 1];
+    mpdp_plan_node nodes[2 * kMaxN - 1];
+};
+
+template <typename M> struct Params {
+    const QueryDev<M>* q;
+    LevelDesc* desc;                       // [kMaxN + 1], indexed by subset size
+    Bucket* arena;                         // memo tables of every level, bump-allocated
+    M* cold;                               // left(S) per slot (2 per bucket)
+    unsigned long long arena_buckets;
+    M* light;                              // compacted level lists (reused per level)
+    M* heavy;
+    unsigned long long* wh;                // [list_cap + 1] exclusive heavy pair prefix
+    Key* bkey;                             // [list_cap] cross-warp (cost, left) min
+    unsigned long long* bdone;             // [list_cap] pairs merged so far
+    unsigned int* first_heavy;             // [fh_cap] heavy set holding item i's first pair
+    unsigned long long fh_cap;
+    TileRec* tiles;                        // ring of look-back records
+    unsigned long long tiles_ring;         // power of two
+    unsigned long long list_cap;           // light list capacity
+    unsigned long long heavy_cap;          // heavy list capacity
+    ResultDev* result;
+    unsigned long long epoch;              // look-back epoch base (unique per query)
+    unsigned int gen;                      // memo tag of this query
+    int n;
+    double inv_load;                       // buckets = ceil(count * inv_load / 2)
+};
+
+// ------------------------------------------------------------- mem helpers
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// --------------------------------------------------------------- memo I/O
+struct Tabs {                              // per-level table geometry in smem
+    unsigned long long off[kMaxN + 1];
+    unsigned long long nb[kMaxN + 1];
+};
+
+// One memo bucket = one 32-byte L2 sector, fetched with a single 256-bit
+// read-only load (LDG.E.ENL2.256): tables of earlier levels are immutable
+// while level k is evaluated.
+struct B4 {
+    unsigned long long k0, c0, k1, c1;
+};
+__device__ __forceinline__ B4 ld_bucket(const Bucket* b) {
+    B4 r;
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.k0), "=l"(r.c0), "=l"(r.k1), "=l"(r.c1)
+                 : "l"(b));
+    return r;
+}
+
+// Continue a linear probe after the home bucket (rare at load factor 0.5).
+template <typename M>
+__device__ __noinline__ double probe_tail(const Params<M>& p, const Tabs& t, M T, int j, unsigned long long b,
+                                          unsigned long long* slot_out) {
+    const unsigned long long want = Tag<M>::make(T, p.gen);
+    const unsigned int g = Tag<M>::gen_of(want);
+    const unsigned long long nb = t.nb[j];
+    B4 x = ld_bucket(p.arena + t.off[j] + b);
+    for (unsigned long long guard = 0; guard < nb; guard++) {
+        if (x.k0 == want) {
+            if (slot_out) *slot_out = (t.off[j] + b) * 2;
+            return __longlong_as_double((long long)x.c0);
+        }
+        if (x.k1 == want) {
+            if (slot_out) *slot_out = (t.off[j] + b) * 2 + 1;
+            return __longlong_as_double((long long)x.c1);
+        }
+        if (Tag<M>::gen_of(x.k0) != g || Tag<M>::gen_of(x.k1) != g) break;   // empty slot: absent
+        b = (b + 1 == nb) ? 0 : b + 1;
+        x = ld_bucket(p.arena + t.off[j] + b);
+    }
+    atomicOr(&p.result->error, ERR_PROBE);
+    return __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// cost(T) for one set (extraction path): leaf or probe of the level-|T| table.
+template <typename M>
+__device__ __forceinline__ double probe(const Params<M>& p, const Tabs& t, M T, int j,
+                                        unsigned long long* slot_out = nullptr) {
+    return probe_tail(p, t, T, j, fastrange(fmix(T), t.nb[j]), slot_out);
+}
+
+// Batched cost lookup: all home-bucket loads of the batch are issued before any
+// is consumed, so each thread keeps up to NP probes in flight.
+template <typename M, int NP>
+__device__ __forceinline__ void lookup_batch(const Params<M>& p, const SQ<M>& q, const Tabs& t, const M (&X)[NP],
+                                             unsigned valid, double (&c)[NP], unsigned long long& nprobe) {
+    B4 bk[NP];
+    unsigned long long bi[NP];
+    int jj[NP];
+#pragma unroll
+    for (int i = 0; i < NP; i++) {
+        jj[i] = popc(X[i]);
+        bi[i] = 0;
+        if (((valid >> i) & 1) && jj[i] > 1) {
+            bi[i] = fastrange(fmix(X[i]), t.nb[jj[i]]);
+            bk[i] = ld_bucket(p.arena + t.off[jj[i]] + bi[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NP; i++) {
+        c[i] = 0.0;
+        if (!((valid >> i) & 1)) continue;
+        if (jj[i] == 1) {
+            c[i] = q.leaf[ctz(X[i])];
+            continue;
+        }
+        nprobe++;
+        const unsigned long long want = Tag<M>::make(X[i], p.gen);
+        if (bk[i].k0 == want) c[i] = __longlong_as_double((long long)bk[i].c0);
+        else if (bk[i].k1 == want) c[i] = __longlong_as_double((long long)bk[i].c1);
+        else c[i] = probe_tail(p, t, X[i], jj[i], bi[i], nullptr);
+    }
+}
+
+// Collects join pairs (A, B) of one set and evaluates them four at a time:
+// cost = (cost(A) + cost(B)) + card(S) (C_out; no FMA, reading R6) and
+// the lexicographic (cost, min(A, B)) minimum (reading R7).
+template <typename M>
+struct PairSink {
+    static constexpr int NP = kSinkPairs;
+    M A[NP], B[NP];
+    int cnt;
+    double cS;
+    Key best;
+    unsigned long long nprobe;
+
+    __device__ __forceinline__ void init(double card) {
+        cnt = 0;
+        cS = card;
+        best = key_inf();
+        nprobe = 0;
+    }
+    __device__ __forceinline__ void flush(const Params<M>& p, const SQ<M>& q, const Tabs& t) {
+        if (!cnt) return;
+        M X[2 * NP];
+        unsigned valid = 0;
+#pragma unroll
+        for (int u = 0; u < NP; u++) {
+            X[2 * u] = A[u];
+            X[2 * u + 1] = B[u];
+            if (u < cnt) valid |= 3u << (2 * u);
+        }
+        double c[2 * NP];
+        lookup_batch<M, 2 * NP>(p, q, t, X, valid, c, nprobe);
+#pragma unroll
+        for (int u = 0; u < NP; u++) {
+            if (u < cnt) {
+                const double v = __dadd_rn(__dadd_rn(c[2 * u], c[2 * u + 1]), cS);
+                const Key key{(unsigned long long)__double_as_longlong(v),
+                              (unsigned long long)(A[u] < B[u] ? A[u] : B[u])};
+                if (key_less(key, best)) best = key;
+            }
+        }
+        cnt = 0;
+    }
+    __device__ __forceinline__ void add(const Params<M>& p, const SQ<M>& q, const Tabs& t, M a, M b) {
+#pragma unroll
+        for (int u = NP - 1; u > 0; u--) {
+            A[u] = A[u - 1];
+            B[u] = B[u - 1];
+        }
+        A[0] = a;
+        B[0] = b;
+        if (++cnt == NP) flush(p, q, t);
+    }
+};
+
+// scatter (S, best) into the level-k table: claim a slot by CAS on
+// its tagged key, then store the cost and the cold `left` mask.
+template <typename M>
+__device__ __forceinline__ void memo_insert(const Params<M>& p, unsigned long long off,
+                                            unsigned long long nb, M S, const Key& best) {
+    const unsigned long long want = Tag<M>::make(S, p.gen);
+    const unsigned int g = Tag<M>::gen_of(want);
+    Bucket* base = p.arena + off;
+    unsigned long long b = fastrange(fmix(S), nb);
+    for (unsigned long long guard = 0; guard < nb; guard++) {
+#pragma unroll
+        for (int s = 0; s < 2; s++) {
+            unsigned long long* kp = &base[b].s[s].key;
+            unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
+            while (Tag<M>::gen_of(cur) != g) {
+                const unsigned long long old = atomicCAS(kp, cur, want);
+                if (old == cur) {
+                    base[b].s[s].cost = __longlong_as_double((long long)best.c);
+                    p.cold[(off + b) * 2 + s] = (M)best.l;
+                    return;
+                }
+                cur = old;
+            }
+        }
+        b = (b + 1 == nb) ? 0 : b + 1;
+    }
+    atomicOr(&p.result->error, ERR_TABLE_FULL);
+}
+
+// ------------------------------------------------------------ k_init
+template <typename M>
+__global__ void k_init(Params<M> p) {
+    for (int i = threadIdx.x; i <= kMaxN; i += blockDim.x) {
+        LevelDesc d = {};
+        p.desc[i] = d;
+    }
+    if (threadIdx.x == 0) p.result->error = 0;
+}
+
+// ------------------------------------------------------------ k_enum
+// Block-wide exclusive scan of three counters (light sets, heavy sets, heavy pairs).
+struct Tri {
+    unsigned long long l, h, w;
+};
+
+__device__ __forceinline__ Tri block_scan(Tri v, Tri& total) {
+    __shared__ Tri s_warp[kBlock / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    Tri inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long l = __shfl_up_sync(0xffffffffu, inc.l, o);
+        const unsigned long long h = __shfl_up_sync(0xffffffffu, inc.h, o);
+        const unsigned long long w = __shfl_up_sync(0xffffffffu, inc.w, o);
+        if (lane >= o) {
+            inc.l += l;
+            inc.h += h;
+            inc.w += w;
+        }
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    Tri base = {0, 0, 0}, tot = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < kBlock / 32; i++) {
+        if (i < wid) {
+            base.l += s_warp[i].l;
+            base.h += s_warp[i].h;
+            base.w += s_warp[i].w;
+        }
+        tot.l += s_warp[i].l;
+        tot.h += s_warp[i].h;
+        tot.w += s_warp[i].w;
+    }
+    total = tot;
+    return Tri{base.l + inc.l - v.l, base.h + inc.h - v.h, base.w + inc.w - v.w};
+}
+
+// Warp-parallel decoupled look-back (warp 0 of the CTA): lanes read the flags of
+// the 32 preceding tiles at once; the exclusive prefix is the sum of aggregates
+// back to the nearest tile that already published its inclusive prefix.
+__device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask, unsigned long long tile,
+                                        unsigned long long epoch, Tri agg) {
+    const int lane = threadIdx.x & 31;
+    TileRec* tr = tiles + (tile & rmask);
+    const unsigned long long me = (tile << 24) | epoch;
+    if (lane == 0) {
+        if (tile == 0) {
+            tr->inc_l = agg.l;
+            tr->inc_h = agg.h;
+            tr->inc_w = agg.w;
+            st_release(&tr->flag, me | 2ull);
+        } else {
+            tr->agg_l = agg.l;
+            tr->agg_h = agg.h;
+            tr->agg_w = agg.w;
+            st_release(&tr->flag, me | 1ull);
+        }
+    }
+    Tri excl = {0, 0, 0};
+    if (tile == 0) return excl;
+    long long top = (long long)tile - 1;
+    while (true) {
+        const long long jj = top - lane;
+        const TileRec* pr = tiles + ((unsigned long long)jj & rmask);
+        bool ready = true, inc = true;
+        if (jj >= 0) {
+            const unsigned long long f = ld_acquire(&pr->flag);
+            const bool mine = (f & ~3ull) == (((unsigned long long)jj << 24) | epoch);
+            ready = mine && (f & 3ull) != 0;
+            inc = mine && (f & 3ull) == 2;
+        }
+        const unsigned inc_mask = __ballot_sync(0xffffffffu, inc);
+        const unsigned ready_mask = __ballot_sync(0xffffffffu, ready);
+        const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+        const unsigned need = (first_inc >= 31) ? 0xffffffffu : ((2u << first_inc) - 1u);
+        if ((ready_mask & need) != need) continue;           // a predecessor has not published yet
+        Tri v = {0, 0, 0};
+        if (jj >= 0 && lane <= first_inc) {
+            if (lane == first_inc) {
+                v.l = ld_relaxed(&pr->inc_l);
+                v.h = ld_relaxed(&pr->inc_h);
+                v.w = ld_relaxed(&pr->inc_w);
+            } else {
+                v.l = ld_relaxed(&pr->agg_l);
+                v.h = ld_relaxed(&pr->agg_h);
+                v.w = ld_relaxed(&pr->agg_w);
+            }
+        }
+        excl.l += warp_sum(v.l);
+        excl.h += warp_sum(v.h);
+        excl.w += warp_sum(v.w);
+        if (first_inc < 32) break;
+        top -= 32;
+    }
+    if (lane == 0) {
+        tr->inc_l = excl.l + agg.l;
+        tr->inc_h = excl.h + agg.h;
+        tr->inc_w = excl.w + agg.w;
+        st_release(&tr->flag, me | 2ull);
+    }
+    return excl;
+}
+
+// Persistent CTAs claim tiles of kTile consecutive colex ranks in ticket order.
+template <typename M, int CLS>
+__global__ void __launch_bounds__(kBlock) k_enum(Params<M> p, int k, unsigned long long nranks,
+                                                 unsigned long long ntiles, unsigned long long item) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);    // only n and adj[] are used here
+    constexpr int NB = MaxN<M>::value + 1;
+    unsigned long long* binom = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(SQ<M>));
+    __shared__ unsigned long long s_tile;
+    __shared__ Tri s_excl, s_agg;
+
+    const int n = p.q->n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q.adj[i] = p.q->adj[i];
+    for (int i = threadIdx.x; i < n * NB; i += blockDim.x) binom[i] = p.q->binom[i];
+    if (threadIdx.x == 0) q.n = n;
+    const unsigned long long rmask = p.tiles_ring - 1;
+    const unsigned long long epoch = ((p.epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
+
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&p.desc[k].tile_ticket, 1u);
+        __syncthreads();
+        const unsigned long long tile = s_tile;
+        if (tile >= ntiles) break;
+
+        // ---- unrank + filter + classify (registers only)
+        const unsigned long long r0 = tile * kTile + (unsigned long long)threadIdx.x * kRanksPerThread;
+        M S0 = 0;
+        unsigned int lflag = 0, hflag = 0;
+        Tri mine = {0, 0, 0};
+        if (r0 < nranks) {
+            S0 = unrank_colex<M>(binom, NB, n, k, r0);
+            M S = S0;
+#pragma unroll
+            for (int i = 0; i < kRanksPerThread; i++) {
+                if (r0 + i < nranks) {
+                    if (connected(q, S)) {
+                        unsigned long long w;
+                        set_kind<M, CLS>(q, S, k, w);
+                        if (w <= kLightMax) {
+                            lflag |= 1u << i;
+                        } else {
+                            hflag |= 1u << i;
+                            mine.w += w;
+                        }
+                    }
+                    if (r0 + i + 1 < nranks) S = gosper(S);
+                }
+            }
+        }
+        mine.l = __popc(lflag);
+        mine.h = __popc(hflag);
+
+        // ---- block scan + warp-parallel decoupled look-back
+        Tri agg;
+        const Tri ex = block_scan(mine, agg);
+        if (threadIdx.x < 32) {
+            const Tri excl = lookback(p.tiles, rmask, tile, epoch, agg);
+            if (threadIdx.x == 0) {
+                s_excl = excl;
+                s_agg = agg;
+            }
+        }
+        __syncthreads();
+        const Tri excl = s_excl;
+        if (threadIdx.x == 0 && tile == ntiles - 1) {   // the last tile knows the level totals
+            LevelDesc& d = p.desc[k];
+            const Tri a = s_agg;
+            const unsigned long long L = excl.l + a.l, H = excl.h + a.h, W = excl.w + a.w;
+            d.n_light = L;
+            d.n_heavy = H;
+            d.heavy_pairs = W;
+            d.n_items = (W + item - 1) / item;
+            if (d.n_items > p.fh_cap) atomicOr(&p.result->error, ERR_ITEMS);
+            if (H < p.heavy_cap + 1) p.wh[H] = W;
+            const unsigned long long cnt = L + H;
+            if (L > p.list_cap || H > p.heavy_cap) atomicOr(&p.result->error, ERR_CAPACITY);
+            unsigned long long nbk = (unsigned long long)ceil((double)cnt * p.inv_load * 0.5);
+            if (nbk < 1) nbk = 1;
+            const unsigned long long off = (k <= 2) ? 0ull : p.desc[k - 1].bucket_off + p.desc[k - 1].n_buckets;
+            if (off + nbk > p.arena_buckets || L > p.list_cap || H > p.heavy_cap) {
+                atomicOr(&p.result->error, ERR_CAPACITY);
+                nbk = 0;
+            }
+            d.bucket_off = off;
+            d.n_buckets = nbk;
+            d.work_ticket = 0;
+        }
+
+        // ---- scatter this thread's survivors (colex order is preserved)
+        if (lflag | hflag) {
+            unsigned long long li = excl.l + ex.l, hi = excl.h + ex.h, wi = excl.w + ex.w;
+            M S = S0;
+#pragma unroll
+            for (int i = 0; i < kRanksPerThread; i++) {
+                if ((lflag >> i) & 1) {
+                    if (li < p.list_cap) p.light[li] = S;
+                    li++;
+                }
+                if ((hflag >> i) & 1) {
+                    unsigned long long w;
+                    set_kind<M, CLS>(q, S, k, w);
+                    if (hi < p.heavy_cap) {
+                        p.heavy[hi] = S;
+                        p.wh[hi] = wi;
+                        p.bkey[hi] = key_inf();
+                        p.bdone[hi] = 0;
+                        // items whose first pair lies in [wi, wi + w)
+                        const unsigned long long it0 = (wi + item - 1) / item, it1 = (wi + w - 1) / item;
+                        for (unsigned long long it = it0; it <= it1; it++)
+                            if (it < p.fh_cap) p.first_heavy[it] = (unsigned int)hi;
+                    }
+                    wi += w;
+                    hi++;
+                }
+                if (r0 + i + 1 < nranks && i + 1 < kRanksPerThread) S = gosper(S);
+            }
+        }
+        __syncthreads();                   // s_tile / s_excl / scan scratch reused next tile
+    }
+}
+
+// ------------------------------------------------------------ k_eval
+// Evaluate pairs j in [j0, j1) of connected set S (|S| = k) into the sink.
+// Pair numbering per kind:
+//   KIND_TREE, CLS_TREE : j -> j-th vertex v of S below the set's top vertex;
+//                         the pair is (S n subtree(v), rest)   [edge (v, parent v)]
+//   KIND_TREE, general  : j -> j-th induced edge (v, u), v < u; sides by grow
+//   KIND_COMPLETE       : j -> lb = {min S} u deposit(j, S \ min S)
+//   KIND_BLOCKS         : blocks in DFS order, per block j -> lb = {min B} u
+//                         deposit(j, B \ min B); CCP check inside the block
+//                         unless the block is complete (Lemma generic:opt);
+//                         S_left = grow(lb, S \ rb), S_right = S \ S_left
+template <typename M, int CLS>
+__device__ void eval_range(const Params<M>& p, const SQ<M>& q, const Tabs& t, M S, int k, int kind,
+                           unsigned long long j0, unsigned long long j1, PairSink<M>& sink,
+                           unsigned long long& nccp) {
+    if (j0 >= j1) return;
+    if (kind == KIND_TREE) {
+        if (CLS == CLS_TREE) {
+            M top = 0;
+            for (int d = 0; d <= q.max_depth; d++) {
+                const M T = S & q.depth_mask[d];
+                if (T) {
+                    top = lowbit(T);
+                    break;
+                }
+            }
+            M Mv = S & ~top;                       // one pair per edge (v, parent v)
+            for (unsigned long long j = 0; j < j0; j++) Mv &= Mv - 1;
+            for (unsigned long long j = j0; j < j1; j++) {
+                const int v = ctz(Mv);
+                Mv &= Mv - 1;
+                const M A = S & q.desc[v];
+                sink.add(p, q, t, A, S ^ A);
+            }
+        } else if (CLS == CLS_GENERAL) {
+            unsigned long long j = 0;
+            for (M T = S; T && j < j1; T &= T - 1) {
+                const int v = ctz(T);
+                const M up = q.adj[v] & S & ~(bitm<M>(v + 1) - 1);   // neighbours u > v in S
+                const unsigned long long c = (unsigned long long)popc(up);
+                if (j + c <= j0) {
+                    j += c;
+                    continue;
+                }
+                for (M U = up; U && j < j1; U &= U - 1, j++) {
+                    if (j < j0) continue;
+                    const int u = ctz(U);
+                    const M A = grow(q, bitm<M>(v), S & ~bitm<M>(u));
+                    sink.add(p, q, t, A, S ^ A);
+                }
+            }
+        }
+        nccp += j1 - j0;
+        return;
+    }
+    if (CLS == CLS_TREE) return;           // trees have no other kind
+    if (kind == KIND_COMPLETE) {
+        const M lo = lowbit(S), R = S ^ lo;
+        M sub = deposit<M>(j0, R);
+        for (unsigned long long j = j0; j < j1; j++) {
+            const M A = lo | sub;
+            sink.add(p, q, t, A, S ^ A);
+            sub = (sub - R) & R;
+        }
+        nccp += j1 - j0;
+        return;
+    }
+    if (CLS != CLS_GENERAL) return;        // cliques are one complete block
+    // KIND_BLOCKS
+    M blk[MaxN<M>::value];
+    const int nb = find_blocks(q, S, blk);
+    unsigned long long base = 0;
+    for (int bi = 0; bi < nb && base < j1; bi++) {
+        const M Bm = blk[bi];
+        const int b = popc(Bm);
+        const unsigned long long wb = (1ull << (b - 1)) - 1;
+        if (base + wb <= j0) {
+            base += wb;
+            continue;
+        }
+        const bool complete = induced_degree_sum(q, Bm) == b * (b - 1);
+        const unsigned long long a0 = (j0 > base ? j0 - base : 0), a1 = (j1 - base < wb ? j1 - base : wb);
+        const M lo = lowbit(Bm), R = Bm ^ lo;
+        M sub = deposit<M>(a0, R);
+        for (unsigned long long j = a0; j < a1; j++) {
+            const M lb = lo | sub, rb = Bm ^ lb;
+            sub = (sub - R) & R;
+            if (!complete && !(connected(q, lb) && connected(q, rb))) continue;   // CCP block
+            nccp++;
+            const M A = grow(q, lb, S & ~rb);
+            sink.add(p, q, t, A, S ^ A);                                        // S_right = S \ S_left
+        }
+        base += wb;
+    }
+}
+
+// Shared prologue of the evaluate kernels: the query, the geometry of every
+// lower level's memo table and this level's descriptor go to shared memory.
+template <typename M>
+__device__ __forceinline__ void eval_prologue(const Params<M>& p, int k, SQ<M>& q, Tabs& t, LevelDesc& d) {
+    load_query(q, p.q);
+    for (int j = threadIdx.x; j <= k; j += blockDim.x) {
+        t.off[j] = (j >= 2) ? p.desc[j].bucket_off : 0;
+        t.nb[j] = (j >= 2) ? p.desc[j].n_buckets : 0;
+    }
+    if (threadIdx.x == 0) d = p.desc[k];
+    __syncthreads();
+}
+
+__device__ __forceinline__ void flush_counters(LevelDesc* dk, unsigned long long pairs, unsigned long long nccp,
+                                               unsigned long long nprobe) {
+    pairs = warp_sum(pairs);
+    nccp = warp_sum(nccp);
+    nprobe = warp_sum(nprobe);
+    if ((threadIdx.x & 31) == 0) {
+        if (pairs) atomicAdd(&dk->pairs, pairs);
+        if (nccp) atomicAdd(&dk->ccp, nccp);
+        if (nprobe) atomicAdd(&dk->probes, nprobe);
+    }
+}
+
+// Light sets (<= kLightMax join pairs): one thread evaluates a whole set, keeps
+// its min in registers and scatters it (prune fused into evaluate).
+template <typename M, int CLS>
+__global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Params<M> p, int k) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
+    __shared__ Tabs t;
+    __shared__ LevelDesc d;
+    eval_prologue(p, k, q, t, d);
+    if (d.n_buckets == 0) return;          // capacity error already flagged
+    unsigned long long pairs = 0, nccp = 0, nprobe = 0;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long n_light = d.n_light;
+    const unsigned long long units = (n_light + stride - 1) / stride;
+    for (unsigned long long u = 0; u < units; u++) {     // warp-uniform trip count
+        const unsigned long long i = u * stride + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (i < n_light) {
+            const M S = p.light[i];
+            unsigned long long w;
+            const int kind = set_kind<M, CLS>(q, S, k, w);
+            PairSink<M> sink;
+            sink.init(card_of(q, S));
+            eval_range<M, CLS>(p, q, t, S, k, kind, 0, w, sink, nccp);
+            sink.flush(p, q, t);
+            nprobe += sink.nprobe;
+            pairs += w;
+            memo_insert(p, d.bucket_off, d.n_buckets, S, sink.best);
+        }
+    }
+    flush_counters(&p.desc[k], pairs, nccp, nprobe);
+}
+
+// Heavy sets: the heavy pair space is cut into `item`-pair work items; warps
+// claim groups of items dynamically, evaluate lane-contiguous chunks, reduce
+// with shuffles, and merge split sets through a 128-bit CAS min + a pair
+// counter (the last contributor scatters the set).
+template <typename M, int CLS>
+__global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, unsigned long long item) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
+    __shared__ Tabs t;
+    __shared__ LevelDesc d;
+    eval_prologue(p, k, q, t, d);
+    if (d.n_buckets == 0 || d.n_items == 0) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long pairs = 0, nccp = 0, nprobe = 0;
+    unsigned long long G = d.n_items / (nwarps * 4);
+    if (G < 1) G = 1;
+    const unsigned long long ngroups = (d.n_items + G - 1) / G;
+    while (true) {
+        unsigned long long g = 0;
+        if (lane == 0) g = atomicAdd(&p.desc[k].work_ticket, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= ngroups) break;
+        const unsigned long long c0 = g * G * item;
+        unsigned long long c1 = (g + 1) * G * item;
+        if (c1 > d.heavy_pairs) c1 = d.heavy_pairs;
+        unsigned long long h = p.first_heavy[g * G];
+        for (; h < d.n_heavy; h++) {
+            const unsigned long long W0 = p.wh[h], w = p.wh[h + 1] - W0;
+            if (W0 >= c1) break;
+            const unsigned long long a = (c0 > W0 ? c0 - W0 : 0), b = (c1 - W0 < w ? c1 - W0 : w);
+            const M S = p.heavy[h];
+            unsigned long long wk;
+            const int kind = set_kind<M, CLS>(q, S, k, wk);
+            PairSink<M> sink;
+            sink.init(card_of(q, S));
+            // lane-contiguous chunks of the segment [a, b)
+            const unsigned long long cnt = b - a, per = (cnt + 31) >> 5;
+            unsigned long long j0 = a + per * lane, j1 = j0 + per;
+            if (j0 > b) j0 = b;
+            if (j1 > b) j1 = b;
+            eval_range<M, CLS>(p, q, t, S, k, kind, j0, j1, sink, nccp);
+            sink.flush(p, q, t);
+            nprobe += sink.nprobe;
+            const Key best = warp_min(sink.best);
+            if (lane == 0) {
+                pairs += cnt;
+                if (a == 0 && b == w) {
+                    memo_insert(p, d.bucket_off, d.n_buckets, S, best);
+                } else {
+                    atomic_key_min(&p.bkey[h], best);
+                    __threadfence();
+                    const unsigned long long old = atomicAdd(&p.bdone[h], cnt);
+                    if (old + cnt == w) {      // last contributor finalises the set
+                        __threadfence();
+                        const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&p.bkey[h]);
+                        const Key fin{ld_relaxed(kp), ld_relaxed(kp + 1)};
+                        memo_insert(p, d.bucket_off, d.n_buckets, S, fin);
+                    }
+                }
+            }
+        }
+    }
+    flush_counters(&p.desc[k], pairs, nccp, nprobe);
+}
+
+// ------------------------------------------------------------ k_extract
+// One thread walks the memo from the full set: left(S) from the
+// cold array, right = S \ left; nodes in post-order, root last.
+template <typename M>
+__global__ void k_extract(Params<M> p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
+    __shared__ Tabs t;
+    load_query(q, p.q);
+    for (int j = threadIdx.x; j <= kMaxN; j += blockDim.x) {
+        t.off[j] = (j >= 2 && j <= p.n) ? p.desc[j].bucket_off : 0;
+        t.nb[j] = (j >= 2 && j <= p.n) ? p.desc[j].n_buckets : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    ResultDev* r = p.result;
+    const int n = p.n;
+    unsigned long long csg = (unsigned long long)n, ccp = 0, pairs = 0, probes = 0;
+    r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
+    r->lvl_csg[1] = (unsigned long long)n;
+    r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
+    for (int j = 2; j <= n; j++) {
+        const LevelDesc& d = p.desc[j];
+        r->lvl_csg[j] = d.n_light + d.n_heavy;
+        r->lvl_ccp[j] = d.ccp;
+        r->lvl_pairs[j] = d.pairs;
+        csg += d.n_light + d.n_heavy;
+        ccp += d.ccp;
+        pairs += d.pairs;
+        probes += d.probes;
+    }
+    r->probes = probes;
+    r->csg = csg;
+    r->ccp = ccp;
+    r->pairs = pairs;
+    if (r->error) {
+        r->n_nodes = 0;
+        return;
+    }
+    // explicit-stack post-order walk
+    M st_set[2 * kMaxN];
+    int st_state[2 * kMaxN], st_left[2 * kMaxN];
+    int sp = 0, nn = 0;
+    const M all = (n == (int)(8 * sizeof(M))) ? ~(M)0 : (bitm<M>(n) - 1);
+    st_set[0] = all;
+    st_state[0] = 0;
+    sp = 1;
+    int last = -1;
+    while (sp) {
+        const int top = sp - 1;
+        const M S = st_set[top];
+        if (popc(S) == 1) {
+            const int v = ctz(S);
+            mpdp_plan_node& nd = r->nodes[nn];
+            nd.left = nd.right = -1;
+            nd.relation = v;
+            nd.reserved = 0;
+            nd.set = (unsigned long long)S;
+            nd.cardinality = q.card[v];
+            nd.cost = q.leaf[v];
+            last = nn++;
+            --sp;
+            continue;
+        }
+        unsigned long long slot = 0;
+        const double c = probe(p, t, S, popc(S), &slot);
+        const M L = p.cold[slot];
+        if (st_state[top] == 0) {
+            st_state[top] = 1;
+            st_set[sp] = L;
+            st_state[sp] = 0;
+            sp++;
+        } else if (st_state[top] == 1) {
+            st_left[top] = last;
+            st_state[top] = 2;
+            st_set[sp] = S & ~L;
+            st_state[sp] = 0;
+            sp++;
+        } else {
+            mpdp_plan_node& nd = r->nodes[nn];
+            nd.left = st_left[top];
+            nd.right = last;
+            nd.relation = -1;
+            nd.reserved = 0;
+            nd.set = (unsigned long long)S;
+            nd.cardinality = card_of(q, S);
+            nd.cost = c;
+            last = nn++;
+            --sp;
+        }
+    }
+    r->n_nodes = (unsigned int)nn;
+    r->cost = r->nodes[nn - 1].cost;
+}
+
+}  // namespace mpdp

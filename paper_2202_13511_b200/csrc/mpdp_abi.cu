@@ -1,0 +1,618 @@
+// mpdp_abi.cu — host engine + C ABI (include/mpdp.h) of the B200 MPDP library.
+//
+// The host validates and stages the query graph (a0 of SURVEY §8(a)), carves
+// the workspace, and enqueues the level loop of Alg. mpdp_gpu:
+//   k_init -> for k = 2..n { k_enum<k> ; k_eval<k> } -> k_extract
+// All on one CUDA stream with no host synchronisation between levels (the
+// per-level table size and heavy-work counts live in device memory), so a
+// query costs one H2D copy, 2n kernels and one D2H copy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <string>
+#include <vector>
+
+#include "level_kernels.cuh"
+
+using namespace mpdp;
+
+namespace {
+
+thread_local std::string g_tls_error;
+
+struct DevLayout {
+    size_t query = 0, desc = 0, result = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
+           fh = 0, arena = 0, cold = 0, end = 0;
+    unsigned long long list_cap = 0, heavy_cap = 0, tiles_cap = 0, fh_cap = 0, arena_buckets = 0;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct mpdp_ctx {
+    int device = 0, rank = 0, world = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    unsigned char* ws = nullptr;
+    size_t ws_bytes = 0;
+    bool own_ws = false;
+    int num_sms = 0;
+    double timeout_ms = 0;
+    std::string err;
+
+    // staged query
+    int n = 0, cls = CLS_TREE;
+    bool wide = false;                    // 64-bit masks
+    bool staged = false;
+    std::vector<unsigned long long> binom;
+    void* h_query = nullptr;              // pinned QueryDev<uint64_t>-sized buffer
+    ResultDev* h_result = nullptr;        // pinned
+    DevLayout lay;
+    unsigned int gen32 = 0, gen8 = 0;
+    int last_width = 0;
+    unsigned long long query_counter = 0;
+    unsigned int launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool ran = false;
+    int occ[2][3][3] = {};               // [wide][class][enum, light, heavy]
+    unsigned int flags = 0;
+    double load_factor = 0.5;
+    cudaEvent_t kev[2 * kMaxN + 2] = {};  // MPDP_FLAG_PROFILE_KERNELS: around every level kernel
+    int nkev = 0;
+    unsigned int enum_launches = 0, eval_launches = 0;
+    size_t h2d_bytes = 0, d2h_bytes = 0;
+};
+
+static mpdp_status fail(mpdp_ctx* c, mpdp_status s, const std::string& msg) {
+    g_tls_error = msg;
+    if (c) c->err = msg;
+    return s;
+}
+
+#define CUDA_TRY(ctx, x)                                                                      \
+    do {                                                                                      \
+        cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? MPDP_ERR_OOM : MPDP_ERR_CUDA, \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                     \
+    } while (0)
+
+static unsigned long long binom_u64(int n, int k) {
+    if (k < 0 || k > n) return 0;
+    if (k > n - k) k = n - k;
+    unsigned long long r = 1;
+    for (int i = 1; i <= k; i++) r = r / i * (n - k + i) + r % i * (n - k + i) / i;
+    return r;
+}
+
+static unsigned long long sat_mul(unsigned long long a, unsigned long long b) {
+    if (a && b > ~0ull / a) return ~0ull;
+    return a * b;
+}
+
+// ------------------------------------------------------------ validation
+static mpdp_status validate(mpdp_ctx* c, const mpdp_query_graph* g, std::vector<unsigned long long>& adj) {
+    if (!g) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "graph is NULL");
+    if (g->n == 0) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "n == 0");
+    if (g->n > (uint32_t)kMaxN)
+        return fail(c, MPDP_ERR_CAPACITY, "exact MPDP supports n <= 56 relations (unranking bound)");
+    if (!g->cardinalities) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "cardinalities is NULL");
+    if (g->n_edges && (!g->edges || !g->selectivities))
+        return fail(c, MPDP_ERR_INVALID_ARGUMENT, "edges/selectivities is NULL");
+    const int n = (int)g->n;
+    adj.assign(n, 0);
+    double lsum = 0;
+    for (int v = 0; v < n; v++) {
+        const double x = g->cardinalities[v];
+        if (!(x > 0.0) || !std::isfinite(x))
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "cardinality[" + std::to_string(v) + "] not finite > 0");
+        lsum += std::log10(std::max(x, 1.0));
+        if (g->leaf_costs && (!(g->leaf_costs[v] >= 0.0) || !std::isfinite(g->leaf_costs[v])))
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "leaf_costs[" + std::to_string(v) + "] not finite >= 0");
+    }
+    if (lsum > 300.0) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "sum of log10 cardinalities > 300");
+    for (uint32_t e = 0; e < g->n_edges; e++) {
+        const uint32_t u = g->edges[2 * e], v = g->edges[2 * e + 1];
+        const double s = g->selectivities[e];
+        if (!(u < v) || v >= g->n)
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "edge " + std::to_string(e) + " not u < v < n");
+        if (adj[u] >> v & 1ull) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "duplicate edge " + std::to_string(e));
+        if (!(s > 0.0) || !(s <= 1.0))
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "selectivity " + std::to_string(e) + " outside (0,1]");
+        adj[u] |= 1ull << v;
+        adj[v] |= 1ull << u;
+    }
+    // connectivity (no cross products): host BFS over the adjacency
+    unsigned long long seen = 1ull, frontier = 1ull;
+    while (frontier) {
+        unsigned long long nx = 0;
+        for (unsigned long long f = frontier; f; f &= f - 1) nx |= adj[__builtin_ctzll(f)];
+        nx &= ~seen;
+        seen |= nx;
+        frontier = nx;
+    }
+    const unsigned long long all = (n == 64) ? ~0ull : ((1ull << n) - 1);
+    if (seen != all) return fail(c, MPDP_ERR_DISCONNECTED, "query graph is not connected (cross products excluded)");
+    return MPDP_OK;
+}
+
+// ------------------------------------------------------------ staging
+template <typename M>
+static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector<unsigned long long>& adj,
+                       QueryDev<M>* q) {
+    const int n = (int)g->n;
+    memset(q, 0, sizeof(QueryDev<M>));
+    q->n = n;
+    q->cls = c->cls;
+    for (int v = 0; v < n; v++) {
+        q->adj[v] = (M)adj[v];
+        q->card[v] = g->cardinalities[v];
+        q->leaf[v] = g->leaf_costs ? g->leaf_costs[v] : 0.0;
+    }
+    for (uint32_t e = 0; e < g->n_edges; e++) {
+        const uint32_t u = g->edges[2 * e], v = g->edges[2 * e + 1];
+        q->sel[u * n + v] = q->sel[v * n + u] = g->selectivities[e];
+    }
+    if (c->cls == CLS_TREE) {             // root the tree at 0: subtree masks + depth masks
+        std::vector<int> order, parent(n, -1), depth(n, 0);
+        order.push_back(0);
+        parent[0] = 0;
+        for (size_t i = 0; i < order.size(); i++) {
+            const int v = order[i];
+            for (unsigned long long a = adj[v]; a; a &= a - 1) {
+                const int u = __builtin_ctzll(a);
+                if (parent[u] < 0) {
+                    parent[u] = v;
+                    depth[u] = depth[v] + 1;
+                    order.push_back(u);
+                }
+            }
+        }
+        std::vector<unsigned long long> desc(n, 0);
+        for (int i = (int)order.size() - 1; i >= 0; i--) {
+            const int v = order[i];
+            desc[v] |= 1ull << v;
+            if (v != 0) desc[parent[v]] |= desc[v];
+        }
+        int maxd = 0;
+        for (int v = 0; v < n; v++) {
+            q->desc[v] = (M)desc[v];
+            q->depth_mask[depth[v]] |= (M)1 << v;
+            maxd = std::max(maxd, depth[v]);
+        }
+        q->max_depth = maxd;
+    }
+    constexpr int NB = MaxN<M>::value + 1;
+    for (int i = 0; i < NB; i++)
+        for (int j = 0; j < NB; j++) q->binom[i * NB + j] = binom_u64(i, j);
+}
+
+static unsigned long long heavy_pair_bound(int n, int k, int cls) {
+    const unsigned long long C = binom_u64(n, k);
+    if (cls == CLS_TREE) return (k - 1 > (int)kLightMax) ? sat_mul(C, (unsigned long long)(k - 1)) : 0ull;
+    if (k - 1 >= 63) return ~0ull;
+    const unsigned long long w = (1ull << (k - 1)) - 1;
+    if (w <= kLightMax) return 0;
+    return sat_mul(C, w);
+}
+
+static unsigned long long level_item(int n, int k, int cls, unsigned long long fh_cap) {
+    const unsigned long long ub = heavy_pair_bound(n, k, cls);
+    unsigned long long item = 256;
+    if (fh_cap && ub / fh_cap + 1 > item) item = ub / fh_cap + 1;
+    return (item + 31) / 32 * 32;
+}
+
+// Workspace layout: [header | memo arena (buckets) | cold left[] | scratch].
+// The arena has a fixed position and size for a given (workspace, mask width),
+// so stale bytes inside it are always memo slots of earlier queries (their tag
+// differs) and never need clearing; the per-query scratch (look-back ring, level
+// lists, heavy bookkeeping) lives after it.
+static mpdp_status plan_layout(mpdp_ctx* c) {
+    DevLayout L;
+    const int n = c->n;
+    const size_t msz = c->wide ? 8 : 4;
+    unsigned long long list_cap = 1, tiles_cap = 1, heavy_cap = 1, fh_need = 1;
+    for (int k = 2; k <= n; k++) {
+        const unsigned long long C = binom_u64(n, k);
+        list_cap = std::max(list_cap, C);
+        tiles_cap = std::max(tiles_cap, (C + kTile - 1) / kTile);
+        const unsigned long long ub = heavy_pair_bound(n, k, c->cls);
+        if (ub) {
+            heavy_cap = std::max(heavy_cap, C);
+            fh_need = std::max(fh_need, std::min<unsigned long long>(ub / 256 + 2, 1ull << 24));
+        }
+    }
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        off = align_up(off, 256);
+        const size_t at = off;
+        off += bytes;
+        return at;
+    };
+    L.query = take(sizeof(QueryDev<uint64_t>));
+    L.desc = take(sizeof(LevelDesc) * (kMaxN + 1));
+    L.result = take(sizeof(ResultDev));
+    off = align_up(off, 256);
+    if (off + (64u << 20) > c->ws_bytes) return fail(c, MPDP_ERR_CAPACITY, "workspace smaller than 64 MiB");
+    const size_t body = c->ws_bytes - off - 1024;
+    const unsigned long long buckets = (unsigned long long)((body * 3 / 4) / (sizeof(Bucket) + 2 * msz));
+    L.arena = take(sizeof(Bucket) * buckets);
+    L.cold = take(2 * msz * buckets);
+    const size_t scratch0 = align_up(off, 256);
+    const size_t scratch = c->ws_bytes - scratch0 - 1024;
+    // level lists are bounded by C(n,k) and by the scratch space (sparse graphs with
+    // large n keep few of their C(n,k) subsets); overflow is detected on the device
+    unsigned long long ring = 1;
+    while (ring < tiles_cap && ring < (1ull << 20)) ring <<= 1;
+    tiles_cap = ring;
+    const size_t fixed = sizeof(TileRec) * tiles_cap + 4 * fh_need + 4096;
+    if (fixed >= scratch) return fail(c, MPDP_ERR_CAPACITY, "workspace too small for n = " + std::to_string(n));
+    const size_t avail = scratch - fixed;
+    list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / msz);
+    heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 32));
+    L.tiles = take(sizeof(TileRec) * tiles_cap);
+    L.light = take(msz * list_cap);
+    L.heavy = take(msz * heavy_cap);
+    L.wh = take(8 * (heavy_cap + 1));
+    L.bkey = take(16 * heavy_cap);
+    L.bdone = take(8 * heavy_cap);
+    L.fh = take(4 * fh_need);
+    L.end = off;
+    if (L.end > c->ws_bytes) return fail(c, MPDP_ERR_INTERNAL, "layout overflow");
+    L.list_cap = list_cap;
+    L.heavy_cap = heavy_cap;
+    L.tiles_cap = tiles_cap;
+    L.fh_cap = fh_need;
+    L.arena_buckets = buckets;
+    c->lay = L;
+    return MPDP_OK;
+}
+
+template <typename M>
+static Params<M> make_params(mpdp_ctx* c) {
+    Params<M> p;
+    unsigned char* b = c->ws;
+    const DevLayout& L = c->lay;
+    p.q = reinterpret_cast<const QueryDev<M>*>(b + L.query);
+    p.desc = reinterpret_cast<LevelDesc*>(b + L.desc);
+    p.arena = reinterpret_cast<Bucket*>(b + L.arena);
+    p.cold = reinterpret_cast<M*>(b + L.cold);
+    p.arena_buckets = L.arena_buckets;
+    p.light = reinterpret_cast<M*>(b + L.light);
+    p.heavy = reinterpret_cast<M*>(b + L.heavy);
+    p.wh = reinterpret_cast<unsigned long long*>(b + L.wh);
+    p.bkey = reinterpret_cast<Key*>(b + L.bkey);
+    p.bdone = reinterpret_cast<unsigned long long*>(b + L.bdone);
+    p.first_heavy = reinterpret_cast<unsigned int*>(b + L.fh);
+    p.fh_cap = L.fh_cap;
+    p.tiles = reinterpret_cast<TileRec*>(b + L.tiles);
+    p.tiles_ring = L.tiles_cap;
+    p.list_cap = L.list_cap;
+    p.heavy_cap = L.heavy_cap;
+    p.result = reinterpret_cast<ResultDev*>(b + L.result);
+    p.epoch = c->query_counter << 6;     // + level k (k <= 56 < 64)
+    p.gen = c->wide ? c->gen8 : c->gen32;
+    p.n = c->n;
+    p.inv_load = 1.0 / c->load_factor;
+    return p;
+}
+
+template <typename M, int CLS>
+static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
+    const size_t smem_enum = sizeof(SQ<M>) + sizeof(unsigned long long) * (MaxN<M>::value + 1) * (MaxN<M>::value + 1);
+    const size_t smem_eval = sizeof(SQ<M>);
+    int* occ = c->occ[c->wide][CLS];      // {enum, light, heavy} CTAs per SM
+    if (!occ[0]) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_enum<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_enum));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_eval_light<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eval));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_eval_heavy<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eval));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_enum<M, CLS>, kBlock, smem_enum));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_eval_light<M, CLS>, kLightBlock, smem_eval));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_eval_heavy<M, CLS>, kBlock, smem_eval));
+        for (int i = 0; i < 3; i++) occ[i] = std::max(occ[i], 1);
+    }
+    const bool prof = c->flags & MPDP_FLAG_PROFILE_KERNELS;
+    const auto t0 = std::chrono::steady_clock::now();
+    c->nkev = 0;
+    c->enum_launches = c->eval_launches = 0;
+    if (prof && c->n >= 2) CUDA_TRY(c, cudaEventRecord(c->kev[c->nkev++], c->stream));
+    for (int k = 2; k <= c->n; k++) {
+        const unsigned long long nranks = binom_u64(c->n, k);
+        const unsigned long long ntiles = (nranks + kTile - 1) / kTile;
+        const unsigned long long item = level_item(c->n, k, CLS, c->lay.fh_cap);
+        const unsigned int grid_enum = (unsigned int)std::min<unsigned long long>(ntiles, (unsigned long long)c->num_sms * occ[0]);
+        // a level has at most C(n,k) light sets: no more light CTAs than that
+        const unsigned long long light_ctas = (nranks + kLightBlock - 1) / kLightBlock;
+        const unsigned int grid_light = (unsigned int)std::min<unsigned long long>(light_ctas, (unsigned long long)c->num_sms * occ[1]);
+        k_enum<M, CLS><<<grid_enum, kBlock, smem_enum, c->stream>>>(p, k, nranks, ntiles, item);
+        if (prof) CUDA_TRY(c, cudaEventRecord(c->kev[c->nkev++], c->stream));
+        k_eval_light<M, CLS><<<grid_light, kLightBlock, smem_eval, c->stream>>>(p, k);
+        c->launches += 2;
+        if (heavy_pair_bound(c->n, k, CLS)) {
+            k_eval_heavy<M, CLS><<<c->num_sms * occ[2], kBlock, smem_eval, c->stream>>>(p, k, item);
+            c->launches++;
+        }
+        if (prof) CUDA_TRY(c, cudaEventRecord(c->kev[c->nkev++], c->stream));
+        c->enum_launches++;
+        c->eval_launches++;
+        CUDA_TRY(c, cudaGetLastError());
+        if (c->timeout_ms > 0) {
+            CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (ms > c->timeout_ms) return fail(c, MPDP_ERR_TIMEOUT, "timeout after level " + std::to_string(k));
+        }
+    }
+    return MPDP_OK;
+}
+
+template <typename M>
+static mpdp_status run_typed(mpdp_ctx* c) {
+    const Params<M> p = make_params<M>(c);
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    k_init<M><<<1, 64, 0, c->stream>>>(p);
+    c->launches = 1;
+    mpdp_status st = MPDP_OK;
+    switch (c->cls) {
+        case CLS_TREE: st = launch_levels<M, CLS_TREE>(c, p); break;
+        case CLS_CLIQUE: st = launch_levels<M, CLS_CLIQUE>(c, p); break;
+        default: st = launch_levels<M, CLS_GENERAL>(c, p); break;
+    }
+    if (st != MPDP_OK) return st;
+    k_extract<M><<<1, 64, sizeof(SQ<M>), c->stream>>>(p);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes = sizeof(ResultDev);
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    return MPDP_OK;
+}
+
+// ------------------------------------------------------------ C ABI
+extern "C" {
+
+int mpdp_abi_version(void) { return MPDP_ABI_VERSION; }
+
+const char* mpdp_status_string(mpdp_status s) {
+    switch (s) {
+        case MPDP_OK: return "MPDP_OK";
+        case MPDP_ERR_INVALID_ARGUMENT: return "MPDP_ERR_INVALID_ARGUMENT";
+        case MPDP_ERR_DISCONNECTED: return "MPDP_ERR_DISCONNECTED";
+        case MPDP_ERR_CAPACITY: return "MPDP_ERR_CAPACITY";
+        case MPDP_ERR_TIMEOUT: return "MPDP_ERR_TIMEOUT";
+        case MPDP_ERR_OOM: return "MPDP_ERR_OOM";
+        case MPDP_ERR_CUDA: return "MPDP_ERR_CUDA";
+        case MPDP_ERR_NCCL: return "MPDP_ERR_NCCL";
+        case MPDP_ERR_INTERNAL: return "MPDP_ERR_INTERNAL";
+        case MPDP_ERR_UNSUPPORTED: return "MPDP_ERR_UNSUPPORTED";
+    }
+    return "unknown";
+}
+
+const char* mpdp_last_error(const mpdp_ctx* ctx) {
+    if (ctx) return ctx->err.c_str();
+    return g_tls_error.c_str();
+}
+
+void mpdp_share(uint64_t total, int rank, int world, uint64_t* lo, uint64_t* hi) {
+    if (world < 1) world = 1;
+    const unsigned __int128 t = total;
+    *lo = (uint64_t)(t * (unsigned)rank / (unsigned)world);
+    *hi = (uint64_t)(t * (unsigned)(rank + 1) / (unsigned)world);
+}
+
+mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
+    if (!cfg || !out) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "cfg/out is NULL");
+    *out = nullptr;
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+        return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "bad rank/world");
+    if (cfg->world > 1)
+        return fail(nullptr, MPDP_ERR_UNSUPPORTED, "multi-GPU contexts are not enabled in this build");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, MPDP_ERR_CUDA, "no CUDA device (this library has no CPU path)");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "bad device");
+    if (cfg->load_factor < 0.0 || cfg->load_factor > 0.9)
+        return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "load_factor outside (0, 0.9]");
+    mpdp_ctx* c = new mpdp_ctx();
+    c->device = cfg->device;
+    c->rank = cfg->rank;
+    c->world = cfg->world;
+    c->timeout_ms = cfg->timeout_ms;
+    c->flags = cfg->flags;
+    if (cfg->load_factor > 0.0) c->load_factor = cfg->load_factor;
+    auto bail = [&](mpdp_status s) {
+        mpdp_ctx_destroy(c);
+        return s;
+    };
+    if (cudaSetDevice(c->device) != cudaSuccess) return bail(fail(nullptr, MPDP_ERR_CUDA, "cudaSetDevice failed"));
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, c->device);
+    c->num_sms = prop.multiProcessorCount;
+    if (prop.major < 10) return bail(fail(nullptr, MPDP_ERR_CUDA, "needs an sm_100 (Blackwell B200) device"));
+    if (cfg->cuda_stream) {
+        c->stream = (cudaStream_t)cfg->cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(nullptr, MPDP_ERR_CUDA, "stream create failed"));
+        c->own_stream = true;
+    }
+    if (cfg->workspace) {
+        c->ws = (unsigned char*)cfg->workspace;
+        c->ws_bytes = cfg->workspace_bytes;
+    } else {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        size_t want = cfg->mem_budget_bytes ? cfg->mem_budget_bytes : (size_t)(fr * 0.25);
+        if (cudaMalloc(&c->ws, want) != cudaSuccess) return bail(fail(nullptr, MPDP_ERR_OOM, "workspace allocation failed"));
+        c->ws_bytes = want;
+        c->own_ws = true;
+    }
+    if (cudaMemsetAsync(c->ws, 0, c->ws_bytes, c->stream) != cudaSuccess)
+        return bail(fail(nullptr, MPDP_ERR_CUDA, "workspace clear failed"));
+    if (cudaMallocHost(&c->h_query, sizeof(QueryDev<uint64_t>)) != cudaSuccess ||
+        cudaMallocHost(&c->h_result, sizeof(ResultDev)) != cudaSuccess)
+        return bail(fail(nullptr, MPDP_ERR_OOM, "pinned host allocation failed"));
+    cudaEventCreate(&c->ev0);
+    cudaEventCreate(&c->ev1);
+    for (auto& e : c->kev) cudaEventCreate(&e);
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(nullptr, MPDP_ERR_CUDA, "init sync failed"));
+    *out = c;
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
+    if (!c) return MPDP_OK;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->own_ws && c->ws) cudaFree(c->ws);
+    if (c->h_query) cudaFreeHost(c->h_query);
+    if (c->h_result) cudaFreeHost(c->h_result);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    for (auto& e : c->kev)
+        if (e) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
+    if (!c) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    c->staged = false;
+    c->ran = false;
+    std::vector<unsigned long long> adj;
+    mpdp_status st = validate(c, g, adj);
+    if (st != MPDP_OK) return st;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    // the previous query's D2H must be done before the pinned buffers are reused
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    const int n = (int)g->n;
+    c->n = n;
+    c->wide = n > 32 || (c->flags & MPDP_FLAG_FORCE_WIDE_MASKS);
+    const unsigned long long m = g->n_edges;
+    if (n >= 3 && m == (unsigned long long)n * (n - 1) / 2) c->cls = CLS_CLIQUE;
+    else if (m == (unsigned long long)(n - 1)) c->cls = CLS_TREE;
+    else c->cls = CLS_GENERAL;
+    const DevLayout prev = c->lay;
+    st = plan_layout(c);
+    if (st != MPDP_OK) return st;
+    // memo tags: a fresh tag per query makes every slot of an earlier query read as empty
+    const int width = c->wide ? 64 : 32;
+    bool clear = (c->last_width != 0 && c->last_width != width);   // arena geometry changed
+    if (prev.tiles != c->lay.tiles || prev.tiles_cap != c->lay.tiles_cap)   // ring moved/grew over scratch
+        CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.tiles, 0, sizeof(TileRec) * c->lay.tiles_cap, c->stream));
+    if (c->wide) {
+        if (++c->gen8 > 255) { c->gen8 = 1; clear = true; }
+    } else {
+        if (++c->gen32 == 0) { c->gen32 = 1; clear = true; }
+    }
+    if (clear) CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.arena, 0, c->lay.cold - c->lay.arena, c->stream));
+    c->last_width = width;
+    c->query_counter++;
+    // look-back epochs are 22 bits wide (query * 64 + level): recycle the ring
+    // records before an epoch value can repeat
+    if ((c->query_counter & ((1ull << 15) - 1)) == 0)
+        CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.tiles, 0, sizeof(TileRec) * c->lay.tiles_cap, c->stream));
+    if (c->wide) {
+        fill_query<uint64_t>(c, g, adj, (QueryDev<uint64_t>*)c->h_query);
+        CUDA_TRY(c, cudaMemcpyAsync(c->ws + c->lay.query, c->h_query, sizeof(QueryDev<uint64_t>), cudaMemcpyHostToDevice, c->stream));
+        c->h2d_bytes = sizeof(QueryDev<uint64_t>);
+    } else {
+        fill_query<uint32_t>(c, g, adj, (QueryDev<uint32_t>*)c->h_query);
+        CUDA_TRY(c, cudaMemcpyAsync(c->ws + c->lay.query, c->h_query, sizeof(QueryDev<uint32_t>), cudaMemcpyHostToDevice, c->stream));
+        c->h2d_bytes = sizeof(QueryDev<uint32_t>);
+    }
+    c->staged = true;
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_run(mpdp_ctx* c) {
+    if (!c) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->staged) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "no staged query");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    const mpdp_status st = c->wide ? run_typed<uint64_t>(c) : run_typed<uint32_t>(c);
+    if (st == MPDP_OK) c->ran = true;
+    return st;
+}
+
+mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
+    if (!c || !out) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "ctx/out is NULL");
+    if (!c->ran) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "nothing was run");
+    const int n = c->n;
+    if (out->nodes && out->capacity < (uint32_t)(2 * n - 1))
+        return fail(c, MPDP_ERR_INVALID_ARGUMENT, "result capacity < 2n-1");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    CUDA_TRY(c, cudaGetLastError());
+    const ResultDev* r = c->h_result;
+    if (r->error) {
+        if (r->error & (ERR_CAPACITY | ERR_ITEMS))
+            return fail(c, MPDP_ERR_CAPACITY, "memo does not fit the workspace (device error bits " + std::to_string(r->error) + ")");
+        return fail(c, MPDP_ERR_INTERNAL, "device consistency check failed (bits " + std::to_string(r->error) + ")");
+    }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    out->time_ms = ms;
+    out->n_nodes = r->n_nodes;
+    out->root = r->n_nodes ? r->n_nodes - 1 : 0;
+    out->cost = r->cost;
+    out->csg_count = r->csg;
+    out->ccp_pairs = r->ccp;
+    out->pairs_evaluated = r->pairs;
+    out->gpu_launches = c->launches;
+    out->probes = r->probes;
+    out->h2d_bytes = c->h2d_bytes;
+    out->d2h_bytes = c->d2h_bytes;
+    out->enum_launches = c->enum_launches;
+    out->eval_launches = c->eval_launches;
+    out->enum_ms = out->eval_ms = 0;
+    for (int i = 0; i + 1 < c->nkev; i++) {
+        float t = 0;
+        cudaEventElapsedTime(&t, c->kev[i], c->kev[i + 1]);
+        if (i % 2 == 0) out->enum_ms += t;
+        else out->eval_ms += t;
+    }
+    if (out->nodes) memcpy(out->nodes, r->nodes, sizeof(mpdp_plan_node) * r->n_nodes);
+    for (int k = 0; k <= n; k++) {
+        if (out->level_csg) out->level_csg[k] = r->lvl_csg[k];
+        if (out->level_ccp) out->level_ccp[k] = r->lvl_ccp[k];
+        if (out->level_pairs) out->level_pairs[k] = r->lvl_pairs[k];
+    }
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, mpdp_result* out) {
+    if (!c) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!out) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "out is NULL");
+    switch (algo) {
+        case MPDP_ALGO_MPDP:
+            if (k != 0) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "k must be 0 for MPDP");
+            break;
+        case MPDP_ALGO_DPSIZE_REF:
+            return fail(c, MPDP_ERR_UNSUPPORTED,
+                        "DPSIZE_REF is the CPU reference; it lives in the test oracle (oracle/liboracle.so), "
+                        "not in this GPU library");
+        case MPDP_ALGO_IDP2_MPDP:
+        case MPDP_ALGO_UNIONDP_MPDP:
+            return fail(c, MPDP_ERR_UNSUPPORTED, "IDP2/UnionDP drivers are not built yet");
+        default:
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "unknown algorithm");
+    }
+    mpdp_status st = mpdp_stage(c, g);
+    if (st != MPDP_OK) return st;
+    st = mpdp_run(c);
+    if (st != MPDP_OK) return st;
+    return mpdp_fetch(c, out);
+}
+
+mpdp_status mpdp_nccl_get_unique_id(void* out128) {
+    if (!out128) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "out is NULL");
+    return fail(nullptr, MPDP_ERR_UNSUPPORTED, "multi-GPU contexts are not enabled in this build");
+}
+
+}  // extern "C"

@@ -1,0 +1,263 @@
+"""Thin ctypes binding of include/mpdp.h (argument marshalling only).
+
+Every step of the DP runs in the CUDA kernels of libmpdp.so; there is no CPU
+path.  If the shared library is missing or no CUDA device is present, the
+calls raise instead of falling back.  PyTorch is used for plumbing only: the
+workspace is a torch CUDA tensor and the context runs on torch's current
+stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmpdp.so")
+
+# mpdp_status
+OK, ERR_INVALID_ARGUMENT, ERR_DISCONNECTED, ERR_CAPACITY, ERR_TIMEOUT, ERR_OOM, \
+    ERR_CUDA, ERR_NCCL, ERR_INTERNAL, ERR_UNSUPPORTED = range(10)
+# mpdp_algo
+ALGOS = {"DPSIZE_REF": 0, "MPDP": 1, "IDP2_MPDP": 2, "UNIONDP_MPDP": 3}
+
+
+class mpdp_query_graph(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("cardinalities", C.POINTER(C.c_double)),
+                ("n_edges", C.c_uint32), ("edges", C.POINTER(C.c_uint32)),
+                ("selectivities", C.POINTER(C.c_double)),
+                ("leaf_costs", C.POINTER(C.c_double))]
+
+
+class mpdp_plan_node(C.Structure):
+    _fields_ = [("left", C.c_int32), ("right", C.c_int32), ("relation", C.c_int32),
+                ("reserved", C.c_uint32), ("set", C.c_uint64),
+                ("cardinality", C.c_double), ("cost", C.c_double)]
+
+
+class mpdp_result(C.Structure):
+    _fields_ = [("nodes", C.POINTER(mpdp_plan_node)), ("capacity", C.c_uint32),
+                ("n_nodes", C.c_uint32), ("root", C.c_uint32), ("gpu_launches", C.c_uint32),
+                ("cost", C.c_double), ("pairs_evaluated", C.c_uint64),
+                ("ccp_pairs", C.c_uint64), ("csg_count", C.c_uint64),
+                ("level_csg", C.POINTER(C.c_uint64)), ("level_ccp", C.POINTER(C.c_uint64)),
+                ("level_pairs", C.POINTER(C.c_uint64)), ("time_ms", C.c_double),
+                ("probes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("enum_ms", C.c_double), ("eval_ms", C.c_double),
+                ("enum_launches", C.c_uint32), ("eval_launches", C.c_uint32)]
+
+
+class mpdp_ctx_config(C.Structure):
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+                ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p),
+                ("mem_budget_bytes", C.c_uint64), ("timeout_ms", C.c_double),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_uint64),
+                ("flags", C.c_uint32), ("load_factor", C.c_double)]
+
+FLAG_FORCE_WIDE_MASKS = 1
+FLAG_PROFILE_KERNELS = 2
+
+
+EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",
+           "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
+           "mpdp_nccl_get_unique_id", "mpdp_share"]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libmpdp.so (raises OSError if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(path)
+    P = C.c_void_p
+    sig = {
+        "mpdp_ctx_create": (C.c_int, [C.POINTER(mpdp_ctx_config), C.POINTER(P)]),
+        "mpdp_ctx_destroy": (C.c_int, [P]),
+        "mpdp_optimize": (C.c_int, [P, C.POINTER(mpdp_query_graph), C.c_int, C.c_uint32,
+                                    C.POINTER(mpdp_result)]),
+        "mpdp_stage": (C.c_int, [P, C.POINTER(mpdp_query_graph)]),
+        "mpdp_run": (C.c_int, [P]),
+        "mpdp_fetch": (C.c_int, [P, C.POINTER(mpdp_result)]),
+        "mpdp_last_error": (C.c_char_p, [P]),
+        "mpdp_status_string": (C.c_char_p, [C.c_int]),
+        "mpdp_abi_version": (C.c_int, []),
+        "mpdp_nccl_get_unique_id": (C.c_int, [P]),
+        "mpdp_share": (None, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64),
+                              C.POINTER(C.c_uint64)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+class MPDPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        name = load_library().mpdp_status_string(status).decode()
+        super().__init__(f"{name}: {msg}")
+        self.status = status
+
+
+@dataclass
+class PlanNode:
+    left: int
+    right: int
+    relation: int
+    set: int
+    cardinality: float
+    cost: float
+
+
+@dataclass
+class Result:
+    cost: float
+    nodes: List[PlanNode]
+    pairs_evaluated: int
+    ccp_pairs: int
+    csg_count: int
+    level_csg: List[int]
+    level_ccp: List[int]
+    level_pairs: List[int]
+    time_ms: float
+    gpu_launches: int
+    probes: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    enum_ms: float = 0.0
+    eval_ms: float = 0.0
+    enum_launches: int = 0
+    eval_launches: int = 0
+
+    def tree(self):
+        """Nested tuples: leaves are relation ids, internal nodes (left, right)."""
+        def rec(i):
+            x = self.nodes[i]
+            return x.relation if x.relation >= 0 else (rec(x.left), rec(x.right))
+        return rec(len(self.nodes) - 1) if self.nodes else None
+
+
+class GraphArgs:
+    """Marshals a workload.QueryGraph-like object (n, card, edges, sel, leaf_cost)."""
+
+    def __init__(self, g):
+        n, m = g.n, len(g.edges)
+        self.card = (C.c_double * n)(*g.card)
+        self.edges = (C.c_uint32 * max(1, 2 * m))(*[x for e in g.edges for x in e])
+        self.sel = (C.c_double * max(1, m))(*g.sel)
+        lc = getattr(g, "leaf_cost", None)
+        self.leaf = (C.c_double * n)(*lc) if lc is not None else None
+        self.s = mpdp_query_graph(n, self.card, m, self.edges, self.sel, self.leaf)
+        self.n = n
+
+    def ref(self):
+        return C.byref(self.s)
+
+
+class ResultBuf:
+    def __init__(self, n: int):
+        self.n = n
+        self.nodes = (mpdp_plan_node * (2 * n - 1))()
+        self.lc = (C.c_uint64 * (n + 1))()
+        self.lx = (C.c_uint64 * (n + 1))()
+        self.lp = (C.c_uint64 * (n + 1))()
+        self.s = mpdp_result(self.nodes, 2 * n - 1)
+        self.s.level_csg, self.s.level_ccp, self.s.level_pairs = self.lc, self.lx, self.lp
+
+    def ref(self):
+        return C.byref(self.s)
+
+    def to_result(self) -> Result:
+        r = self.s
+        nodes = [PlanNode(x.left, x.right, x.relation, x.set, x.cardinality, x.cost)
+                 for x in self.nodes[:r.n_nodes]]
+        return Result(r.cost, nodes, r.pairs_evaluated, r.ccp_pairs, r.csg_count,
+                      list(self.lc), list(self.lx), list(self.lp), r.time_ms, r.gpu_launches,
+                      r.probes, r.h2d_bytes, r.d2h_bytes, r.enum_ms, r.eval_ms,
+                      r.enum_launches, r.eval_launches)
+
+
+class Context:
+    """One mpdp_ctx on one GPU.  The workspace is a torch uint8 CUDA tensor
+    (torch = device-memory plumbing); the context runs on torch's current stream."""
+
+    def __init__(self, device: int = 0, workspace_bytes: int = 4 << 30, timeout_ms: float = 0.0,
+                 use_torch: bool = True, stream: Optional[int] = None, flags: int = 0,
+                 load_factor: float = 0.0):
+        L = load_library()
+        self._ws = None
+        self.stream = None
+        ws_ptr, stream_ptr = None, stream
+        if use_torch:
+            import torch
+            if not torch.cuda.is_available():
+                raise MPDPError(ERR_CUDA, "no CUDA device (this library has no CPU path)")
+            torch.cuda.set_device(device)
+            self._ws = torch.empty(workspace_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+            torch.cuda.synchronize(device)
+            ws_ptr = self._ws.data_ptr()
+            if stream_ptr is None:
+                # a dedicated torch stream (the legacy default stream's handle is 0,
+                # which the C ABI reads as "create your own")
+                self.stream = torch.cuda.Stream(device=device)
+                stream_ptr = self.stream.cuda_stream
+        cfg = mpdp_ctx_config(device, 0, 1, None, stream_ptr, workspace_bytes, timeout_ms,
+                              ws_ptr, workspace_bytes if ws_ptr else 0, flags, load_factor)
+        h = C.c_void_p()
+        st = L.mpdp_ctx_create(C.byref(cfg), C.byref(h))
+        if st != OK:
+            raise MPDPError(st, L.mpdp_last_error(None).decode())
+        self.h = h
+        self.L = L
+
+    def _check(self, st):
+        if st != OK:
+            raise MPDPError(st, self.L.mpdp_last_error(self.h).decode())
+
+    def mpdp_optimize(self, g, algo: str = "MPDP", k: int = 0) -> Result:
+        ga, rb = GraphArgs(g), ResultBuf(g.n)
+        self._check(self.L.mpdp_optimize(self.h, ga.ref(), ALGOS[algo], k, rb.ref()))
+        return rb.to_result()
+
+    optimize = mpdp_optimize
+
+    def mpdp_stage(self, g):
+        self._ga = GraphArgs(g)
+        self._check(self.L.mpdp_stage(self.h, self._ga.ref()))
+
+    def mpdp_run(self):
+        self._check(self.L.mpdp_run(self.h))
+
+    def mpdp_fetch(self) -> Result:
+        rb = ResultBuf(self._ga.n)
+        self._check(self.L.mpdp_fetch(self.h, rb.ref()))
+        return rb.to_result()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.mpdp_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def mpdp_share(total: int, rank: int, world: int):
+    lo, hi = C.c_uint64(), C.c_uint64()
+    load_library().mpdp_share(total, rank, world, C.byref(lo), C.byref(hi))
+    return lo.value, hi.value
