@@ -123,6 +123,9 @@ typedef struct {
 #define MPDP_FLAG_FORCE_WIDE_MASKS 1u
 /* flags: record CUDA events around every level kernel (enum_ms / eval_ms)      */
 #define MPDP_FLAG_PROFILE_KERNELS 2u
+/* flags: use the Murmur3 open-addressing memo even where the perfect-hash
+ * (colex-rank) memo applies (n <= 32); for ablations                           */
+#define MPDP_FLAG_HASH_MEMO 4u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

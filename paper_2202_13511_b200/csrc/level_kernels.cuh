@@ -1,18 +1,18 @@
 // level_kernels.cuh — the per-level kernels of the MPDP dynamic program
 // (Alg. mpdp_gpu) for sm_100a.
 //
-//   k_enum<M,CLS>    unrank (colex + Gosper) -> connectivity
-//                    filter (grow from the lowest vertex) -> set
-//                    kind + join-pair count -> stream compaction into a light
-//                    list (<= 32 pairs: thread per set) and a heavy list, with
-//                    a single-pass decoupled look-back scan.
-//   k_eval<M,CLS>    evaluate MPDP's join pairs (Alg. mpdp_generalization
-//                    P:531-579), C_out cost with memo probes, per-set
-//                    min (prune fused into evaluate) and scatter into
-//                    the level's open-addressing memo.
-//   k_extract<M>     plan extraction from the memo + counters.
+//   k_enum<M,CLS>          unrank (colex + Gosper) -> connectivity
+//                          filter (grow from the lowest vertex) ->
+//                          set kind + join-pair count -> stream compaction into a
+//                          light list (<= 32 pairs: thread per set) and a heavy
+//                          list, single-pass decoupled look-back scan.
+//   k_eval_light/heavy     evaluate MPDP's join pairs (Alg.
+//                          mpdp_generalization P:531-579), C_out cost
+//                          from memo probes, per-set min (prune fused into
+//                          evaluate), scatter into the memo.
+//   k_extract<M,MEMO>      plan extraction from the memo + counters.
 #pragma once
-#include "dev_graph.cuh"
+#include "memo.cuh"
 #include "../../include/mpdp.h"
 
 namespace mpdp {
@@ -23,7 +23,7 @@ struct __align__(16) LevelDesc {
     unsigned long long n_items;            // heavy work items of `item` pairs
     unsigned long long pairs, ccp;         // counters (R3, R2)
     unsigned long long probes;             // memo probes of non-singleton sets
-    unsigned long long bucket_off, n_buckets;   // this level's memo table
+    unsigned long long bucket_off, n_buckets;   // HASH: this level's table
     unsigned int tile_ticket, work_ticket, pad0, pad1;
 };
 
@@ -32,8 +32,6 @@ struct __align__(64) TileRec {            // decoupled look-back record (ring sl
     unsigned long long agg_l, agg_h, agg_w;
     unsigned long long inc_l, inc_h, inc_w, pad;
 };
-
-enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u };
 
 struct ResultDev {
     double cost;
@@ -46,14 +44,13 @@ struct ResultDev {
 template <typename M> struct Params {
     const QueryDev<M>* q;
     LevelDesc* desc;                       // [kMaxN + 1], indexed by subset size
-    Bucket* arena;                         // memo tables of every level, bump-allocated
-    M* cold;                               // left(S) per slot (2 per bucket)
-    unsigned long long arena_buckets;
+    MemoPtrs memo;
+    unsigned long long dense_off[kMaxN + 1];   // DENSE: first entry of level j
     M* light;                              // compacted level lists (reused per level)
     M* heavy;
-    unsigned long long* wh;                // [list_cap + 1] exclusive heavy pair prefix
-    Key* bkey;                             // [list_cap] cross-warp (cost, left) min
-    unsigned long long* bdone;             // [list_cap] pairs merged so far
+    unsigned long long* wh;                // [heavy_cap + 1] exclusive heavy pair prefix
+    Key* bkey;                             // [heavy_cap] cross-warp (cost, left) min
+    unsigned long long* bdone;             // [heavy_cap] pairs merged so far
     unsigned int* first_heavy;             // [fh_cap] heavy set holding item i's first pair
     unsigned long long fh_cap;
     TileRec* tiles;                        // ring of look-back records
@@ -62,9 +59,9 @@ template <typename M> struct Params {
     unsigned long long heavy_cap;          // heavy list capacity
     ResultDev* result;
     unsigned long long epoch;              // look-back epoch base (unique per query)
-    unsigned int gen;                      // memo tag of this query
     int n;
-    double inv_load;                       // buckets = ceil(count * inv_load / 2)
+    int memo_kind;                         // MEMO_HASH / MEMO_DENSE
+    double inv_load;                       // HASH: buckets = ceil(count * inv_load / 2)
 };
 
 // ------------------------------------------------------------- mem helpers
@@ -82,110 +79,35 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// --------------------------------------------------------------- memo I/O
-struct Tabs {                              // per-level table geometry in smem
-    unsigned long long off[kMaxN + 1];
-    unsigned long long nb[kMaxN + 1];
-};
-
-// One memo bucket = one 32-byte L2 sector, fetched with a single 256-bit
-// read-only load (LDG.E.ENL2.256): tables of earlier levels are immutable
-// while level k is evaluated.
-struct B4 {
-    unsigned long long k0, c0, k1, c1;
-};
-__device__ __forceinline__ B4 ld_bucket(const Bucket* b) {
-    B4 r;
-    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
-                 : "=l"(r.k0), "=l"(r.c0), "=l"(r.k1), "=l"(r.c1)
-                 : "l"(b));
-    return r;
-}
-
-// Continue a linear probe after the home bucket (rare at load factor 0.5).
-template <typename M>
-__device__ __noinline__ double probe_tail(const Params<M>& p, const Tabs& t, M T, int j, unsigned long long b,
-                                          unsigned long long* slot_out) {
-    const unsigned long long want = Tag<M>::make(T, p.gen);
-    const unsigned int g = Tag<M>::gen_of(want);
-    const unsigned long long nb = t.nb[j];
-    B4 x = ld_bucket(p.arena + t.off[j] + b);
-    for (unsigned long long guard = 0; guard < nb; guard++) {
-        if (x.k0 == want) {
-            if (slot_out) *slot_out = (t.off[j] + b) * 2;
-            return __longlong_as_double((long long)x.c0);
-        }
-        if (x.k1 == want) {
-            if (slot_out) *slot_out = (t.off[j] + b) * 2 + 1;
-            return __longlong_as_double((long long)x.c1);
-        }
-        if (Tag<M>::gen_of(x.k0) != g || Tag<M>::gen_of(x.k1) != g) break;   // empty slot: absent
-        b = (b + 1 == nb) ? 0 : b + 1;
-        x = ld_bucket(p.arena + t.off[j] + b);
-    }
-    atomicOr(&p.result->error, ERR_PROBE);
-    return __longlong_as_double(0x7ff8000000000000ll);
-}
-
-// cost(T) for one set (extraction path): leaf or probe of the level-|T| table.
-template <typename M>
-__device__ __forceinline__ double probe(const Params<M>& p, const Tabs& t, M T, int j,
-                                        unsigned long long* slot_out = nullptr) {
-    return probe_tail(p, t, T, j, fastrange(fmix(T), t.nb[j]), slot_out);
-}
-
-// Batched cost lookup: all home-bucket loads of the batch are issued before any
-// is consumed, so each thread keeps up to NP probes in flight.
-template <typename M, int NP>
-__device__ __forceinline__ void lookup_batch(const Params<M>& p, const SQ<M>& q, const Tabs& t, const M (&X)[NP],
-                                             unsigned valid, double (&c)[NP], unsigned long long& nprobe) {
-    B4 bk[NP];
-    unsigned long long bi[NP];
-    int jj[NP];
-#pragma unroll
-    for (int i = 0; i < NP; i++) {
-        jj[i] = popc(X[i]);
-        bi[i] = 0;
-        if (((valid >> i) & 1) && jj[i] > 1) {
-            bi[i] = fastrange(fmix(X[i]), t.nb[jj[i]]);
-            bk[i] = ld_bucket(p.arena + t.off[jj[i]] + bi[i]);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < NP; i++) {
-        c[i] = 0.0;
-        if (!((valid >> i) & 1)) continue;
-        if (jj[i] == 1) {
-            c[i] = q.leaf[ctz(X[i])];
-            continue;
-        }
-        nprobe++;
-        const unsigned long long want = Tag<M>::make(X[i], p.gen);
-        if (bk[i].k0 == want) c[i] = __longlong_as_double((long long)bk[i].c0);
-        else if (bk[i].k1 == want) c[i] = __longlong_as_double((long long)bk[i].c1);
-        else c[i] = probe_tail(p, t, X[i], jj[i], bi[i], nullptr);
-    }
-}
-
-// Collects join pairs (A, B) of one set and evaluates them four at a time:
-// cost = (cost(A) + cost(B)) + card(S) (C_out; no FMA, reading R6) and
-// the lexicographic (cost, min(A, B)) minimum (reading R7).
-template <typename M>
+// ------------------------------------------------------------ pair sink
+// Collects the join pairs (A, B) of one set and evaluates them NP at a time:
+// cost = (cost(A) + cost(B)) + card(S) (C_out; no FMA, reading R6),
+// keeping the lexicographic (cost, min(A, B)) minimum (reading R7).
+template <typename M, int MEMO>
 struct PairSink {
-    static constexpr int NP = kSinkPairs;
+    static constexpr int NP = (MEMO == MEMO_DENSE) ? 4 : 2;
+    const MemoPtrs* P;
+    const MemoView* v;
+    const unsigned int* rtab;
+    const SQ<M>* q;
     M A[NP], B[NP];
     int cnt;
     double cS;
     Key best;
     unsigned long long nprobe;
 
-    __device__ __forceinline__ void init(double card) {
+    __device__ __forceinline__ void init(const MemoPtrs* P_, const MemoView* v_, const unsigned int* rt,
+                                         const SQ<M>* q_, double card) {
+        P = P_;
+        v = v_;
+        rtab = rt;
+        q = q_;
         cnt = 0;
         cS = card;
         best = key_inf();
         nprobe = 0;
     }
-    __device__ __forceinline__ void flush(const Params<M>& p, const SQ<M>& q, const Tabs& t) {
+    __device__ __forceinline__ void flush() {
         if (!cnt) return;
         M X[2 * NP];
         unsigned valid = 0;
@@ -196,19 +118,19 @@ struct PairSink {
             if (u < cnt) valid |= 3u << (2 * u);
         }
         double c[2 * NP];
-        lookup_batch<M, 2 * NP>(p, q, t, X, valid, c, nprobe);
+        memo_lookup<M, MEMO, 2 * NP>(*P, *v, rtab, *q, X, valid, c, nprobe);
 #pragma unroll
         for (int u = 0; u < NP; u++) {
             if (u < cnt) {
-                const double v = __dadd_rn(__dadd_rn(c[2 * u], c[2 * u + 1]), cS);
-                const Key key{(unsigned long long)__double_as_longlong(v),
+                const double x = __dadd_rn(__dadd_rn(c[2 * u], c[2 * u + 1]), cS);
+                const Key key{(unsigned long long)__double_as_longlong(x),
                               (unsigned long long)(A[u] < B[u] ? A[u] : B[u])};
                 if (key_less(key, best)) best = key;
             }
         }
         cnt = 0;
     }
-    __device__ __forceinline__ void add(const Params<M>& p, const SQ<M>& q, const Tabs& t, M a, M b) {
+    __device__ __forceinline__ void add(M a, M b) {
 #pragma unroll
         for (int u = NP - 1; u > 0; u--) {
             A[u] = A[u - 1];
@@ -216,38 +138,9 @@ struct PairSink {
         }
         A[0] = a;
         B[0] = b;
-        if (++cnt == NP) flush(p, q, t);
+        if (++cnt == NP) flush();
     }
 };
-
-// scatter (S, best) into the level-k table: claim a slot by CAS on
-// its tagged key, then store the cost and the cold `left` mask.
-template <typename M>
-__device__ __forceinline__ void memo_insert(const Params<M>& p, unsigned long long off,
-                                            unsigned long long nb, M S, const Key& best) {
-    const unsigned long long want = Tag<M>::make(S, p.gen);
-    const unsigned int g = Tag<M>::gen_of(want);
-    Bucket* base = p.arena + off;
-    unsigned long long b = fastrange(fmix(S), nb);
-    for (unsigned long long guard = 0; guard < nb; guard++) {
-#pragma unroll
-        for (int s = 0; s < 2; s++) {
-            unsigned long long* kp = &base[b].s[s].key;
-            unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(kp);
-            while (Tag<M>::gen_of(cur) != g) {
-                const unsigned long long old = atomicCAS(kp, cur, want);
-                if (old == cur) {
-                    base[b].s[s].cost = __longlong_as_double((long long)best.c);
-                    p.cold[(off + b) * 2 + s] = (M)best.l;
-                    return;
-                }
-                cur = old;
-            }
-        }
-        b = (b + 1 == nb) ? 0 : b + 1;
-    }
-    atomicOr(&p.result->error, ERR_TABLE_FULL);
-}
 
 // ------------------------------------------------------------ k_init
 template <typename M>
@@ -439,11 +332,15 @@ __global__ void __launch_bounds__(kBlock) k_enum(Params<M> p, int k, unsigned lo
             if (d.n_items > p.fh_cap) atomicOr(&p.result->error, ERR_ITEMS);
             if (H < p.heavy_cap + 1) p.wh[H] = W;
             const unsigned long long cnt = L + H;
-            if (L > p.list_cap || H > p.heavy_cap) atomicOr(&p.result->error, ERR_CAPACITY);
-            unsigned long long nbk = (unsigned long long)ceil((double)cnt * p.inv_load * 0.5);
-            if (nbk < 1) nbk = 1;
-            const unsigned long long off = (k <= 2) ? 0ull : p.desc[k - 1].bucket_off + p.desc[k - 1].n_buckets;
-            if (off + nbk > p.arena_buckets || L > p.list_cap || H > p.heavy_cap) {
+            bool over = L > p.list_cap || H > p.heavy_cap;
+            unsigned long long nbk = 1, off = 0;
+            if (p.memo_kind == MEMO_HASH) {     // size this level's table from the exact count
+                nbk = (unsigned long long)ceil((double)cnt * p.inv_load * 0.5);
+                if (nbk < 1) nbk = 1;
+                off = (k <= 2) ? 0ull : p.desc[k - 1].bucket_off + p.desc[k - 1].n_buckets;
+                over = over || off + nbk > p.memo.arena_buckets;
+            }
+            if (over) {
                 atomicOr(&p.result->error, ERR_CAPACITY);
                 nbk = 0;
             }
@@ -486,20 +383,9 @@ __global__ void __launch_bounds__(kBlock) k_enum(Params<M> p, int k, unsigned lo
 }
 
 // ------------------------------------------------------------ k_eval
-// Evaluate pairs j in [j0, j1) of connected set S (|S| = k) into the sink.
-// Pair numbering per kind:
-//   KIND_TREE, CLS_TREE : j -> j-th vertex v of S below the set's top vertex;
-//                         the pair is (S n subtree(v), rest)   [edge (v, parent v)]
-//   KIND_TREE, general  : j -> j-th induced edge (v, u), v < u; sides by grow
-//   KIND_COMPLETE       : j -> lb = {min S} u deposit(j, S \ min S)
-//   KIND_BLOCKS         : blocks in DFS order, per block j -> lb = {min B} u
-//                         deposit(j, B \ min B); CCP check inside the block
-//                         unless the block is complete (Lemma generic:opt);
-//                         S_left = grow(lb, S \ rb), S_right = S \ S_left
-template <typename M, int CLS>
-__device__ void eval_range(const Params<M>& p, const SQ<M>& q, const Tabs& t, M S, int k, int kind,
-                           unsigned long long j0, unsigned long long j1, PairSink<M>& sink,
-                           unsigned long long& nccp) {
+template <typename M, int CLS, typename Sink>
+__device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long long j0, unsigned long long j1,
+                           Sink& sink, unsigned long long& nccp) {
     if (j0 >= j1) return;
     if (kind == KIND_TREE) {
         if (CLS == CLS_TREE) {
@@ -517,7 +403,7 @@ __device__ void eval_range(const Params<M>& p, const SQ<M>& q, const Tabs& t, M 
                 const int v = ctz(Mv);
                 Mv &= Mv - 1;
                 const M A = S & q.desc[v];
-                sink.add(p, q, t, A, S ^ A);
+                sink.add(A, S ^ A);
             }
         } else if (CLS == CLS_GENERAL) {
             unsigned long long j = 0;
@@ -533,7 +419,7 @@ __device__ void eval_range(const Params<M>& p, const SQ<M>& q, const Tabs& t, M 
                     if (j < j0) continue;
                     const int u = ctz(U);
                     const M A = grow(q, bitm<M>(v), S & ~bitm<M>(u));
-                    sink.add(p, q, t, A, S ^ A);
+                    sink.add(A, S ^ A);
                 }
             }
         }
@@ -546,7 +432,7 @@ __device__ void eval_range(const Params<M>& p, const SQ<M>& q, const Tabs& t, M 
         M sub = deposit<M>(j0, R);
         for (unsigned long long j = j0; j < j1; j++) {
             const M A = lo | sub;
-            sink.add(p, q, t, A, S ^ A);
+            sink.add(A, S ^ A);
             sub = (sub - R) & R;
         }
         nccp += j1 - j0;
@@ -575,23 +461,38 @@ __device__ void eval_range(const Params<M>& p, const SQ<M>& q, const Tabs& t, M 
             if (!complete && !(connected(q, lb) && connected(q, rb))) continue;   // CCP block
             nccp++;
             const M A = grow(q, lb, S & ~rb);
-            sink.add(p, q, t, A, S ^ A);                                        // S_right = S \ S_left
+            sink.add(A, S ^ A);                                        // S_right = S \ S_left
         }
         base += wb;
     }
 }
 
-// Shared prologue of the evaluate kernels: the query, the geometry of every
-// lower level's memo table and this level's descriptor go to shared memory.
-template <typename M>
-__device__ __forceinline__ void eval_prologue(const Params<M>& p, int k, SQ<M>& q, Tabs& t, LevelDesc& d) {
+// Shared prologue of the evaluate / extract kernels: the query, the memo view
+// (per-level table geometry) and, for DENSE, the rank tables go to shared memory.
+template <typename M, int MEMO>
+__device__ __forceinline__ void memo_prologue(const Params<M>& p, int kmax, SQ<M>& q, MemoView& v,
+                                              unsigned int* rtab) {
     load_query(q, p.q);
-    for (int j = threadIdx.x; j <= k; j += blockDim.x) {
-        t.off[j] = (j >= 2) ? p.desc[j].bucket_off : 0;
-        t.nb[j] = (j >= 2) ? p.desc[j].n_buckets : 0;
+    for (int j = threadIdx.x; j <= kmax; j += blockDim.x) {
+        if (MEMO == MEMO_DENSE) {
+            v.off[j] = p.dense_off[j];
+            v.nb[j] = 0;
+        } else {
+            v.off[j] = (j >= 2) ? p.desc[j].bucket_off : 0;
+            v.nb[j] = (j >= 2) ? p.desc[j].n_buckets : 0;
+        }
     }
-    if (threadIdx.x == 0) d = p.desc[k];
-    __syncthreads();
+    if (MEMO == MEMO_DENSE) {
+        const RankGeom g = rank_geom(p.n);
+        if (threadIdx.x == 0) {
+            for (int c = 0; c < kRankChunks; c++) {
+                v.rbase[c] = g.base[c];
+                v.rlen[c] = g.len[c];
+            }
+            v.nch = g.nch;
+        }
+        for (unsigned int i = threadIdx.x; i < g.entries; i += blockDim.x) rtab[i] = p.memo.rank_tab[i];
+    }
 }
 
 __device__ __forceinline__ void flush_counters(LevelDesc* dk, unsigned long long pairs, unsigned long long nccp,
@@ -608,13 +509,16 @@ __device__ __forceinline__ void flush_counters(LevelDesc* dk, unsigned long long
 
 // Light sets (<= kLightMax join pairs): one thread evaluates a whole set, keeps
 // its min in registers and scatters it (prune fused into evaluate).
-template <typename M, int CLS>
+template <typename M, int CLS, int MEMO>
 __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Params<M> p, int k) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
-    __shared__ Tabs t;
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
+    __shared__ MemoView v;
     __shared__ LevelDesc d;
-    eval_prologue(p, k, q, t, d);
+    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    if (threadIdx.x == 0) d = p.desc[k];
+    __syncthreads();
     if (d.n_buckets == 0) return;          // capacity error already flagged
     unsigned long long pairs = 0, nccp = 0, nprobe = 0;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -626,13 +530,13 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Par
             const M S = p.light[i];
             unsigned long long w;
             const int kind = set_kind<M, CLS>(q, S, k, w);
-            PairSink<M> sink;
-            sink.init(card_of(q, S));
-            eval_range<M, CLS>(p, q, t, S, k, kind, 0, w, sink, nccp);
-            sink.flush(p, q, t);
+            PairSink<M, MEMO> sink;
+            sink.init(&p.memo, &v, rtab, &q, card_of(q, S));
+            eval_range<M, CLS>(q, S, k, kind, 0, w, sink, nccp);
+            sink.flush();
             nprobe += sink.nprobe;
             pairs += w;
-            memo_insert(p, d.bucket_off, d.n_buckets, S, sink.best);
+            memo_insert<M, MEMO>(p.memo, v, rtab, k, S, sink.best);
         }
     }
     flush_counters(&p.desc[k], pairs, nccp, nprobe);
@@ -642,13 +546,16 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Par
 // claim groups of items dynamically, evaluate lane-contiguous chunks, reduce
 // with shuffles, and merge split sets through a 128-bit CAS min + a pair
 // counter (the last contributor scatters the set).
-template <typename M, int CLS>
+template <typename M, int CLS, int MEMO>
 __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, unsigned long long item) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
-    __shared__ Tabs t;
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
+    __shared__ MemoView v;
     __shared__ LevelDesc d;
-    eval_prologue(p, k, q, t, d);
+    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    if (threadIdx.x == 0) d = p.desc[k];
+    __syncthreads();
     if (d.n_buckets == 0 || d.n_items == 0) return;
     const int lane = threadIdx.x & 31;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
@@ -672,21 +579,21 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
             const M S = p.heavy[h];
             unsigned long long wk;
             const int kind = set_kind<M, CLS>(q, S, k, wk);
-            PairSink<M> sink;
-            sink.init(card_of(q, S));
+            PairSink<M, MEMO> sink;
+            sink.init(&p.memo, &v, rtab, &q, card_of(q, S));
             // lane-contiguous chunks of the segment [a, b)
             const unsigned long long cnt = b - a, per = (cnt + 31) >> 5;
             unsigned long long j0 = a + per * lane, j1 = j0 + per;
             if (j0 > b) j0 = b;
             if (j1 > b) j1 = b;
-            eval_range<M, CLS>(p, q, t, S, k, kind, j0, j1, sink, nccp);
-            sink.flush(p, q, t);
+            eval_range<M, CLS>(q, S, k, kind, j0, j1, sink, nccp);
+            sink.flush();
             nprobe += sink.nprobe;
             const Key best = warp_min(sink.best);
             if (lane == 0) {
                 pairs += cnt;
                 if (a == 0 && b == w) {
-                    memo_insert(p, d.bucket_off, d.n_buckets, S, best);
+                    memo_insert<M, MEMO>(p.memo, v, rtab, k, S, best);
                 } else {
                     atomic_key_min(&p.bkey[h], best);
                     __threadfence();
@@ -695,7 +602,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
                         __threadfence();
                         const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&p.bkey[h]);
                         const Key fin{ld_relaxed(kp), ld_relaxed(kp + 1)};
-                        memo_insert(p, d.bucket_off, d.n_buckets, S, fin);
+                        memo_insert<M, MEMO>(p.memo, v, rtab, k, S, fin);
                     }
                 }
             }
@@ -706,17 +613,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
 
 // ------------------------------------------------------------ k_extract
 // One thread walks the memo from the full set: left(S) from the
-// cold array, right = S \ left; nodes in post-order, root last.
-template <typename M>
+// memo, right = S \ left; nodes in post-order, root last.
+template <typename M, int MEMO>
 __global__ void k_extract(Params<M> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
-    __shared__ Tabs t;
-    load_query(q, p.q);
-    for (int j = threadIdx.x; j <= kMaxN; j += blockDim.x) {
-        t.off[j] = (j >= 2 && j <= p.n) ? p.desc[j].bucket_off : 0;
-        t.nb[j] = (j >= 2 && j <= p.n) ? p.desc[j].n_buckets : 0;
-    }
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
+    __shared__ MemoView v;
+    memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
     __syncthreads();
     if (threadIdx.x != 0) return;
     ResultDev* r = p.result;
@@ -735,10 +639,10 @@ __global__ void k_extract(Params<M> p) {
         pairs += d.pairs;
         probes += d.probes;
     }
-    r->probes = probes;
     r->csg = csg;
     r->ccp = ccp;
     r->pairs = pairs;
+    r->probes = probes;
     if (r->error) {
         r->n_nodes = 0;
         return;
@@ -756,21 +660,20 @@ __global__ void k_extract(Params<M> p) {
         const int top = sp - 1;
         const M S = st_set[top];
         if (popc(S) == 1) {
-            const int v = ctz(S);
+            const int vtx = ctz(S);
             mpdp_plan_node& nd = r->nodes[nn];
             nd.left = nd.right = -1;
-            nd.relation = v;
+            nd.relation = vtx;
             nd.reserved = 0;
             nd.set = (unsigned long long)S;
-            nd.cardinality = q.card[v];
-            nd.cost = q.leaf[v];
+            nd.cardinality = q.card[vtx];
+            nd.cost = q.leaf[vtx];
             last = nn++;
             --sp;
             continue;
         }
-        unsigned long long slot = 0;
-        const double c = probe(p, t, S, popc(S), &slot);
-        const M L = p.cold[slot];
+        M L;
+        const double c = memo_get<M, MEMO>(p.memo, v, rtab, S, L);
         if (st_state[top] == 0) {
             st_state[top] = 1;
             st_set[sp] = L;

@@ -26,8 +26,9 @@ namespace {
 thread_local std::string g_tls_error;
 
 struct DevLayout {
-    size_t query = 0, desc = 0, result = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
-           fh = 0, arena = 0, cold = 0, end = 0;
+    size_t query = 0, desc = 0, result = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
+           fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
+    int memo_kind = MEMO_HASH;
     unsigned long long list_cap = 0, heavy_cap = 0, tiles_cap = 0, fh_cap = 0, arena_buckets = 0;
 };
 
@@ -60,9 +61,13 @@ struct mpdp_ctx {
     unsigned int launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool ran = false;
-    int occ[2][3][3] = {};               // [wide][class][enum, light, heavy]
+    int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
+    int occ_n[2][3][2] = {};
     unsigned int flags = 0;
     double load_factor = 0.5;
+    int last_memo = -1;
+    int rank_n = -1;                      // n the uploaded rank tables were built for
+    std::vector<unsigned int> h_rank;
     cudaEvent_t kev[2 * kMaxN + 2] = {};  // MPDP_FLAG_PROFILE_KERNELS: around every level kernel
     int nkev = 0;
     unsigned int enum_launches = 0, eval_launches = 0;
@@ -239,12 +244,25 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.query = take(sizeof(QueryDev<uint64_t>));
     L.desc = take(sizeof(LevelDesc) * (kMaxN + 1));
     L.result = take(sizeof(ResultDev));
+    L.rank = take(sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25));
     off = align_up(off, 256);
     if (off + (64u << 20) > c->ws_bytes) return fail(c, MPDP_ERR_CAPACITY, "workspace smaller than 64 MiB");
     const size_t body = c->ws_bytes - off - 1024;
-    const unsigned long long buckets = (unsigned long long)((body * 3 / 4) / (sizeof(Bucket) + 2 * msz));
+    const size_t memo_bytes = body * 3 / 4;
+    const size_t memo0 = off;
+    // memo region (fixed position): DENSE = cost[] + left[] over all C(n,k);
+    // HASH = buckets + cold left[] (geometry fixed per mask width)
+    unsigned long long dense_entries = 0;
+    for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k);
+    const bool dense_ok = !c->wide && !(c->flags & MPDP_FLAG_HASH_MEMO) &&
+                          dense_entries * 12 + 1024 <= memo_bytes;
+    L.memo_kind = dense_ok ? MEMO_DENSE : MEMO_HASH;
+    const unsigned long long buckets = (unsigned long long)(memo_bytes / (sizeof(Bucket) + 2 * msz));
     L.arena = take(sizeof(Bucket) * buckets);
     L.cold = take(2 * msz * buckets);
+    L.dcost = memo0;
+    L.dleft = align_up(memo0 + 8 * dense_entries, 256);
+    L.memo_end = off;
     const size_t scratch0 = align_up(off, 256);
     const size_t scratch = c->ws_bytes - scratch0 - 1024;
     // level lists are bounded by C(n,k) and by the scratch space (sparse graphs with
@@ -278,13 +296,25 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
 template <typename M>
 static Params<M> make_params(mpdp_ctx* c) {
     Params<M> p;
+    memset(&p, 0, sizeof(p));
     unsigned char* b = c->ws;
     const DevLayout& L = c->lay;
     p.q = reinterpret_cast<const QueryDev<M>*>(b + L.query);
     p.desc = reinterpret_cast<LevelDesc*>(b + L.desc);
-    p.arena = reinterpret_cast<Bucket*>(b + L.arena);
-    p.cold = reinterpret_cast<M*>(b + L.cold);
-    p.arena_buckets = L.arena_buckets;
+    p.memo.arena = reinterpret_cast<Bucket*>(b + L.arena);
+    p.memo.cold = b + L.cold;
+    p.memo.arena_buckets = L.arena_buckets;
+    p.memo.dcost = reinterpret_cast<double*>(b + L.dcost);
+    p.memo.dleft = reinterpret_cast<unsigned int*>(b + L.dleft);
+    p.memo.rank_tab = reinterpret_cast<const unsigned int*>(b + L.rank);
+    p.memo.gen = c->wide ? c->gen8 : c->gen32;
+    p.memo.error = &reinterpret_cast<ResultDev*>(b + L.result)->error;
+    p.memo_kind = L.memo_kind;
+    unsigned long long acc = 0;
+    for (int k = 0; k <= kMaxN; k++) {
+        p.dense_off[k] = acc;
+        if (k >= 2 && k <= c->n) acc += binom_u64(c->n, k);
+    }
     p.light = reinterpret_cast<M*>(b + L.light);
     p.heavy = reinterpret_cast<M*>(b + L.heavy);
     p.wh = reinterpret_cast<unsigned long long*>(b + L.wh);
@@ -298,25 +328,27 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.heavy_cap = L.heavy_cap;
     p.result = reinterpret_cast<ResultDev*>(b + L.result);
     p.epoch = c->query_counter << 6;     // + level k (k <= 56 < 64)
-    p.gen = c->wide ? c->gen8 : c->gen32;
     p.n = c->n;
     p.inv_load = 1.0 / c->load_factor;
     return p;
 }
 
-template <typename M, int CLS>
+template <typename M, int CLS, int MEMO>
 static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
     const size_t smem_enum = sizeof(SQ<M>) + sizeof(unsigned long long) * (MaxN<M>::value + 1) * (MaxN<M>::value + 1);
-    const size_t smem_eval = sizeof(SQ<M>);
-    int* occ = c->occ[c->wide][CLS];      // {enum, light, heavy} CTAs per SM
-    if (!occ[0]) {
+    const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
+    const size_t smem_max = sizeof(SQ<M>) + sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25);
+    int* occ = c->occ[c->wide][CLS][MEMO];   // {enum, light, heavy} CTAs per SM
+    if (!occ[0] || c->occ_n[c->wide][CLS][MEMO] != c->n) {
         CUDA_TRY(c, cudaFuncSetAttribute(k_enum<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_enum));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_eval_light<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eval));
-        CUDA_TRY(c, cudaFuncSetAttribute(k_eval_heavy<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_eval));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_eval_light<M, CLS, MEMO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_eval_heavy<M, CLS, MEMO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_extract<M, MEMO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_enum<M, CLS>, kBlock, smem_enum));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_eval_light<M, CLS>, kLightBlock, smem_eval));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_eval_heavy<M, CLS>, kBlock, smem_eval));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_eval_light<M, CLS, MEMO>, kLightBlock, smem_eval));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_eval_heavy<M, CLS, MEMO>, kBlock, smem_eval));
         for (int i = 0; i < 3; i++) occ[i] = std::max(occ[i], 1);
+        c->occ_n[c->wide][CLS][MEMO] = c->n;
     }
     const bool prof = c->flags & MPDP_FLAG_PROFILE_KERNELS;
     const auto t0 = std::chrono::steady_clock::now();
@@ -333,10 +365,10 @@ static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
         const unsigned int grid_light = (unsigned int)std::min<unsigned long long>(light_ctas, (unsigned long long)c->num_sms * occ[1]);
         k_enum<M, CLS><<<grid_enum, kBlock, smem_enum, c->stream>>>(p, k, nranks, ntiles, item);
         if (prof) CUDA_TRY(c, cudaEventRecord(c->kev[c->nkev++], c->stream));
-        k_eval_light<M, CLS><<<grid_light, kLightBlock, smem_eval, c->stream>>>(p, k);
+        k_eval_light<M, CLS, MEMO><<<grid_light, kLightBlock, smem_eval, c->stream>>>(p, k);
         c->launches += 2;
         if (heavy_pair_bound(c->n, k, CLS)) {
-            k_eval_heavy<M, CLS><<<c->num_sms * occ[2], kBlock, smem_eval, c->stream>>>(p, k, item);
+            k_eval_heavy<M, CLS, MEMO><<<c->num_sms * occ[2], kBlock, smem_eval, c->stream>>>(p, k, item);
             c->launches++;
         }
         if (prof) CUDA_TRY(c, cudaEventRecord(c->kev[c->nkev++], c->stream));
@@ -352,21 +384,31 @@ static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
     return MPDP_OK;
 }
 
+template <typename M, int MEMO>
+static mpdp_status run_memo(mpdp_ctx* c, const Params<M>& p) {
+    mpdp_status st = MPDP_OK;
+    switch (c->cls) {
+        case CLS_TREE: st = launch_levels<M, CLS_TREE, MEMO>(c, p); break;
+        case CLS_CLIQUE: st = launch_levels<M, CLS_CLIQUE, MEMO>(c, p); break;
+        default: st = launch_levels<M, CLS_GENERAL, MEMO>(c, p); break;
+    }
+    if (st != MPDP_OK) return st;
+    const size_t smem = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
+    k_extract<M, MEMO><<<1, 64, smem, c->stream>>>(p);
+    c->launches++;
+    return MPDP_OK;
+}
+
 template <typename M>
 static mpdp_status run_typed(mpdp_ctx* c) {
     const Params<M> p = make_params<M>(c);
     CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
     k_init<M><<<1, 64, 0, c->stream>>>(p);
     c->launches = 1;
-    mpdp_status st = MPDP_OK;
-    switch (c->cls) {
-        case CLS_TREE: st = launch_levels<M, CLS_TREE>(c, p); break;
-        case CLS_CLIQUE: st = launch_levels<M, CLS_CLIQUE>(c, p); break;
-        default: st = launch_levels<M, CLS_GENERAL>(c, p); break;
-    }
+    mpdp_status st;
+    if (!c->wide && c->lay.memo_kind == MEMO_DENSE) st = run_memo<M, MEMO_DENSE>(c, p);
+    else st = run_memo<M, MEMO_HASH>(c, p);
     if (st != MPDP_OK) return st;
-    k_extract<M><<<1, 64, sizeof(SQ<M>), c->stream>>>(p);
-    c->launches++;
     CUDA_TRY(c, cudaGetLastError());
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     c->d2h_bytes = sizeof(ResultDev);
@@ -505,6 +547,8 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
     // memo tags: a fresh tag per query makes every slot of an earlier query read as empty
     const int width = c->wide ? 64 : 32;
     bool clear = (c->last_width != 0 && c->last_width != width);   // arena geometry changed
+    // dense memo entries are plain doubles: they must not be read as hash tags later
+    if (c->lay.memo_kind == MEMO_HASH && c->last_memo == MEMO_DENSE) clear = true;
     if (prev.tiles != c->lay.tiles || prev.tiles_cap != c->lay.tiles_cap)   // ring moved/grew over scratch
         CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.tiles, 0, sizeof(TileRec) * c->lay.tiles_cap, c->stream));
     if (c->wide) {
@@ -514,6 +558,25 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
     }
     if (clear) CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.arena, 0, c->lay.cold - c->lay.arena, c->stream));
     c->last_width = width;
+    c->last_memo = c->lay.memo_kind;
+    if (c->lay.memo_kind == MEMO_DENSE && c->rank_n != n) {       // chunked colex-rank tables
+        const RankGeom rg = rank_geom(n);
+        c->h_rank.assign(rg.entries, 0);
+        for (int ch = 0; ch < rg.nch; ch++) {
+            const int bits = std::min(8, n - 8 * ch);
+            for (int o = 0; o <= 8 * ch; o++)
+                for (unsigned int bv = 0; bv < (1u << bits); bv++) {
+                    unsigned long long val = 0;
+                    int seen = 0;
+                    for (int i = 0; i < bits; i++)
+                        if (bv >> i & 1) val += binom_u64(8 * ch + i, o + (seen++) + 1);
+                    c->h_rank[rg.base[ch] + o * rg.len[ch] + bv] = (unsigned int)val;
+                }
+        }
+        CUDA_TRY(c, cudaMemcpy(c->ws + c->lay.rank, c->h_rank.data(), sizeof(unsigned int) * rg.entries,
+                               cudaMemcpyHostToDevice));
+        c->rank_n = n;
+    }
     c->query_counter++;
     // look-back epochs are 22 bits wide (query * 64 + level): recycle the ring
     // records before an epoch value can repeat

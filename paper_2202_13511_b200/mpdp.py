@@ -57,6 +57,7 @@ class mpdp_ctx_config(C.Structure):
 
 FLAG_FORCE_WIDE_MASKS = 1
 FLAG_PROFILE_KERNELS = 2
+FLAG_HASH_MEMO = 4
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",

@@ -164,5 +164,30 @@ def test_load_factor_variants():
     g = W.clique(12, 4)
     o = O.optimize(g)
     for lf in (0.25, 0.75, 0.9):
-        with mpdp.Context(device=0, workspace_bytes=256 << 20, load_factor=lf) as c:
+        with mpdp.Context(device=0, workspace_bytes=256 << 20, load_factor=lf,
+                          flags=mpdp.FLAG_HASH_MEMO) as c:
             check(c.mpdp_optimize(g), o, g)
+
+
+@pytest.fixture(scope="module")
+def hash_ctx():
+    from paper_2202_13511_b200 import mpdp
+    with mpdp.Context(device=0, workspace_bytes=2 << 30, flags=mpdp.FLAG_HASH_MEMO) as c:
+        yield c
+
+
+@pytest.mark.parametrize("topo,n,seed", [("star", 14, 0), ("clique", 12, 1), ("cycle", 13, 2),
+                                         ("random", 14, 3), ("snowflake", 17, 4), ("star", 20, 5),
+                                         ("clique", 15, 6)])
+def test_hash_memo_ablation_parity(hash_ctx, topo, n, seed):
+    """The Murmur3 open-addressing memo (MPDP_FLAG_HASH_MEMO) gives the same results."""
+    g = W.generate(topo, n, seed)
+    check(hash_ctx.mpdp_optimize(g), O.optimize(g), g)
+
+
+def test_alternating_memo_kinds(ctx, hash_ctx):
+    # interleave both memo layouts and widths on one device
+    for g in [W.star(12, 1), W.clique(9, 2), W.random_connected(13, 3)]:
+        o = O.optimize(g)
+        check(ctx.mpdp_optimize(g), o, g)
+        check(hash_ctx.mpdp_optimize(g), o, g)
