@@ -101,6 +101,8 @@ typedef struct {
     double eval_ms;                /* out, MPDP_FLAG_PROFILE_KERNELS: sum of k_eval   */
     uint32_t enum_launches;        /* out: k_enum launches                            */
     uint32_t eval_launches;        /* out: k_eval launches                            */
+    uint32_t memo_kind;            /* out: 1 = perfect-hash (colex rank) memo,
+                                           0 = Murmur3 open-addressing memo          */
 } mpdp_result;
 
 typedef struct {
@@ -121,11 +123,15 @@ typedef struct {
 
 /* flags: use 64-bit set masks even when n <= 32 (exercises the wide kernels) */
 #define MPDP_FLAG_FORCE_WIDE_MASKS 1u
-/* flags: record CUDA events around every level kernel (enum_ms / eval_ms)      */
+/* flags: record CUDA events around every level kernel (enum_ms / eval_ms);
+ * implies the direct-launch path (no graph replay)                             */
 #define MPDP_FLAG_PROFILE_KERNELS 2u
 /* flags: use the Murmur3 open-addressing memo even where the perfect-hash
  * (colex-rank) memo applies (n <= 32); for ablations                           */
 #define MPDP_FLAG_HASH_MEMO 4u
+/* flags: launch kernels one by one instead of replaying the cached CUDA graph
+ * of the level loop (always the case when timeout_ms > 0)                      */
+#define MPDP_FLAG_NO_GRAPH 8u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

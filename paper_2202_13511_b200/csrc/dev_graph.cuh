@@ -14,6 +14,8 @@ template <> struct MaxN<uint64_t> { static constexpr int value = kMaxN; };
 template <typename M> struct QueryDev {
     static constexpr int N = MaxN<M>::value;
     int n, cls, max_depth, pad;
+    unsigned long long epoch;   // look-back epoch base of this query (query counter << 6)
+    unsigned int gen, pad2;     // HASH memo tag of this query
     M adj[N];            // adjacency bitmaps ("adjacency lists ... as bitmap sets")
     M desc[N];           // CLS_TREE: vertices of the subtree rooted at v (root = 0)
     M depth_mask[N];     // CLS_TREE: vertices at depth d

@@ -50,6 +50,7 @@ template <typename M> struct Params {
     M* heavy;
     unsigned long long* wh;                // [heavy_cap + 1] exclusive heavy pair prefix
     Key* bkey;                             // [heavy_cap] cross-warp (cost, left) min
+    double* hcard;                         // [heavy_cap] card(S) of heavy sets (computed once)
     unsigned long long* bdone;             // [heavy_cap] pairs merged so far
     unsigned int* first_heavy;             // [fh_cap] heavy set holding item i's first pair
     unsigned long long fh_cap;
@@ -58,7 +59,6 @@ template <typename M> struct Params {
     unsigned long long list_cap;           // light list capacity
     unsigned long long heavy_cap;          // heavy list capacity
     ResultDev* result;
-    unsigned long long epoch;              // look-back epoch base (unique per query)
     int n;
     int memo_kind;                         // MEMO_HASH / MEMO_DENSE
     double inv_load;                       // HASH: buckets = ceil(count * inv_load / 2)
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kBlock) k_enum(Params<M> p, int k, unsigned lo
     for (int i = threadIdx.x; i < n * NB; i += blockDim.x) binom[i] = p.q->binom[i];
     if (threadIdx.x == 0) q.n = n;
     const unsigned long long rmask = p.tiles_ring - 1;
-    const unsigned long long epoch = ((p.epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
+    const unsigned long long epoch = ((p.q->epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
 
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&p.desc[k].tile_ticket, 1u);
@@ -471,8 +471,12 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
 // (per-level table geometry) and, for DENSE, the rank tables go to shared memory.
 template <typename M, int MEMO>
 __device__ __forceinline__ void memo_prologue(const Params<M>& p, int kmax, SQ<M>& q, MemoView& v,
-                                              unsigned int* rtab) {
+                                              unsigned int* rtab, MemoPtrs& P) {
     load_query(q, p.q);
+    if (threadIdx.x == 0) {
+        P = p.memo;
+        P.gen = p.q->gen;                  // the per-query tag lives with the staged query
+    }
     for (int j = threadIdx.x; j <= kmax; j += blockDim.x) {
         if (MEMO == MEMO_DENSE) {
             v.off[j] = p.dense_off[j];
@@ -515,8 +519,9 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Par
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
     __shared__ MemoView v;
+    __shared__ MemoPtrs P;
     __shared__ LevelDesc d;
-    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    memo_prologue<M, MEMO>(p, k, q, v, rtab, P);
     if (threadIdx.x == 0) d = p.desc[k];
     __syncthreads();
     if (d.n_buckets == 0) return;          // capacity error already flagged
@@ -531,14 +536,19 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Par
             unsigned long long w;
             const int kind = set_kind<M, CLS>(q, S, k, w);
             PairSink<M, MEMO> sink;
-            sink.init(&p.memo, &v, rtab, &q, card_of(q, S));
+            sink.init(&P, &v, rtab, &q, card_of(q, S));
             eval_range<M, CLS>(q, S, k, kind, 0, w, sink, nccp);
             sink.flush();
             nprobe += sink.nprobe;
             pairs += w;
-            memo_insert<M, MEMO>(p.memo, v, rtab, k, S, sink.best);
+            memo_insert<M, MEMO>(P, v, rtab, k, S, sink.best);
         }
     }
+    // card(S) of the heavy sets, one thread per set, for k_eval_heavy (next in
+    // stream order) so its work-item warps never recompute the product chain
+    const unsigned long long n_heavy = d.n_heavy < p.heavy_cap ? d.n_heavy : p.heavy_cap;
+    for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < n_heavy; h += stride)
+        p.hcard[h] = card_of(q, p.heavy[h]);
     flush_counters(&p.desc[k], pairs, nccp, nprobe);
 }
 
@@ -552,8 +562,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
     __shared__ MemoView v;
+    __shared__ MemoPtrs P;
     __shared__ LevelDesc d;
-    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    memo_prologue<M, MEMO>(p, k, q, v, rtab, P);
     if (threadIdx.x == 0) d = p.desc[k];
     __syncthreads();
     if (d.n_buckets == 0 || d.n_items == 0) return;
@@ -580,7 +591,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
             unsigned long long wk;
             const int kind = set_kind<M, CLS>(q, S, k, wk);
             PairSink<M, MEMO> sink;
-            sink.init(&p.memo, &v, rtab, &q, card_of(q, S));
+            sink.init(&P, &v, rtab, &q, p.hcard[h]);
             // lane-contiguous chunks of the segment [a, b)
             const unsigned long long cnt = b - a, per = (cnt + 31) >> 5;
             unsigned long long j0 = a + per * lane, j1 = j0 + per;
@@ -593,7 +604,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
             if (lane == 0) {
                 pairs += cnt;
                 if (a == 0 && b == w) {
-                    memo_insert<M, MEMO>(p.memo, v, rtab, k, S, best);
+                    memo_insert<M, MEMO>(P, v, rtab, k, S, best);
                 } else {
                     atomic_key_min(&p.bkey[h], best);
                     __threadfence();
@@ -602,7 +613,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
                         __threadfence();
                         const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&p.bkey[h]);
                         const Key fin{ld_relaxed(kp), ld_relaxed(kp + 1)};
-                        memo_insert<M, MEMO>(p.memo, v, rtab, k, S, fin);
+                        memo_insert<M, MEMO>(P, v, rtab, k, S, fin);
                     }
                 }
             }
@@ -620,7 +631,8 @@ __global__ void k_extract(Params<M> p) {
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
     __shared__ MemoView v;
-    memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
+    __shared__ MemoPtrs P;
+    memo_prologue<M, MEMO>(p, p.n, q, v, rtab, P);
     __syncthreads();
     if (threadIdx.x != 0) return;
     ResultDev* r = p.result;
@@ -673,7 +685,7 @@ __global__ void k_extract(Params<M> p) {
             continue;
         }
         M L;
-        const double c = memo_get<M, MEMO>(p.memo, v, rtab, S, L);
+        const double c = memo_get<M, MEMO>(P, v, rtab, S, L);
         if (st_state[top] == 0) {
             st_state[top] = 1;
             st_set[sp] = L;

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <dlfcn.h>
 #include <string>
 #include <vector>
@@ -27,6 +28,7 @@ thread_local std::string g_tls_error;
 
 struct DevLayout {
     size_t query = 0, desc = 0, result = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
+           hcard = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
     unsigned long long list_cap = 0, heavy_cap = 0, tiles_cap = 0, fh_cap = 0, arena_buckets = 0;
@@ -66,6 +68,12 @@ struct mpdp_ctx {
     unsigned int flags = 0;
     double load_factor = 0.5;
     int last_memo = -1;
+    struct GraphEntry {
+        cudaGraphExec_t exec;
+        unsigned int launches, enum_launches, eval_launches;
+        int nkev;
+    };
+    std::map<unsigned long long, GraphEntry> graphs;   // level loop per (n, class, memo, width, flags)
     int rank_n = -1;                      // n the uploaded rank tables were built for
     std::vector<unsigned int> h_rank;
     cudaEvent_t kev[2 * kMaxN + 2] = {};  // MPDP_FLAG_PROFILE_KERNELS: around every level kernel
@@ -155,6 +163,8 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
     memset(q, 0, sizeof(QueryDev<M>));
     q->n = n;
     q->cls = c->cls;
+    q->epoch = c->query_counter << 6;     // + level k (k <= 56 < 64)
+    q->gen = c->wide ? c->gen8 : c->gen32;
     for (int v = 0; v < n; v++) {
         q->adj[v] = (M)adj[v];
         q->card[v] = g->cardinalities[v];
@@ -274,13 +284,14 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     if (fixed >= scratch) return fail(c, MPDP_ERR_CAPACITY, "workspace too small for n = " + std::to_string(n));
     const size_t avail = scratch - fixed;
     list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / msz);
-    heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 32));
+    heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 40));
     L.tiles = take(sizeof(TileRec) * tiles_cap);
     L.light = take(msz * list_cap);
     L.heavy = take(msz * heavy_cap);
     L.wh = take(8 * (heavy_cap + 1));
     L.bkey = take(16 * heavy_cap);
     L.bdone = take(8 * heavy_cap);
+    L.hcard = take(8 * heavy_cap);
     L.fh = take(4 * fh_need);
     L.end = off;
     if (L.end > c->ws_bytes) return fail(c, MPDP_ERR_INTERNAL, "layout overflow");
@@ -307,7 +318,6 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.memo.dcost = reinterpret_cast<double*>(b + L.dcost);
     p.memo.dleft = reinterpret_cast<unsigned int*>(b + L.dleft);
     p.memo.rank_tab = reinterpret_cast<const unsigned int*>(b + L.rank);
-    p.memo.gen = c->wide ? c->gen8 : c->gen32;
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.result)->error;
     p.memo_kind = L.memo_kind;
     unsigned long long acc = 0;
@@ -320,6 +330,7 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.wh = reinterpret_cast<unsigned long long*>(b + L.wh);
     p.bkey = reinterpret_cast<Key*>(b + L.bkey);
     p.bdone = reinterpret_cast<unsigned long long*>(b + L.bdone);
+    p.hcard = reinterpret_cast<double*>(b + L.hcard);
     p.first_heavy = reinterpret_cast<unsigned int*>(b + L.fh);
     p.fh_cap = L.fh_cap;
     p.tiles = reinterpret_cast<TileRec*>(b + L.tiles);
@@ -327,14 +338,13 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.list_cap = L.list_cap;
     p.heavy_cap = L.heavy_cap;
     p.result = reinterpret_cast<ResultDev*>(b + L.result);
-    p.epoch = c->query_counter << 6;     // + level k (k <= 56 < 64)
     p.n = c->n;
     p.inv_load = 1.0 / c->load_factor;
     return p;
 }
 
 template <typename M, int CLS, int MEMO>
-static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
+static mpdp_status prepare_kernels(mpdp_ctx* c) {
     const size_t smem_enum = sizeof(SQ<M>) + sizeof(unsigned long long) * (MaxN<M>::value + 1) * (MaxN<M>::value + 1);
     const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
     const size_t smem_max = sizeof(SQ<M>) + sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25);
@@ -350,10 +360,23 @@ static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
         for (int i = 0; i < 3; i++) occ[i] = std::max(occ[i], 1);
         c->occ_n[c->wide][CLS][MEMO] = c->n;
     }
+    return MPDP_OK;
+}
+
+// Enqueue the whole query on c->stream: k_init, per level k_enum + evaluate,
+// k_extract, and the D2H copy of the result.  Used directly (timeout mode) or
+// under stream capture to build the cached CUDA graph.
+template <typename M, int CLS, int MEMO>
+static mpdp_status enqueue_query(mpdp_ctx* c, const Params<M>& p, bool sync_levels) {
+    const size_t smem_enum = sizeof(SQ<M>) + sizeof(unsigned long long) * (MaxN<M>::value + 1) * (MaxN<M>::value + 1);
+    const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
+    const int* occ = c->occ[c->wide][CLS][MEMO];
     const bool prof = c->flags & MPDP_FLAG_PROFILE_KERNELS;
     const auto t0 = std::chrono::steady_clock::now();
     c->nkev = 0;
     c->enum_launches = c->eval_launches = 0;
+    k_init<M><<<1, 64, 0, c->stream>>>(p);
+    c->launches = 1;
     if (prof && c->n >= 2) CUDA_TRY(c, cudaEventRecord(c->kev[c->nkev++], c->stream));
     for (int k = 2; k <= c->n; k++) {
         const unsigned long long nranks = binom_u64(c->n, k);
@@ -375,45 +398,82 @@ static mpdp_status launch_levels(mpdp_ctx* c, const Params<M>& p) {
         c->enum_launches++;
         c->eval_launches++;
         CUDA_TRY(c, cudaGetLastError());
-        if (c->timeout_ms > 0) {
+        if (sync_levels && c->timeout_ms > 0) {
             CUDA_TRY(c, cudaStreamSynchronize(c->stream));
             const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
             if (ms > c->timeout_ms) return fail(c, MPDP_ERR_TIMEOUT, "timeout after level " + std::to_string(k));
         }
     }
+    k_extract<M, MEMO><<<1, 64, smem_eval, c->stream>>>(p);
+    c->launches++;
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
+}
+
+template <typename M, int CLS, int MEMO>
+static mpdp_status run_query(mpdp_ctx* c) {
+    mpdp_status st = prepare_kernels<M, CLS, MEMO>(c);
+    if (st != MPDP_OK) return st;
+    const Params<M> p = make_params<M>(c);   // query-invariant: epoch/tag live in QueryDev
+    // per-kernel profiling events are recorded on the direct-launch path
+    const bool graph = c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_GRAPH | MPDP_FLAG_PROFILE_KERNELS));
+    if (!graph) {
+        CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+        st = enqueue_query<M, CLS, MEMO>(c, p, true);
+        if (st != MPDP_OK) return st;
+        CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+        return MPDP_OK;
+    }
+    const unsigned long long key = (unsigned long long)c->n | (unsigned long long)CLS << 8 |
+                                   (unsigned long long)MEMO << 10 | (unsigned long long)c->wide << 11 |
+                                   (unsigned long long)(c->flags & MPDP_FLAG_PROFILE_KERNELS) << 12;
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        st = enqueue_query<M, CLS, MEMO>(c, p, false);
+        const cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
+        if (st != MPDP_OK) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (ec != cudaSuccess) return fail(c, MPDP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+        mpdp_ctx::GraphEntry e{};
+        const cudaError_t ei = cudaGraphInstantiate(&e.exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) return fail(c, MPDP_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+        e.launches = c->launches;
+        e.enum_launches = c->enum_launches;
+        e.eval_launches = c->eval_launches;
+        e.nkev = c->nkev;
+        it = c->graphs.emplace(key, e).first;
+    }
+    c->launches = it->second.launches;
+    c->enum_launches = it->second.enum_launches;
+    c->eval_launches = it->second.eval_launches;
+    c->nkev = it->second.nkev;
+    c->d2h_bytes = sizeof(ResultDev);
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(c, cudaGraphLaunch(it->second.exec, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
     return MPDP_OK;
 }
 
 template <typename M, int MEMO>
-static mpdp_status run_memo(mpdp_ctx* c, const Params<M>& p) {
-    mpdp_status st = MPDP_OK;
+static mpdp_status run_memo(mpdp_ctx* c) {
     switch (c->cls) {
-        case CLS_TREE: st = launch_levels<M, CLS_TREE, MEMO>(c, p); break;
-        case CLS_CLIQUE: st = launch_levels<M, CLS_CLIQUE, MEMO>(c, p); break;
-        default: st = launch_levels<M, CLS_GENERAL, MEMO>(c, p); break;
+        case CLS_TREE: return run_query<M, CLS_TREE, MEMO>(c);
+        case CLS_CLIQUE: return run_query<M, CLS_CLIQUE, MEMO>(c);
+        default: return run_query<M, CLS_GENERAL, MEMO>(c);
     }
-    if (st != MPDP_OK) return st;
-    const size_t smem = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
-    k_extract<M, MEMO><<<1, 64, smem, c->stream>>>(p);
-    c->launches++;
-    return MPDP_OK;
 }
 
 template <typename M>
 static mpdp_status run_typed(mpdp_ctx* c) {
-    const Params<M> p = make_params<M>(c);
-    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-    k_init<M><<<1, 64, 0, c->stream>>>(p);
-    c->launches = 1;
-    mpdp_status st;
-    if (!c->wide && c->lay.memo_kind == MEMO_DENSE) st = run_memo<M, MEMO_DENSE>(c, p);
-    else st = run_memo<M, MEMO_HASH>(c, p);
-    if (st != MPDP_OK) return st;
-    CUDA_TRY(c, cudaGetLastError());
-    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
-    c->d2h_bytes = sizeof(ResultDev);
-    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-    return MPDP_OK;
+    if (!c->wide && c->lay.memo_kind == MEMO_DENSE) return run_memo<M, MEMO_DENSE>(c);
+    return run_memo<M, MEMO_HASH>(c);
 }
 
 // ------------------------------------------------------------ C ABI
@@ -519,6 +579,7 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto& e : c->kev)
         if (e) cudaEventDestroy(e);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
     return MPDP_OK;
@@ -633,6 +694,7 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     out->d2h_bytes = c->d2h_bytes;
     out->enum_launches = c->enum_launches;
     out->eval_launches = c->eval_launches;
+    out->memo_kind = (uint32_t)c->lay.memo_kind;
     out->enum_ms = out->eval_ms = 0;
     for (int i = 0; i + 1 < c->nkev; i++) {
         float t = 0;

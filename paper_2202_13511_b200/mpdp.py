@@ -45,7 +45,8 @@ class mpdp_result(C.Structure):
                 ("level_pairs", C.POINTER(C.c_uint64)), ("time_ms", C.c_double),
                 ("probes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("enum_ms", C.c_double), ("eval_ms", C.c_double),
-                ("enum_launches", C.c_uint32), ("eval_launches", C.c_uint32)]
+                ("enum_launches", C.c_uint32), ("eval_launches", C.c_uint32),
+                ("memo_kind", C.c_uint32)]
 
 
 class mpdp_ctx_config(C.Structure):
@@ -58,6 +59,7 @@ class mpdp_ctx_config(C.Structure):
 FLAG_FORCE_WIDE_MASKS = 1
 FLAG_PROFILE_KERNELS = 2
 FLAG_HASH_MEMO = 4
+FLAG_NO_GRAPH = 8
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",
@@ -135,6 +137,7 @@ class Result:
     eval_ms: float = 0.0
     enum_launches: int = 0
     eval_launches: int = 0
+    memo_kind: int = 0
 
     def tree(self):
         """Nested tuples: leaves are relation ids, internal nodes (left, right)."""
@@ -181,7 +184,7 @@ class ResultBuf:
         return Result(r.cost, nodes, r.pairs_evaluated, r.ccp_pairs, r.csg_count,
                       list(self.lc), list(self.lx), list(self.lp), r.time_ms, r.gpu_launches,
                       r.probes, r.h2d_bytes, r.d2h_bytes, r.enum_ms, r.eval_ms,
-                      r.enum_launches, r.eval_launches)
+                      r.enum_launches, r.eval_launches, r.memo_kind)
 
 
 class Context:

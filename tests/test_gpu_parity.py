@@ -191,3 +191,18 @@ def test_alternating_memo_kinds(ctx, hash_ctx):
         o = O.optimize(g)
         check(ctx.mpdp_optimize(g), o, g)
         check(hash_ctx.mpdp_optimize(g), o, g)
+
+
+def test_graph_and_direct_paths_agree():
+    """The cached CUDA-graph replay, the direct launch path and the timeout
+    (per-level synchronising) path produce identical results."""
+    from paper_2202_13511_b200 import mpdp
+    gs = [W.star(16, 2), W.clique(13, 3), W.random_connected(14, 4, extra=0.3)]
+    outs = []
+    for flags, tmo in [(0, 0.0), (mpdp.FLAG_NO_GRAPH, 0.0), (0, 60000.0)]:
+        with mpdp.Context(device=0, workspace_bytes=512 << 20, flags=flags, timeout_ms=tmo) as c:
+            outs.append([c.mpdp_optimize(g) for g in gs] + [c.mpdp_optimize(g) for g in gs])
+    for g, o in zip(gs + gs, zip(*outs)):
+        ref = O.optimize(g)
+        for r in o:
+            check(r, ref, g)
