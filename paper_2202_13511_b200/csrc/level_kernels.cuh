@@ -86,19 +86,21 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
 template <typename M, int MEMO>
 struct PairSink {
     static constexpr int NP = (MEMO == MEMO_DENSE) ? 4 : 2;
-    const MemoPtrs* P;
+    const MemoPtrs* P;                     // kernel parameter space
     const MemoView* v;
     const unsigned int* rtab;
     const SQ<M>* q;
+    unsigned int gen;
     M A[NP], B[NP];
     int cnt;
     double cS;
     Key best;
     unsigned long long nprobe;
 
-    __device__ __forceinline__ void init(const MemoPtrs* P_, const MemoView* v_, const unsigned int* rt,
-                                         const SQ<M>* q_, double card) {
+    __device__ __forceinline__ void init(const MemoPtrs* P_, unsigned int gen_, const MemoView* v_,
+                                         const unsigned int* rt, const SQ<M>* q_, double card) {
         P = P_;
+        gen = gen_;
         v = v_;
         rtab = rt;
         q = q_;
@@ -118,7 +120,7 @@ struct PairSink {
             if (u < cnt) valid |= 3u << (2 * u);
         }
         double c[2 * NP];
-        memo_lookup<M, MEMO, 2 * NP>(*P, *v, rtab, *q, X, valid, c, nprobe);
+        memo_lookup<M, MEMO, 2 * NP>(*P, gen, *v, rtab, *q, X, valid, c, nprobe);
 #pragma unroll
         for (int u = 0; u < NP; u++) {
             if (u < cnt) {
@@ -144,7 +146,7 @@ struct PairSink {
 
 // ------------------------------------------------------------ k_init
 template <typename M>
-__global__ void k_init(Params<M> p) {
+__global__ void k_init(const __grid_constant__ Params<M> p) {
     for (int i = threadIdx.x; i <= kMaxN; i += blockDim.x) {
         LevelDesc d = {};
         p.desc[i] = d;
@@ -259,7 +261,7 @@ __device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask
 
 // Persistent CTAs claim tiles of kTile consecutive colex ranks in ticket order.
 template <typename M, int CLS>
-__global__ void __launch_bounds__(kBlock) k_enum(Params<M> p, int k, unsigned long long nranks,
+__global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<M> p, int k, unsigned long long nranks,
                                                  unsigned long long ntiles, unsigned long long item) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);    // only n and adj[] are used here
@@ -467,16 +469,114 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
     }
 }
 
+// Tree fast path (CLS_TREE, DENSE memo; 32-bit masks).  For a set S with
+// elements p_0 < ... < p_{k-1}, rank(S) = sum_i C(p_i, i+1) and removing a
+// single element p_m gives
+//     rank(S \ {p_m}) = rank(S) - C(p_m, m+1) - sum_{i>m} (C(p_i, i+1) - C(p_i, i)),
+// so every split of S along an edge (v, parent v) whose lower side is the single
+// vertex v (all splits of a star) costs two binomial lookups instead of a rank
+// computation; card(S) (reading R5) is folded into the same ascending pass and
+// rank(S) is reused for the insert.  Other splits go through the generic sink.
+template <int MEMO>
+__device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int gen, const MemoView& v,
+                                                const unsigned int* rtab, const unsigned int* bin, const SQ<uint32_t>& q,
+                                                uint32_t S, int k, unsigned long long& nprobe) {
+    constexpr int BS = 33;                 // binomial row stride
+    // ---- ascending pass: rank(S) and card(S)
+    unsigned int R = 0;
+    double x = 1.0;
+    int i = 0;
+    for (uint32_t T = S; T; T &= T - 1, i++) {
+        const int vtx = __ffs(T) - 1;
+        R += bin[vtx * BS + i + 1];
+        x = __dmul_rn(x, q.card[vtx]);
+        for (uint32_t U = S & q.adj[vtx] & ((1u << vtx) - 1u); U; U &= U - 1)
+            x = __dmul_rn(x, q.sel[(__ffs(U) - 1) * q.n + vtx]);
+    }
+    const double cS = x;
+    uint32_t top = 0;
+    for (int d = 0; d <= q.max_depth; d++) {
+        const uint32_t T = S & q.depth_mask[d];
+        if (T) {
+            top = T & (0u - T);
+            break;
+        }
+    }
+    PairSink<uint32_t, MEMO> sink;         // generic splits (internal vertices)
+    sink.init(&P, gen, &v, rtab, &q, cS);
+    // ---- descending pass: leaf splits with incremental ranks, 4 probes in flight
+    const double* lvl = P.dcost + v.off[k - 1];
+    unsigned int rk[4];
+    uint32_t lv[4];
+    int cnt = 0;
+    unsigned int SD = 0;
+    int m = k - 1;
+    for (uint32_t T = S; T; m--) {
+        const int vtx = 31 - __clz(T);
+        const uint32_t b = 1u << vtx;
+        T ^= b;
+        const unsigned int c1 = bin[vtx * BS + m + 1], c0 = bin[vtx * BS + m];
+        if (b != top) {
+            const uint32_t A = S & q.desc[vtx];
+            if (A == b) {                  // v is a leaf of G[S]: B = S \ {v}
+#pragma unroll
+                for (int u = 3; u > 0; u--) {
+                    rk[u] = rk[u - 1];
+                    lv[u] = lv[u - 1];
+                }
+                rk[0] = R - c1 - SD;
+                lv[0] = b;
+                if (++cnt == 4) {
+                    double d[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) d[u] = __ldg(lvl + rk[u]);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const double c = __dadd_rn(__dadd_rn(q.leaf[__ffs(lv[u]) - 1], d[u]), cS);
+                        const uint32_t Bm = S ^ lv[u];
+                        const Key key{(unsigned long long)__double_as_longlong(c),
+                                      (unsigned long long)(lv[u] < Bm ? lv[u] : Bm)};
+                        if (key_less(key, sink.best)) sink.best = key;
+                    }
+                    nprobe += 4;
+                    cnt = 0;
+                }
+            } else {
+                sink.add(A, S ^ A);
+            }
+        }
+        SD += c1 - c0;
+    }
+    if (cnt) {
+        double d[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) d[u] = (u < cnt) ? __ldg(lvl + rk[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (u < cnt) {
+                const double c = __dadd_rn(__dadd_rn(q.leaf[__ffs(lv[u]) - 1], d[u]), cS);
+                const uint32_t Bm = S ^ lv[u];
+                const Key key{(unsigned long long)__double_as_longlong(c),
+                              (unsigned long long)(lv[u] < Bm ? lv[u] : Bm)};
+                if (key_less(key, sink.best)) sink.best = key;
+            }
+        }
+        nprobe += (unsigned long long)cnt;
+    }
+    sink.flush();
+    nprobe += sink.nprobe;
+    // ---- scatter with the rank already known
+    const unsigned long long idx = v.off[k] + R;
+    P.dcost[idx] = __longlong_as_double((long long)sink.best.c);
+    P.dleft[idx] = (unsigned int)sink.best.l;
+}
+
 // Shared prologue of the evaluate / extract kernels: the query, the memo view
 // (per-level table geometry) and, for DENSE, the rank tables go to shared memory.
 template <typename M, int MEMO>
 __device__ __forceinline__ void memo_prologue(const Params<M>& p, int kmax, SQ<M>& q, MemoView& v,
-                                              unsigned int* rtab, MemoPtrs& P) {
+                                              unsigned int* rtab) {
     load_query(q, p.q);
-    if (threadIdx.x == 0) {
-        P = p.memo;
-        P.gen = p.q->gen;                  // the per-query tag lives with the staged query
-    }
     for (int j = threadIdx.x; j <= kmax; j += blockDim.x) {
         if (MEMO == MEMO_DENSE) {
             v.off[j] = p.dense_off[j];
@@ -487,15 +587,14 @@ __device__ __forceinline__ void memo_prologue(const Params<M>& p, int kmax, SQ<M
         }
     }
     if (MEMO == MEMO_DENSE) {
-        const RankGeom g = rank_geom(p.n);
-        if (threadIdx.x == 0) {
-            for (int c = 0; c < kRankChunks; c++) {
-                v.rbase[c] = g.base[c];
-                v.rlen[c] = g.len[c];
-            }
-            v.nch = g.nch;
+        for (unsigned int i = threadIdx.x; i < p.memo.rg.entries; i += blockDim.x) rtab[i] = p.memo.rank_tab[i];
+        // 32-bit binomials C(i, j), i < 33, j < 33, after the rank tables (tree fast path)
+        unsigned int* bin = rtab + p.memo.rg.entries;
+        constexpr int NB = MaxN<M>::value + 1;
+        for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
+            const int a = i / 33, b = i % 33;
+            bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
         }
-        for (unsigned int i = threadIdx.x; i < g.entries; i += blockDim.x) rtab[i] = p.memo.rank_tab[i];
     }
 }
 
@@ -514,14 +613,14 @@ __device__ __forceinline__ void flush_counters(LevelDesc* dk, unsigned long long
 // Light sets (<= kLightMax join pairs): one thread evaluates a whole set, keeps
 // its min in registers and scatters it (prune fused into evaluate).
 template <typename M, int CLS, int MEMO>
-__global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Params<M> p, int k) {
+__global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(const __grid_constant__ Params<M> p, int k) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
     __shared__ MemoView v;
-    __shared__ MemoPtrs P;
     __shared__ LevelDesc d;
-    memo_prologue<M, MEMO>(p, k, q, v, rtab, P);
+    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    const unsigned int gen = p.q->gen;     // the per-query tag lives with the staged query
     if (threadIdx.x == 0) d = p.desc[k];
     __syncthreads();
     if (d.n_buckets == 0) return;          // capacity error already flagged
@@ -535,13 +634,21 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Par
             const M S = p.light[i];
             unsigned long long w;
             const int kind = set_kind<M, CLS>(q, S, k, w);
+            if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE && sizeof(M) == 4) {
+                if (k > 2) {                   // k = 2: both sides are leaves (no level-1 table)
+                    eval_tree_dense<MEMO>(p.memo, gen, v, rtab, rtab + p.memo.rg.entries, q, S, k, nprobe);
+                    nccp += w;
+                    pairs += w;
+                    continue;
+                }
+            }
             PairSink<M, MEMO> sink;
-            sink.init(&P, &v, rtab, &q, card_of(q, S));
+            sink.init(&p.memo, gen, &v, rtab, &q, card_of(q, S));
             eval_range<M, CLS>(q, S, k, kind, 0, w, sink, nccp);
             sink.flush();
             nprobe += sink.nprobe;
             pairs += w;
-            memo_insert<M, MEMO>(P, v, rtab, k, S, sink.best);
+            memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, sink.best);
         }
     }
     // card(S) of the heavy sets, one thread per set, for k_eval_heavy (next in
@@ -557,14 +664,14 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(Par
 // with shuffles, and merge split sets through a 128-bit CAS min + a pair
 // counter (the last contributor scatters the set).
 template <typename M, int CLS, int MEMO>
-__global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, unsigned long long item) {
+__global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(const __grid_constant__ Params<M> p, int k, unsigned long long item) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
     __shared__ MemoView v;
-    __shared__ MemoPtrs P;
     __shared__ LevelDesc d;
-    memo_prologue<M, MEMO>(p, k, q, v, rtab, P);
+    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    const unsigned int gen = p.q->gen;     // the per-query tag lives with the staged query
     if (threadIdx.x == 0) d = p.desc[k];
     __syncthreads();
     if (d.n_buckets == 0 || d.n_items == 0) return;
@@ -591,7 +698,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
             unsigned long long wk;
             const int kind = set_kind<M, CLS>(q, S, k, wk);
             PairSink<M, MEMO> sink;
-            sink.init(&P, &v, rtab, &q, p.hcard[h]);
+            sink.init(&p.memo, gen, &v, rtab, &q, p.hcard[h]);
             // lane-contiguous chunks of the segment [a, b)
             const unsigned long long cnt = b - a, per = (cnt + 31) >> 5;
             unsigned long long j0 = a + per * lane, j1 = j0 + per;
@@ -604,7 +711,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
             if (lane == 0) {
                 pairs += cnt;
                 if (a == 0 && b == w) {
-                    memo_insert<M, MEMO>(P, v, rtab, k, S, best);
+                    memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, best);
                 } else {
                     atomic_key_min(&p.bkey[h], best);
                     __threadfence();
@@ -613,7 +720,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
                         __threadfence();
                         const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&p.bkey[h]);
                         const Key fin{ld_relaxed(kp), ld_relaxed(kp + 1)};
-                        memo_insert<M, MEMO>(P, v, rtab, k, S, fin);
+                        memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, fin);
                     }
                 }
             }
@@ -626,13 +733,13 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(Params<M> p, int k, un
 // One thread walks the memo from the full set: left(S) from the
 // memo, right = S \ left; nodes in post-order, root last.
 template <typename M, int MEMO>
-__global__ void k_extract(Params<M> p) {
+__global__ void k_extract(const __grid_constant__ Params<M> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
     __shared__ MemoView v;
-    __shared__ MemoPtrs P;
-    memo_prologue<M, MEMO>(p, p.n, q, v, rtab, P);
+    memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
+    const unsigned int gen = p.q->gen;
     __syncthreads();
     if (threadIdx.x != 0) return;
     ResultDev* r = p.result;
@@ -685,7 +792,7 @@ __global__ void k_extract(Params<M> p) {
             continue;
         }
         M L;
-        const double c = memo_get<M, MEMO>(P, v, rtab, S, L);
+        const double c = memo_get<M, MEMO>(p.memo, gen, v, rtab, S, L);
         if (st_state[top] == 0) {
             st_state[top] = 1;
             st_set[sp] = L;

@@ -48,8 +48,6 @@ __host__ __device__ inline RankGeom rank_geom(int n) {
 struct MemoView {
     unsigned long long off[kMaxN + 1];     // per level: DENSE entry offset / HASH bucket offset
     unsigned long long nb[kMaxN + 1];      // HASH: buckets per level
-    unsigned int rbase[kRankChunks], rlen[kRankChunks];
-    int nch;
 };
 
 struct MemoPtrs {
@@ -58,23 +56,24 @@ struct MemoPtrs {
     unsigned int* dleft;                   // [sum_j C(n,j)] left(S) (32-bit masks)
     const unsigned int* rank_tab;          // [RankGeom::entries]
     // HASH
+    RankGeom rg;                           // chunk geometry of the rank tables (depends on n)
     Bucket* arena;
     void* cold;                            // left(S) per slot (2 per bucket), mask width
     unsigned long long arena_buckets;
-    unsigned int gen;                      // tag of this query
     unsigned int* error;
 };
 
 // -------------------------------------------------------------- dense memo
-__device__ __forceinline__ unsigned int rank_of(const MemoView& v, const unsigned int* tab, uint32_t T) {
-    unsigned int r = 0;
-    int o = 0;
+// The geometry comes from the kernel parameter block (constant bank, warp
+// uniform); only the table itself is in shared memory.
+__device__ __forceinline__ unsigned int rank_of(const RankGeom& g, const unsigned int* tab, uint32_t T) {
+    unsigned int r = tab[T & 255u];                          // chunk 0: offset 0
 #pragma unroll
-    for (int c = 0; c < kRankChunks; c++) {
-        if (c < v.nch) {
+    for (int c = 1; c < kRankChunks; c++) {
+        if (c < g.nch) {
             const unsigned int b = (T >> (8 * c)) & 255u;
-            r += tab[v.rbase[c] + (unsigned int)o * v.rlen[c] + b];
-            o += __popc(b);
+            const unsigned int o = (unsigned int)__popc(T & ((1u << (8 * c)) - 1u));
+            r += tab[g.base[c] + o * g.len[c] + b];
         }
     }
     return r;
@@ -101,9 +100,9 @@ __device__ __forceinline__ unsigned long long hash_home(const MemoView& v, M T, 
 
 // Walk the probe sequence from bucket b until T or an empty slot is found.
 template <typename M>
-__device__ double hash_walk(const MemoPtrs& P, const MemoView& v, M T, int j, unsigned long long b,
-                            unsigned long long* slot_out) {
-    const unsigned long long want = Tag<M>::make(T, P.gen);
+__device__ double hash_walk(const MemoPtrs& P, unsigned int gen, const MemoView& v, M T, int j,
+                            unsigned long long b, unsigned long long* slot_out) {
+    const unsigned long long want = Tag<M>::make(T, gen);
     const unsigned int g = Tag<M>::gen_of(want);
     const unsigned long long nb = v.nb[j];
     for (unsigned long long guard = 0; guard < nb; guard++) {
@@ -124,9 +123,9 @@ __device__ double hash_walk(const MemoPtrs& P, const MemoView& v, M T, int j, un
 }
 
 template <typename M>
-__device__ __forceinline__ void hash_insert(const MemoPtrs& P, unsigned long long off, unsigned long long nb, M S,
-                                            const Key& best) {
-    const unsigned long long want = Tag<M>::make(S, P.gen);
+__device__ __forceinline__ void hash_insert(const MemoPtrs& P, unsigned int gen, unsigned long long off,
+                                            unsigned long long nb, M S, const Key& best) {
+    const unsigned long long want = Tag<M>::make(S, gen);
     const unsigned int g = Tag<M>::gen_of(want);
     Bucket* base = P.arena + off;
     unsigned long long b = fastrange(fmix(S), nb);
@@ -154,7 +153,8 @@ __device__ __forceinline__ void hash_insert(const MemoPtrs& P, unsigned long lon
 // Batched cost lookup: every load of the batch is issued before any is used,
 // so a thread keeps NP probes in flight.  Singletons read the leaf cost.
 template <typename M, int MEMO, int NP>
-__device__ __forceinline__ void memo_lookup(const MemoPtrs& P, const MemoView& v, const unsigned int* rtab,
+__device__ __forceinline__ void memo_lookup(const MemoPtrs& P, unsigned int gen, const MemoView& v,
+                                            const unsigned int* rtab,
                                             const SQ<M>& q, const M (&X)[NP], unsigned valid, double (&c)[NP],
                                             unsigned long long& nprobe) {
     if (MEMO == MEMO_DENSE) {
@@ -164,7 +164,7 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, const MemoView& v
             const int j = popc(X[i]);
             d[i] = 0.0;
             if (((valid >> i) & 1) && j > 1)
-                d[i] = __ldg(P.dcost + v.off[j] + rank_of(v, rtab, (uint32_t)X[i]));
+                d[i] = __ldg(P.dcost + v.off[j] + rank_of(P.rg, rtab, (uint32_t)X[i]));
         }
 #pragma unroll
         for (int i = 0; i < NP; i++) {
@@ -197,7 +197,7 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, const MemoView& v
                 continue;
             }
             nprobe++;
-            const unsigned long long want = Tag<M>::make(X[i], P.gen);
+            const unsigned long long want = Tag<M>::make(X[i], gen);
             if (bk[i].k0 == want) c[i] = __longlong_as_double((long long)bk[i].c0);
             else if (bk[i].k1 == want) c[i] = __longlong_as_double((long long)bk[i].c1);
             else pending |= 1u << i;
@@ -215,7 +215,7 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, const MemoView& v
 #pragma unroll
             for (int i = 0; i < NP; i++) {
                 if ((pending >> i) & 1) {
-                    const unsigned long long want = Tag<M>::make(X[i], P.gen);
+                    const unsigned long long want = Tag<M>::make(X[i], gen);
                     if (bk[i].k0 == want) {
                         c[i] = __longlong_as_double((long long)bk[i].c0);
                         pending &= ~(1u << i);
@@ -236,29 +236,29 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, const MemoView& v
 
 // scatter (S, best(S)) into the level-k table
 template <typename M, int MEMO>
-__device__ __forceinline__ void memo_insert(const MemoPtrs& P, const MemoView& v, const unsigned int* rtab, int k,
-                                            M S, const Key& best) {
+__device__ __forceinline__ void memo_insert(const MemoPtrs& P, unsigned int gen, const MemoView& v,
+                                            const unsigned int* rtab, int k, M S, const Key& best) {
     if (MEMO == MEMO_DENSE) {
-        const unsigned long long idx = v.off[k] + rank_of(v, rtab, (uint32_t)S);
+        const unsigned long long idx = v.off[k] + rank_of(P.rg, rtab, (uint32_t)S);
         P.dcost[idx] = __longlong_as_double((long long)best.c);
         P.dleft[idx] = (unsigned int)best.l;
     } else {
-        hash_insert(P, v.off[k], v.nb[k], S, best);
+        hash_insert(P, gen, v.off[k], v.nb[k], S, best);
     }
 }
 
 // (cost, left) of a finished set (extraction)
 template <typename M, int MEMO>
-__device__ __forceinline__ double memo_get(const MemoPtrs& P, const MemoView& v, const unsigned int* rtab, M S,
-                                           M& left) {
+__device__ __forceinline__ double memo_get(const MemoPtrs& P, unsigned int gen, const MemoView& v,
+                                           const unsigned int* rtab, M S, M& left) {
     const int j = popc(S);
     if (MEMO == MEMO_DENSE) {
-        const unsigned long long idx = v.off[j] + rank_of(v, rtab, (uint32_t)S);
+        const unsigned long long idx = v.off[j] + rank_of(P.rg, rtab, (uint32_t)S);
         left = (M)P.dleft[idx];
         return P.dcost[idx];
     } else {
         unsigned long long slot = 0;
-        const double c = hash_walk(P, v, S, j, hash_home(v, S, j), &slot);
+        const double c = hash_walk(P, gen, v, S, j, hash_home(v, S, j), &slot);
         left = reinterpret_cast<const M*>(P.cold)[slot];
         return c;
     }

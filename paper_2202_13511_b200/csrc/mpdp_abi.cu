@@ -318,6 +318,7 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.memo.dcost = reinterpret_cast<double*>(b + L.dcost);
     p.memo.dleft = reinterpret_cast<unsigned int*>(b + L.dleft);
     p.memo.rank_tab = reinterpret_cast<const unsigned int*>(b + L.rank);
+    p.memo.rg = rank_geom(c->n <= 32 ? c->n : 32);
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.result)->error;
     p.memo_kind = L.memo_kind;
     unsigned long long acc = 0;
@@ -346,8 +347,8 @@ static Params<M> make_params(mpdp_ctx* c) {
 template <typename M, int CLS, int MEMO>
 static mpdp_status prepare_kernels(mpdp_ctx* c) {
     const size_t smem_enum = sizeof(SQ<M>) + sizeof(unsigned long long) * (MaxN<M>::value + 1) * (MaxN<M>::value + 1);
-    const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
-    const size_t smem_max = sizeof(SQ<M>) + sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25);
+    const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * (rank_geom(c->n).entries + 33 * 33) : 0);
+    const size_t smem_max = sizeof(SQ<M>) + sizeof(unsigned int) * (256 * (1 + 9 + 17 + 25) + 33 * 33);
     int* occ = c->occ[c->wide][CLS][MEMO];   // {enum, light, heavy} CTAs per SM
     if (!occ[0] || c->occ_n[c->wide][CLS][MEMO] != c->n) {
         CUDA_TRY(c, cudaFuncSetAttribute(k_enum<M, CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_enum));
@@ -369,7 +370,7 @@ static mpdp_status prepare_kernels(mpdp_ctx* c) {
 template <typename M, int CLS, int MEMO>
 static mpdp_status enqueue_query(mpdp_ctx* c, const Params<M>& p, bool sync_levels) {
     const size_t smem_enum = sizeof(SQ<M>) + sizeof(unsigned long long) * (MaxN<M>::value + 1) * (MaxN<M>::value + 1);
-    const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * rank_geom(c->n).entries : 0);
+    const size_t smem_eval = sizeof(SQ<M>) + (MEMO == MEMO_DENSE ? sizeof(unsigned int) * (rank_geom(c->n).entries + 33 * 33) : 0);
     const int* occ = c->occ[c->wide][CLS][MEMO];
     const bool prof = c->flags & MPDP_FLAG_PROFILE_KERNELS;
     const auto t0 = std::chrono::steady_clock::now();
