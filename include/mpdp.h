@@ -132,6 +132,9 @@ typedef struct {
 /* flags: launch kernels one by one instead of replaying the cached CUDA graph
  * of the level loop (always the case when timeout_ms > 0)                      */
 #define MPDP_FLAG_NO_GRAPH 8u
+/* flags: do not use the single persistent cooperative kernel for the level
+ * loop (perfect-hash memo); launch per-level kernels instead (ablation)        */
+#define MPDP_FLAG_NO_FUSED 16u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

@@ -1,0 +1,236 @@
+// fused.cuh — the whole level loop of Alg. mpdp_gpu as ONE
+// persistent cooperative kernel (perfect-hash memo, n <= 32).
+//
+// Per level k every CTA claims tiles of colex ranks.  A tile is enumerated
+// (unrank + Gosper + connectivity + classification, as k_enum); its light
+// sets (<= 32 join pairs) go to a CTA-local shared-memory queue together with
+// their colex rank -- which IS their memo slot -- and are evaluated on the spot
+// by the CTA's threads.  Light sets therefore need no global compaction, list
+// traffic or second launch.  Heavy sets are compacted into the global heavy
+// list by the decoupled look-back scan exactly as in k_enum, then evaluated
+// after a grid barrier by the work-item heavy phase.  Levels are separated by
+// a grid barrier (the dependency of P:209-215), and block 0 extracts the plan
+// at the end.  One launch per query instead of 2-3 per level.
+#pragma once
+#include "level_kernels.cuh"
+
+namespace mpdp {
+
+constexpr int kFusedRanksPerThread = 8;
+constexpr int kFusedTile = kBlock * kFusedRanksPerThread;   // 2048 ranks, queue of 2048 sets
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Sense-free grid barrier: bar[0] counts arrivals, bar[1] is the generation.
+// All CTAs are co-resident (cooperative launch).  Afterwards every thread
+// fences, which also invalidates this SM's L1 (CCTL.IVALL), so no CTA keeps a
+// stale line of memo entries written by another SM in the previous phase.
+__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int* err) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int g = ld_acquire_u32(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            const unsigned long long t0 = globaltimer_ns();
+            while (ld_acquire_u32(bar + 1) == g) {
+                __nanosleep(64);
+                if (watchdog_expired(t0)) {   // never hang the device: flag and fall through
+                    atomicOr(err, ERR_HANG);
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    __threadfence();
+}
+
+__device__ __forceinline__ uint32_t unrank_colex32(const unsigned int* bin, int n, int k, unsigned int r) {
+    uint32_t S = 0;
+    int c = n - 1;
+    for (int i = k; i >= 1; i--) {
+        while (bin[c * 33 + i] > r) c--;
+        S |= 1u << c;
+        r -= bin[c * 33 + i];
+        c--;
+    }
+    return S;
+}
+
+template <int CLS>
+__global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ Params<uint32_t> p) {
+    using M = uint32_t;
+    constexpr int MEMO = MEMO_DENSE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
+    unsigned int* bin = rtab + p.memo.rg.entries;                  // 33 x 33 binomials
+    uint32_t* qmask = bin + 33 * 33;                               // light-set queue
+    unsigned int* qrank = qmask + kFusedTile;
+    __shared__ MemoView v;
+    __shared__ LevelDesc d;
+    __shared__ unsigned long long s_tile;
+    __shared__ Tri s_excl, s_agg;
+
+    memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
+    const unsigned int gen = p.q->gen;
+    const int n = p.n;
+    __syncthreads();
+    const unsigned long long rmask = p.tiles_ring - 1;
+
+    for (int k = 2; k <= n; k++) {
+        const unsigned int nranks = bin[n * 33 + k];
+        const unsigned long long ntiles = (nranks + kFusedTile - 1) / kFusedTile;
+        const bool heavy_level = (p.heavy_levels >> k) & 1ull;
+        const unsigned long long item = p.item_of[k];
+        const unsigned long long epoch = ((p.q->epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
+        unsigned long long pairs = 0, nccp = 0, nprobe = 0, nlight = 0;
+
+        while (true) {
+            if (threadIdx.x == 0) s_tile = atomicAdd(&p.desc[k].tile_ticket, 1u);
+            __syncthreads();
+            const unsigned long long tile = s_tile;
+            if (tile >= ntiles) break;
+
+            // ---- unrank + filter + classify (registers only)
+            const unsigned int r0 = (unsigned int)(tile * kFusedTile) + threadIdx.x * kFusedRanksPerThread;
+            M S0 = 0;
+            unsigned int lflag = 0, hflag = 0;
+            Tri mine = {0, 0, 0};
+            if (r0 < nranks) {
+                S0 = unrank_colex32(bin, n, k, r0);
+                M S = S0;
+#pragma unroll
+                for (int i = 0; i < kFusedRanksPerThread; i++) {
+                    if (r0 + i < nranks) {
+                        if (connected(q, S)) {
+                            unsigned long long w;
+                            set_kind<M, CLS>(q, S, k, w);
+                            if (w <= kLightMax) {
+                                lflag |= 1u << i;
+                            } else {
+                                hflag |= 1u << i;
+                                mine.w += w;
+                            }
+                        }
+                        if (r0 + i + 1 < nranks) S = gosper(S);
+                    }
+                }
+            }
+            mine.l = __popc(lflag);
+            mine.h = __popc(hflag);
+
+            // ---- block scan; global look-back only where heavy sets can exist
+            Tri agg;
+            const Tri ex = block_scan(mine, agg);
+            if (heavy_level) {
+                if (threadIdx.x < 32) {
+                    const Tri excl = lookback(p.tiles, rmask, tile, epoch, agg, &p.result->error);
+                    if (threadIdx.x == 0) {
+                        s_excl = excl;
+                        s_agg = agg;
+                    }
+                }
+                __syncthreads();
+                if (threadIdx.x == 0 && tile == ntiles - 1) {   // level totals of the heavy list
+                    LevelDesc& dk = p.desc[k];
+                    const unsigned long long H = s_excl.h + s_agg.h, W = s_excl.w + s_agg.w;
+                    dk.n_heavy = H;
+                    dk.heavy_pairs = W;
+                    dk.n_items = (W + item - 1) / item;
+                    if (dk.n_items > p.fh_cap || H > p.heavy_cap) atomicOr(&p.result->error, ERR_CAPACITY);
+                    if (H < p.heavy_cap + 1) p.wh[H] = W;
+                    dk.n_buckets = 1;
+                }
+            }
+            const Tri excl = heavy_level ? s_excl : Tri{0, 0, 0};
+
+            // ---- light sets -> CTA queue (slot = colex rank); heavy sets -> global list
+            if (lflag | hflag) {
+                unsigned int li = (unsigned int)ex.l;
+                unsigned long long hi = excl.h + ex.h, wi = excl.w + ex.w;
+                M S = S0;
+#pragma unroll
+                for (int i = 0; i < kFusedRanksPerThread; i++) {
+                    if ((lflag >> i) & 1) {
+                        qmask[li] = S;
+                        qrank[li] = r0 + i;
+                        li++;
+                    }
+                    if ((hflag >> i) & 1) {
+                        unsigned long long w;
+                        set_kind<M, CLS>(q, S, k, w);
+                        if (hi < p.heavy_cap) {
+                            p.heavy[hi] = S;
+                            p.wh[hi] = wi;
+                            p.bkey[hi] = key_inf();
+                            p.bdone[hi] = 0;
+                            const unsigned long long it0 = (wi + item - 1) / item, it1 = (wi + w - 1) / item;
+                            for (unsigned long long it = it0; it <= it1; it++)
+                                if (it < p.fh_cap) p.first_heavy[it] = (unsigned int)hi;
+                        }
+                        wi += w;
+                        hi++;
+                    }
+                    if (r0 + i + 1 < nranks && i + 1 < kFusedRanksPerThread) S = gosper(S);
+                }
+            }
+            __syncthreads();
+
+            // ---- evaluate the tile's light sets (thread per set)
+            const unsigned int nq = (unsigned int)agg.l;
+            for (unsigned int e = threadIdx.x; e < nq; e += blockDim.x) {
+                const M S = qmask[e];
+                unsigned long long w;
+                const int kind = set_kind<M, CLS>(q, S, k, w);
+                pairs += w;
+                if constexpr (CLS == CLS_TREE) {
+                    if (k > 2) {
+                        eval_tree_dense<MEMO>(p.memo, gen, v, rtab, bin, q, S, k, nprobe);
+                        nccp += w;
+                        continue;
+                    }
+                }
+                PairSink<M, MEMO> sink;
+                sink.init(&p.memo, gen, &v, rtab, &q, card_of(q, S));
+                eval_range<M, CLS>(q, S, k, kind, 0, w, sink, nccp);
+                sink.flush();
+                nprobe += sink.nprobe;
+                const unsigned long long idx = v.off[k] + qrank[e];
+                p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
+                p.memo.dleft[idx] = (unsigned int)sink.best.l;
+            }
+            if (threadIdx.x == 0) nlight += nq;
+            __syncthreads();                   // queue, s_tile, scan scratch reused next tile
+        }
+        if (threadIdx.x == 0 && nlight) atomicAdd(&p.desc[k].n_light, nlight);
+        flush_counters(&p.desc[k], pairs, nccp, nprobe);
+        grid_sync(p.gbar, &p.result->error);
+
+        if (heavy_level) {
+            // card(S) of every heavy set once (one thread per set)
+            if (threadIdx.x == 0) d = p.desc[k];
+            __syncthreads();
+            const unsigned long long nh = d.n_heavy < p.heavy_cap ? d.n_heavy : p.heavy_cap;
+            const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+            for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride)
+                p.hcard[h] = card_of(q, p.heavy[h]);
+            grid_sync(p.gbar, &p.result->error);
+            unsigned long long hp = 0, hc = 0, hpr = 0;
+            heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, hp, hc, hpr);
+            flush_counters(&p.desc[k], hp, hc, hpr);
+            grid_sync(p.gbar, &p.result->error);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) extract_phase<M, MEMO>(p, q, v, rtab, gen);
+}
+
+}  // namespace mpdp

@@ -59,6 +59,9 @@ template <typename M> struct Params {
     unsigned long long list_cap;           // light list capacity
     unsigned long long heavy_cap;          // heavy list capacity
     ResultDev* result;
+    unsigned int* gbar;                    // fused kernel: grid barrier {count, generation}
+    unsigned long long heavy_levels;       // bit k: level k can have heavy sets
+    unsigned long long item_of[kMaxN + 1]; // heavy work-item size per level
     int n;
     int memo_kind;                         // MEMO_HASH / MEMO_DENSE
     double inv_load;                       // HASH: buckets = ceil(count * inv_load / 2)
@@ -197,7 +200,7 @@ __device__ __forceinline__ Tri block_scan(Tri v, Tri& total) {
 // the 32 preceding tiles at once; the exclusive prefix is the sum of aggregates
 // back to the nearest tile that already published its inclusive prefix.
 __device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask, unsigned long long tile,
-                                        unsigned long long epoch, Tri agg) {
+                                        unsigned long long epoch, Tri agg, unsigned int* err) {
     const int lane = threadIdx.x & 31;
     TileRec* tr = tiles + (tile & rmask);
     const unsigned long long me = (tile << 24) | epoch;
@@ -217,6 +220,7 @@ __device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask
     Tri excl = {0, 0, 0};
     if (tile == 0) return excl;
     long long top = (long long)tile - 1;
+    const unsigned long long t0 = globaltimer_ns();
     while (true) {
         const long long jj = top - lane;
         const TileRec* pr = tiles + ((unsigned long long)jj & rmask);
@@ -231,7 +235,13 @@ __device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask
         const unsigned ready_mask = __ballot_sync(0xffffffffu, ready);
         const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
         const unsigned need = (first_inc >= 31) ? 0xffffffffu : ((2u << first_inc) - 1u);
-        if ((ready_mask & need) != need) continue;           // a predecessor has not published yet
+        if ((ready_mask & need) != need) {                   // a predecessor has not published yet
+            if (watchdog_expired(t0)) {
+                if (lane == 0) atomicOr(err, ERR_HANG);
+                break;
+            }
+            continue;
+        }
         Tri v = {0, 0, 0};
         if (jj >= 0 && lane <= first_inc) {
             if (lane == first_inc) {
@@ -315,7 +325,7 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
         Tri agg;
         const Tri ex = block_scan(mine, agg);
         if (threadIdx.x < 32) {
-            const Tri excl = lookback(p.tiles, rmask, tile, epoch, agg);
+            const Tri excl = lookback(p.tiles, rmask, tile, epoch, agg, &p.result->error);
             if (threadIdx.x == 0) {
                 s_excl = excl;
                 s_agg = agg;
@@ -529,7 +539,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
                 if (++cnt == 4) {
                     double d[4];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) d[u] = __ldg(lvl + rk[u]);
+                    for (int u = 0; u < 4; u++) d[u] = lvl[rk[u]];
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         const double c = __dadd_rn(__dadd_rn(q.leaf[__ffs(lv[u]) - 1], d[u]), cS);
@@ -550,7 +560,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
     if (cnt) {
         double d[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) d[u] = (u < cnt) ? __ldg(lvl + rk[u]) : 0.0;
+        for (int u = 0; u < 4; u++) d[u] = (u < cnt) ? lvl[rk[u]] : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; u++) {
             if (u < cnt) {
@@ -663,21 +673,18 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(con
 // claim groups of items dynamically, evaluate lane-contiguous chunks, reduce
 // with shuffles, and merge split sets through a 128-bit CAS min + a pair
 // counter (the last contributor scatters the set).
+// Heavy phase of level k (shared by k_eval_heavy and the fused kernel): the
+// heavy pair space is cut into `item`-pair work items; warps claim groups of
+// items dynamically, evaluate lane-contiguous chunks, reduce with shuffles and
+// merge split sets through a 128-bit CAS min + a pair counter (the last
+// contributor scatters the set).
 template <typename M, int CLS, int MEMO>
-__global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(const __grid_constant__ Params<M> p, int k, unsigned long long item) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
-    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
-    __shared__ MemoView v;
-    __shared__ LevelDesc d;
-    memo_prologue<M, MEMO>(p, k, q, v, rtab);
-    const unsigned int gen = p.q->gen;     // the per-query tag lives with the staged query
-    if (threadIdx.x == 0) d = p.desc[k];
-    __syncthreads();
+__device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, const SQ<M>& q, const MemoView& v,
+                            const unsigned int* rtab, unsigned int gen, const LevelDesc& d,
+                            unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe) {
     if (d.n_buckets == 0 || d.n_items == 0) return;
     const int lane = threadIdx.x & 31;
     const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-    unsigned long long pairs = 0, nccp = 0, nprobe = 0;
     unsigned long long G = d.n_items / (nwarps * 4);
     if (G < 1) G = 1;
     const unsigned long long ngroups = (d.n_items + G - 1) / G;
@@ -726,22 +733,30 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(const __grid_constant_
             }
         }
     }
+}
+
+template <typename M, int CLS, int MEMO>
+__global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(const __grid_constant__ Params<M> p, int k, unsigned long long item) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
+    __shared__ MemoView v;
+    __shared__ LevelDesc d;
+    memo_prologue<M, MEMO>(p, k, q, v, rtab);
+    const unsigned int gen = p.q->gen;
+    if (threadIdx.x == 0) d = p.desc[k];
+    __syncthreads();
+    unsigned long long pairs = 0, nccp = 0, nprobe = 0;
+    heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, pairs, nccp, nprobe);
     flush_counters(&p.desc[k], pairs, nccp, nprobe);
 }
 
 // ------------------------------------------------------------ k_extract
 // One thread walks the memo from the full set: left(S) from the
-// memo, right = S \ left; nodes in post-order, root last.
+// memo, right = S \ left; nodes in post-order, root last.  Also sums counters.
 template <typename M, int MEMO>
-__global__ void k_extract(const __grid_constant__ Params<M> p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
-    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
-    __shared__ MemoView v;
-    memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
-    const unsigned int gen = p.q->gen;
-    __syncthreads();
-    if (threadIdx.x != 0) return;
+__device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView& v, const unsigned int* rtab,
+                              unsigned int gen) {
     ResultDev* r = p.result;
     const int n = p.n;
     unsigned long long csg = (unsigned long long)n, ccp = 0, pairs = 0, probes = 0;
@@ -819,6 +834,18 @@ __global__ void k_extract(const __grid_constant__ Params<M> p) {
     }
     r->n_nodes = (unsigned int)nn;
     r->cost = r->nodes[nn - 1].cost;
+}
+
+template <typename M, int MEMO>
+__global__ void k_extract(const __grid_constant__ Params<M> p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
+    __shared__ MemoView v;
+    memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
+    const unsigned int gen = p.q->gen;
+    __syncthreads();
+    if (threadIdx.x == 0) extract_phase<M, MEMO>(p, q, v, rtab, gen);
 }
 
 }  // namespace mpdp

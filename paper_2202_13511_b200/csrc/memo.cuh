@@ -21,7 +21,18 @@ namespace mpdp {
 
 enum MemoKind : int { MEMO_HASH = 0, MEMO_DENSE = 1 };
 
-enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u };
+enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u, ERR_HANG = 16u };
+
+// Watchdog for device spin-waits: a bug must surface as an error, never as a
+// hung GPU.  Returns true once `t0` (from globaltimer_ns) is more than 2 s old.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ bool watchdog_expired(unsigned long long t0) {
+    return globaltimer_ns() - t0 > 2000000000ull;
+}
 
 constexpr int kRankChunks = 4;             // 4 x 8 bits cover n <= 32
 
@@ -164,7 +175,7 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, unsigned int gen,
             const int j = popc(X[i]);
             d[i] = 0.0;
             if (((valid >> i) & 1) && j > 1)
-                d[i] = __ldg(P.dcost + v.off[j] + rank_of(P.rg, rtab, (uint32_t)X[i]));
+                d[i] = P.dcost[v.off[j] + rank_of(P.rg, rtab, (uint32_t)X[i])];   // coherent load
         }
 #pragma unroll
         for (int i = 0; i < NP; i++) {

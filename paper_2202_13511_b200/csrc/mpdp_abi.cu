@@ -18,7 +18,7 @@
 #include <string>
 #include <vector>
 
-#include "level_kernels.cuh"
+#include "fused.cuh"
 
 using namespace mpdp;
 
@@ -27,7 +27,7 @@ namespace {
 thread_local std::string g_tls_error;
 
 struct DevLayout {
-    size_t query = 0, desc = 0, result = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
+    size_t query = 0, desc = 0, result = 0, gbar = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
            hcard = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
@@ -64,6 +64,7 @@ struct mpdp_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool ran = false;
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
+    int fused_occ[3] = {}, fused_n[3] = {};
     int occ_n[2][3][2] = {};
     unsigned int flags = 0;
     double load_factor = 0.5;
@@ -254,6 +255,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.query = take(sizeof(QueryDev<uint64_t>));
     L.desc = take(sizeof(LevelDesc) * (kMaxN + 1));
     L.result = take(sizeof(ResultDev));
+    L.gbar = take(64);
     L.rank = take(sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25));
     off = align_up(off, 256);
     if (off + (64u << 20) > c->ws_bytes) return fail(c, MPDP_ERR_CAPACITY, "workspace smaller than 64 MiB");
@@ -277,7 +279,11 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     const size_t scratch = c->ws_bytes - scratch0 - 1024;
     // level lists are bounded by C(n,k) and by the scratch space (sparse graphs with
     // large n keep few of their C(n,k) subsets); overflow is detected on the device
-    unsigned long long ring = 1;
+    // ring >= 4096 records: more than the tiles that can be in flight at once
+    // (resident CTAs), and never smaller than the tile count of the smallest tile
+    // size (the fused kernel uses 2048-rank tiles)
+    tiles_cap = tiles_cap * (kTile / kFusedTile) + 1;
+    unsigned long long ring = 4096;
     while (ring < tiles_cap && ring < (1ull << 20)) ring <<= 1;
     tiles_cap = ring;
     const size_t fixed = sizeof(TileRec) * tiles_cap + 4 * fh_need + 4096;
@@ -321,6 +327,12 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.memo.rg = rank_geom(c->n <= 32 ? c->n : 32);
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.result)->error;
     p.memo_kind = L.memo_kind;
+    p.gbar = reinterpret_cast<unsigned int*>(b + L.gbar);
+    p.heavy_levels = 0;
+    for (int k = 2; k <= c->n; k++) {
+        if (heavy_pair_bound(c->n, k, c->cls)) p.heavy_levels |= 1ull << k;
+        p.item_of[k] = level_item(c->n, k, c->cls, L.fh_cap);
+    }
     unsigned long long acc = 0;
     for (int k = 0; k <= kMaxN; k++) {
         p.dense_off[k] = acc;
@@ -413,8 +425,39 @@ static mpdp_status enqueue_query(mpdp_ctx* c, const Params<M>& p, bool sync_leve
     return MPDP_OK;
 }
 
+// The fused path: k_init, ONE cooperative persistent kernel for every level
+// and the extraction, then the D2H copy of the result.
+template <int CLS>
+static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
+    const size_t smem = sizeof(SQ<uint32_t>) +
+                        sizeof(unsigned int) * (rank_geom(c->n).entries + 33 * 33 + 2 * kFusedTile);
+    int& occ = c->fused_occ[CLS];
+    if (!occ || c->fused_n[CLS] != c->n) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_fused<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_fused<CLS>, kBlock, smem));
+        if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
+        c->fused_n[CLS] = c->n;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    k_init<uint32_t><<<1, 64, 0, c->stream>>>(p);
+    void* args[] = {const_cast<Params<uint32_t>*>(&p)};
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3(c->num_sms * occ), dim3(kBlock), args,
+                                            smem, c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = 2;
+    c->enum_launches = c->eval_launches = 1;
+    c->nkev = 0;
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
+}
+
 template <typename M, int CLS, int MEMO>
 static mpdp_status run_query(mpdp_ctx* c) {
+    if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
+        if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
+            return run_fused<CLS>(c, make_params<M>(c));
+    }
     mpdp_status st = prepare_kernels<M, CLS, MEMO>(c);
     if (st != MPDP_OK) return st;
     const Params<M> p = make_params<M>(c);   // query-invariant: epoch/tag live in QueryDev
@@ -676,6 +719,8 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     CUDA_TRY(c, cudaGetLastError());
     const ResultDev* r = c->h_result;
     if (r->error) {
+        if (r->error & ERR_HANG)
+            return fail(c, MPDP_ERR_INTERNAL, "device watchdog fired (a spin-wait exceeded 2 s); results discarded");
         if (r->error & (ERR_CAPACITY | ERR_ITEMS))
             return fail(c, MPDP_ERR_CAPACITY, "memo does not fit the workspace (device error bits " + std::to_string(r->error) + ")");
         return fail(c, MPDP_ERR_INTERNAL, "device consistency check failed (bits " + std::to_string(r->error) + ")");

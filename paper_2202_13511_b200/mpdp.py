@@ -60,6 +60,7 @@ FLAG_FORCE_WIDE_MASKS = 1
 FLAG_PROFILE_KERNELS = 2
 FLAG_HASH_MEMO = 4
 FLAG_NO_GRAPH = 8
+FLAG_NO_FUSED = 16
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",

@@ -206,3 +206,19 @@ def test_graph_and_direct_paths_agree():
         ref = O.optimize(g)
         for r in o:
             check(r, ref, g)
+
+
+@pytest.mark.parametrize("topo,n,seed", [("star", 12, 0), ("clique", 13, 1), ("cycle", 14, 2),
+                                         ("random", 15, 3), ("snowflake", 18, 4), ("chain", 16, 5)])
+def test_fused_and_per_level_kernels_agree(topo, n, seed):
+    """The single cooperative kernel (default) and the per-level kernels
+    (MPDP_FLAG_NO_FUSED) both match the oracle."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate(topo, n, seed)
+    o = O.optimize(g)
+    for flags in (0, mpdp.FLAG_NO_FUSED):
+        with mpdp.Context(device=0, workspace_bytes=512 << 20, flags=flags) as c:
+            r = c.mpdp_optimize(g)
+            check(r, o, g)
+            if flags == 0:
+                assert r.gpu_launches == 2          # k_init + the fused level loop
