@@ -103,6 +103,9 @@ typedef struct {
     uint32_t eval_launches;        /* out: k_eval launches                            */
     uint32_t memo_kind;            /* out: 1 = perfect-hash (colex rank) memo,
                                            0 = Murmur3 open-addressing memo          */
+    double* level_ms;              /* optional [n+1]: device time of each level (fused
+                                      kernel: %globaltimer at the level barriers; 0 on
+                                      the per-level-kernel path)                       */
 } mpdp_result;
 
 typedef struct {
@@ -171,6 +174,10 @@ mpdp_status mpdp_fetch(mpdp_ctx* ctx, mpdp_result* out);
 const char* mpdp_last_error(const mpdp_ctx* ctx);
 const char* mpdp_status_string(mpdp_status s);
 int mpdp_abi_version(void);
+
+/* Debug: phase timestamps of CTA 0 of the last fused run (builds with
+ * -DMPDP_TRACE; otherwise returns 0).  Entry = ns << 8 | level << 3 | phase. */
+int mpdp_debug_trace(const mpdp_ctx* ctx, unsigned long long* out, int cap);
 
 /* Multi-GPU bootstrap: 128-byte NCCL unique id (call on rank 0 only). */
 mpdp_status mpdp_nccl_get_unique_id(void* out128);

@@ -13,7 +13,7 @@ template <> struct MaxN<uint64_t> { static constexpr int value = kMaxN; };
 // Query as staged in global memory (written by the host once per query).
 template <typename M> struct QueryDev {
     static constexpr int N = MaxN<M>::value;
-    int n, cls, max_depth, pad;
+    int n, cls, max_depth, has_leaf_costs;
     unsigned long long epoch;   // look-back epoch base of this query (query counter << 6)
     unsigned int gen, pad2;     // HASH memo tag of this query
     M adj[N];            // adjacency bitmaps ("adjacency lists ... as bitmap sets")
@@ -28,7 +28,7 @@ template <typename M> struct QueryDev {
 // The part every kernel keeps in shared memory (sel compacted to n x n).
 template <typename M> struct SQ {
     static constexpr int N = MaxN<M>::value;
-    int n, cls, max_depth, pad;
+    int n, cls, max_depth, pad;            // pad = has_leaf_costs (any leaf cost != 0)
     M adj[N];
     M desc[N];
     M depth_mask[N];
@@ -44,6 +44,7 @@ __device__ __forceinline__ void load_query(SQ<M>& s, const QueryDev<M>* q) {
         s.n = n;
         s.cls = q->cls;
         s.max_depth = q->max_depth;
+        s.pad = q->has_leaf_costs;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         s.adj[i] = q->adj[i];
@@ -109,6 +110,18 @@ __device__ __forceinline__ int induced_degree_sum(const SQ<M>& q, M S) {
     int e2 = 0;
     for (M T = S; T; T &= T - 1) e2 += popc(q.adj[ctz(T)] & S);
     return e2;
+}
+
+// Connectivity filter specialised by graph class (same predicate as Alg.
+// connected):
+//   clique : every non-empty subset is connected;
+//   others : grow from the lowest vertex (register BFS; on stars and
+//            snowflakes it stops after a few frontier steps, which measured
+//            faster than counting induced edges).
+template <typename M, int CLS>
+__device__ __forceinline__ bool connected_cls(const SQ<M>& q, M S, int k) {
+    if (CLS == CLS_CLIQUE) return S != 0;
+    return connected(q, S);
 }
 
 // Find-Blocks: biconnected components of G[S] by an iterative

@@ -25,14 +25,23 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
     return v;
 }
 
+__device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Sense-free grid barrier: bar[0] counts arrivals, bar[1] is the generation.
-// All CTAs are co-resident (cooperative launch).  Afterwards every thread
-// fences, which also invalidates this SM's L1 (CCTL.IVALL), so no CTA keeps a
-// stale line of memo entries written by another SM in the previous phase.
+// All CTAs are co-resident (cooperative launch).  Thread 0 releases (fence)
+// before arriving, spins with relaxed loads, then issues ONE acq_rel fence at
+// gpu scope, which also invalidates this SM's L1 (CCTL.IVALL): no thread of the
+// CTA can then read a stale line of memo entries another SM wrote before the
+// barrier.  bar.sync propagates the ordering to the rest of the CTA.
 __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int* err) {
     __syncthreads();
+    if (gridDim.x == 1) return;        // one CTA: bar.sync already orders its global accesses
     if (threadIdx.x == 0) {
-        const unsigned int g = ld_acquire_u32(bar + 1);
+        const unsigned int g = ld_relaxed_u32(bar + 1);
         __threadfence();
         if (atomicAdd(bar, 1u) == gridDim.x - 1) {
             atomicExch(bar, 0u);
@@ -40,17 +49,17 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int* err) 
             atomicAdd(bar + 1, 1u);
         } else {
             const unsigned long long t0 = globaltimer_ns();
-            while (ld_acquire_u32(bar + 1) == g) {
-                __nanosleep(64);
+            while (ld_relaxed_u32(bar + 1) == g) {
+                __nanosleep(32);
                 if (watchdog_expired(t0)) {   // never hang the device: flag and fall through
                     atomicOr(err, ERR_HANG);
                     break;
                 }
             }
         }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
-    __threadfence();
 }
 
 __device__ __forceinline__ uint32_t unrank_colex32(const unsigned int* bin, int n, int k, unsigned int r) {
@@ -86,22 +95,35 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
     __syncthreads();
     const unsigned long long rmask = p.tiles_ring - 1;
 
+#ifdef MPDP_TRACE
+    int trace_i = 0;
+#define TRACE(tag) if (blockIdx.x == 0 && threadIdx.x == 0 && trace_i < kTraceCap) \
+        p.result->trace[trace_i++] = (globaltimer_ns() << 8) | ((unsigned long long)k << 3) | (unsigned long long)(tag)
+#else
+#define TRACE(tag)
+#endif
     for (int k = 2; k <= n; k++) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+        TRACE(0);
         const unsigned int nranks = bin[n * 33 + k];
-        const unsigned long long ntiles = (nranks + kFusedTile - 1) / kFusedTile;
+        // adaptive tiles: small levels are spread over the whole grid (1..8 ranks
+        // per thread) so no CTA serialises a level's evaluation
+        unsigned int rpt = (nranks + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
+        rpt = rpt < 1 ? 1 : (rpt > kFusedRanksPerThread ? kFusedRanksPerThread : rpt);
+        const unsigned int tile_ranks = rpt * blockDim.x;
+        const unsigned long long ntiles = (nranks + tile_ranks - 1) / tile_ranks;
         const bool heavy_level = (p.heavy_levels >> k) & 1ull;
         const unsigned long long item = p.item_of[k];
         const unsigned long long epoch = ((p.q->epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
         unsigned long long pairs = 0, nccp = 0, nprobe = 0, nlight = 0;
 
-        while (true) {
-            if (threadIdx.x == 0) s_tile = atomicAdd(&p.desc[k].tile_ticket, 1u);
-            __syncthreads();
-            const unsigned long long tile = s_tile;
-            if (tile >= ntiles) break;
+        // static tile assignment (all CTAs are co-resident, so the look-back
+        // still makes progress); no ticket atomics on the critical path
+        for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            TRACE(1);
 
             // ---- unrank + filter + classify (registers only)
-            const unsigned int r0 = (unsigned int)(tile * kFusedTile) + threadIdx.x * kFusedRanksPerThread;
+            const unsigned int r0 = (unsigned int)(tile * tile_ranks) + threadIdx.x * rpt;
             M S0 = 0;
             unsigned int lflag = 0, hflag = 0;
             Tri mine = {0, 0, 0};
@@ -110,8 +132,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
                 M S = S0;
 #pragma unroll
                 for (int i = 0; i < kFusedRanksPerThread; i++) {
-                    if (r0 + i < nranks) {
-                        if (connected(q, S)) {
+                    if (i < (int)rpt && r0 + i < nranks) {
+                        if (connected_cls<M, CLS>(q, S, k)) {
                             unsigned long long w;
                             set_kind<M, CLS>(q, S, k, w);
                             if (w <= kLightMax) {
@@ -121,12 +143,13 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
                                 mine.w += w;
                             }
                         }
-                        if (r0 + i + 1 < nranks) S = gosper(S);
+                        if (i + 1 < (int)rpt && r0 + i + 1 < nranks) S = gosper(S);
                     }
                 }
             }
             mine.l = __popc(lflag);
             mine.h = __popc(hflag);
+            TRACE(2);
 
             // ---- block scan; global look-back only where heavy sets can exist
             Tri agg;
@@ -180,14 +203,39 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
                         wi += w;
                         hi++;
                     }
-                    if (r0 + i + 1 < nranks && i + 1 < kFusedRanksPerThread) S = gosper(S);
+                    if (r0 + i + 1 < nranks && i + 1 < (int)rpt) S = gosper(S);
                 }
             }
             __syncthreads();
 
-            // ---- evaluate the tile's light sets (thread per set)
+            TRACE(3);
+            // ---- evaluate the tile's light sets: warp per set (lanes = join pairs)
+            // when the queue is short, else thread per set
             const unsigned int nq = (unsigned int)agg.l;
-            for (unsigned int e = threadIdx.x; e < nq; e += blockDim.x) {
+            const bool warp_mode = nq * 4 <= blockDim.x;
+            if (warp_mode) {
+                const unsigned int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                for (unsigned int e = wid; e < nq; e += blockDim.x >> 5) {
+                    const M S = qmask[e];
+                    unsigned long long w;
+                    const int kind = set_kind<M, CLS>(q, S, k, w);
+                    PairSink<M, MEMO> sink;
+                    sink.init(&p.memo, gen, &v, rtab, &q, card_of(q, S));
+                    unsigned long long ccp_l = 0;
+                    if (lane < w) eval_range<M, CLS>(q, S, k, kind, lane, lane + 1, sink, ccp_l);
+                    sink.flush();
+                    nprobe += sink.nprobe;
+                    nccp += ccp_l;
+                    const Key best = warp_min(sink.best);
+                    if (lane == 0) {
+                        pairs += w;
+                        const unsigned long long idx = v.off[k] + qrank[e];
+                        p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
+                        p.memo.dleft[idx] = (unsigned int)best.l;
+                    }
+                }
+            }
+            for (unsigned int e = threadIdx.x; e < (warp_mode ? 0u : nq); e += blockDim.x) {
                 const M S = qmask[e];
                 unsigned long long w;
                 const int kind = set_kind<M, CLS>(q, S, k, w);
@@ -209,11 +257,14 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
                 p.memo.dleft[idx] = (unsigned int)sink.best.l;
             }
             if (threadIdx.x == 0) nlight += nq;
-            __syncthreads();                   // queue, s_tile, scan scratch reused next tile
+            __syncthreads();                   // queue and scan scratch reused next tile
+            TRACE(4);
         }
         if (threadIdx.x == 0 && nlight) atomicAdd(&p.desc[k].n_light, nlight);
         flush_counters(&p.desc[k], pairs, nccp, nprobe);
+        TRACE(5);
         grid_sync(p.gbar, &p.result->error);
+        TRACE(6);
 
         if (heavy_level) {
             // card(S) of every heavy set once (one thread per set)
@@ -230,7 +281,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
             grid_sync(p.gbar, &p.result->error);
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) extract_phase<M, MEMO>(p, q, v, rtab, gen);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.result->t_level[n + 1] = globaltimer_ns();
+        extract_phase<M, MEMO>(p, q, v, rtab, gen);
+    }
 }
 
 }  // namespace mpdp

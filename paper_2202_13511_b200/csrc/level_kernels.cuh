@@ -33,11 +33,15 @@ struct __align__(64) TileRec {            // decoupled look-back record (ring sl
     unsigned long long inc_l, inc_h, inc_w, pad;
 };
 
+constexpr int kTraceCap = 512;
+
 struct ResultDev {
     double cost;
     unsigned long long csg, ccp, pairs, probes;
     unsigned int n_nodes, error;
     unsigned long long lvl_csg[kMaxN + 1], lvl_ccp[kMaxN + 1], lvl_pairs[kMaxN + 1];
+    unsigned long long t_level[kMaxN + 2];  // fused kernel: globaltimer at each level start (+ end)
+    unsigned long long trace[kTraceCap];    // MPDP_TRACE builds: (ns << 8 | level << 3 | phase) of block 0
     mpdp_plan_node nodes[2 * kMaxN - 1];
 };
 
@@ -155,6 +159,8 @@ __global__ void k_init(const __grid_constant__ Params<M> p) {
         p.desc[i] = d;
     }
     if (threadIdx.x == 0) p.result->error = 0;
+    for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) p.result->t_level[i] = 0;
+    for (int i = threadIdx.x; i < kTraceCap; i += blockDim.x) p.result->trace[i] = 0;
 }
 
 // ------------------------------------------------------------ k_enum
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
 #pragma unroll
             for (int i = 0; i < kRanksPerThread; i++) {
                 if (r0 + i < nranks) {
-                    if (connected(q, S)) {
+                    if (connected_cls<M, CLS>(q, S, k)) {
                         unsigned long long w;
                         set_kind<M, CLS>(q, S, k, w);
                         if (w <= kLightMax) {
@@ -492,6 +498,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
                                                 const unsigned int* rtab, const unsigned int* bin, const SQ<uint32_t>& q,
                                                 uint32_t S, int k, unsigned long long& nprobe) {
     constexpr int BS = 33;                 // binomial row stride
+    constexpr int U = 4;                   // elements per unrolled step = probes in flight
     // ---- ascending pass: rank(S) and card(S)
     unsigned int R = 0;
     double x = 1.0;
@@ -500,8 +507,8 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
         const int vtx = __ffs(T) - 1;
         R += bin[vtx * BS + i + 1];
         x = __dmul_rn(x, q.card[vtx]);
-        for (uint32_t U = S & q.adj[vtx] & ((1u << vtx) - 1u); U; U &= U - 1)
-            x = __dmul_rn(x, q.sel[(__ffs(U) - 1) * q.n + vtx]);
+        for (uint32_t W = S & q.adj[vtx] & ((1u << vtx) - 1u); W; W &= W - 1)
+            x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + vtx]);
     }
     const double cS = x;
     uint32_t top = 0;
@@ -512,73 +519,74 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
             break;
         }
     }
-    PairSink<uint32_t, MEMO> sink;         // generic splits (internal vertices)
-    sink.init(&P, gen, &v, rtab, &q, cS);
-    // ---- descending pass: leaf splits with incremental ranks, 4 probes in flight
+    double best_c = __longlong_as_double(0x7ff0000000000000ll);
+    uint32_t best_l = 0xffffffffu;
+    const bool leaf_costs = q.pad != 0;    // any non-zero leaf cost in this query
+    // ---- descending pass, U elements per step: leaf splits with incremental
+    // ranks, all their probes issued before any is consumed; splits at
+    // internal vertices are only recorded here
     const double* lvl = P.dcost + v.off[k - 1];
-    unsigned int rk[4];
-    uint32_t lv[4];
-    int cnt = 0;
     unsigned int SD = 0;
+    uint32_t internal = 0;
     int m = k - 1;
-    for (uint32_t T = S; T; m--) {
-        const int vtx = 31 - __clz(T);
-        const uint32_t b = 1u << vtx;
-        T ^= b;
-        const unsigned int c1 = bin[vtx * BS + m + 1], c0 = bin[vtx * BS + m];
-        if (b != top) {
-            const uint32_t A = S & q.desc[vtx];
-            if (A == b) {                  // v is a leaf of G[S]: B = S \ {v}
+    for (uint32_t T = S; T;) {
+        unsigned int rk[U];
+        uint32_t lb[U];
 #pragma unroll
-                for (int u = 3; u > 0; u--) {
-                    rk[u] = rk[u - 1];
-                    lv[u] = lv[u - 1];
-                }
-                rk[0] = R - c1 - SD;
-                lv[0] = b;
-                if (++cnt == 4) {
-                    double d[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) d[u] = lvl[rk[u]];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const double c = __dadd_rn(__dadd_rn(q.leaf[__ffs(lv[u]) - 1], d[u]), cS);
-                        const uint32_t Bm = S ^ lv[u];
-                        const Key key{(unsigned long long)__double_as_longlong(c),
-                                      (unsigned long long)(lv[u] < Bm ? lv[u] : Bm)};
-                        if (key_less(key, sink.best)) sink.best = key;
+        for (int u = 0; u < U; u++) {
+            lb[u] = 0;
+            rk[u] = 0;
+            if (T) {
+                const int vtx = 31 - __clz(T);
+                const uint32_t b = 1u << vtx;
+                T ^= b;
+                const unsigned int c1 = bin[vtx * BS + m + 1], c0 = bin[vtx * BS + m];
+                if (b != top) {
+                    if ((S & q.desc[vtx]) == b) {   // v is a leaf of G[S]: B = S \ {v}
+                        lb[u] = b;
+                        rk[u] = R - c1 - SD;
+                    } else {
+                        internal |= b;
                     }
-                    nprobe += 4;
-                    cnt = 0;
                 }
-            } else {
-                sink.add(A, S ^ A);
+                SD += c1 - c0;
+                m--;
             }
         }
-        SD += c1 - c0;
-    }
-    if (cnt) {
-        double d[4];
+        double dv[U];
 #pragma unroll
-        for (int u = 0; u < 4; u++) d[u] = (u < cnt) ? lvl[rk[u]] : 0.0;
+        for (int u = 0; u < U; u++) dv[u] = lb[u] ? lvl[rk[u]] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            if (u < cnt) {
-                const double c = __dadd_rn(__dadd_rn(q.leaf[__ffs(lv[u]) - 1], d[u]), cS);
-                const uint32_t Bm = S ^ lv[u];
-                const Key key{(unsigned long long)__double_as_longlong(c),
-                              (unsigned long long)(lv[u] < Bm ? lv[u] : Bm)};
-                if (key_less(key, sink.best)) sink.best = key;
+        for (int u = 0; u < U; u++) {
+            if (lb[u]) {
+                const double a = leaf_costs ? __dadd_rn(q.leaf[__ffs(lb[u]) - 1], dv[u]) : dv[u];
+                const double c = __dadd_rn(a, cS);
+                const uint32_t Bm = S ^ lb[u];
+                const uint32_t l = lb[u] < Bm ? lb[u] : Bm;
+                if (c < best_c || (c == best_c && l < best_l)) {
+                    best_c = c;
+                    best_l = l;
+                }
+                nprobe++;
             }
         }
-        nprobe += (unsigned long long)cnt;
     }
-    sink.flush();
-    nprobe += sink.nprobe;
+    Key best{(unsigned long long)__double_as_longlong(best_c), (unsigned long long)best_l};
+    if (internal) {                        // generic splits: both sides are multi-vertex
+        PairSink<uint32_t, MEMO> sink;
+        sink.init(&P, gen, &v, rtab, &q, cS);
+        for (uint32_t I = internal; I; I &= I - 1) {
+            const uint32_t A = S & q.desc[__ffs(I) - 1];
+            sink.add(A, S ^ A);
+        }
+        sink.flush();
+        nprobe += sink.nprobe;
+        if (key_less(sink.best, best)) best = sink.best;
+    }
     // ---- scatter with the rank already known
     const unsigned long long idx = v.off[k] + R;
-    P.dcost[idx] = __longlong_as_double((long long)sink.best.c);
-    P.dleft[idx] = (unsigned int)sink.best.l;
+    P.dcost[idx] = __longlong_as_double((long long)best.c);
+    P.dleft[idx] = (unsigned int)best.l;
 }
 
 // Shared prologue of the evaluate / extract kernels: the query, the memo view

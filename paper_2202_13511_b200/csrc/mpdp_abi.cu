@@ -166,10 +166,12 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
     q->cls = c->cls;
     q->epoch = c->query_counter << 6;     // + level k (k <= 56 < 64)
     q->gen = c->wide ? c->gen8 : c->gen32;
+    q->has_leaf_costs = 0;
     for (int v = 0; v < n; v++) {
         q->adj[v] = (M)adj[v];
         q->card[v] = g->cardinalities[v];
         q->leaf[v] = g->leaf_costs ? g->leaf_costs[v] : 0.0;
+        if (q->leaf[v] != 0.0) q->has_leaf_costs = 1;
     }
     for (uint32_t e = 0; e < g->n_edges; e++) {
         const uint32_t u = g->edges[2 * e], v = g->edges[2 * e + 1];
@@ -440,8 +442,18 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     }
     CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
     k_init<uint32_t><<<1, 64, 0, c->stream>>>(p);
+    // grid: enough CTAs for the widest level (tiles) and the heavy work, never
+    // more than can be co-resident; small queries get a small grid so the grid
+    // barriers between levels stay cheap
+    unsigned long long want = 1;
+    for (int k = 2; k <= c->n; k++) {
+        want = std::max(want, (binom_u64(c->n, k) + 511) / 512);
+        want = std::max(want, heavy_pair_bound(c->n, k, CLS) / 16384);
+    }
+    if (CLS == CLS_GENERAL && c->n > 12) want = ~0ull;     // heavy work unknown up front
+    const unsigned int grid = (unsigned int)std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ);
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3(c->num_sms * occ), dim3(kBlock), args,
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3(grid), dim3(kBlock), args,
                                             smem, c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
@@ -750,6 +762,8 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     }
     if (out->nodes) memcpy(out->nodes, r->nodes, sizeof(mpdp_plan_node) * r->n_nodes);
     for (int k = 0; k <= n; k++) {
+        if (out->level_ms)
+            out->level_ms[k] = (k >= 2 && r->t_level[k] && r->t_level[k + 1]) ? 1e-6 * (double)(r->t_level[k + 1] - r->t_level[k]) : 0.0;
         if (out->level_csg) out->level_csg[k] = r->lvl_csg[k];
         if (out->level_ccp) out->level_ccp[k] = r->lvl_ccp[k];
         if (out->level_pairs) out->level_pairs[k] = r->lvl_pairs[k];
@@ -779,6 +793,17 @@ mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo
     st = mpdp_run(c);
     if (st != MPDP_OK) return st;
     return mpdp_fetch(c, out);
+}
+
+// Debug: copy the block-0 phase trace of the last fused run (MPDP_TRACE builds).
+int mpdp_debug_trace(const mpdp_ctx* c, unsigned long long* out, int cap) {
+    if (!c || !c->h_result || !out) return 0;
+    int nn = 0;
+    for (int i = 0; i < kTraceCap && i < cap; i++) {
+        if (!c->h_result->trace[i]) break;
+        out[nn++] = c->h_result->trace[i];
+    }
+    return nn;
 }
 
 mpdp_status mpdp_nccl_get_unique_id(void* out128) {

@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 from typing import List, Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmpdp.so")
+LIB_PATH = os.environ.get("MPDP_LIBRARY", os.path.join(HERE, "libmpdp.so"))
 
 # mpdp_status
 OK, ERR_INVALID_ARGUMENT, ERR_DISCONNECTED, ERR_CAPACITY, ERR_TIMEOUT, ERR_OOM, \
@@ -46,7 +46,7 @@ class mpdp_result(C.Structure):
                 ("probes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("enum_ms", C.c_double), ("eval_ms", C.c_double),
                 ("enum_launches", C.c_uint32), ("eval_launches", C.c_uint32),
-                ("memo_kind", C.c_uint32)]
+                ("memo_kind", C.c_uint32), ("level_ms", C.POINTER(C.c_double))]
 
 
 class mpdp_ctx_config(C.Structure):
@@ -65,7 +65,7 @@ FLAG_NO_FUSED = 16
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",
            "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
-           "mpdp_nccl_get_unique_id", "mpdp_share"]
+           "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace"]
 
 _lib = None
 
@@ -139,6 +139,7 @@ class Result:
     enum_launches: int = 0
     eval_launches: int = 0
     memo_kind: int = 0
+    level_ms: List[float] = field(default_factory=list)
 
     def tree(self):
         """Nested tuples: leaves are relation ids, internal nodes (left, right)."""
@@ -173,7 +174,9 @@ class ResultBuf:
         self.lx = (C.c_uint64 * (n + 1))()
         self.lp = (C.c_uint64 * (n + 1))()
         self.s = mpdp_result(self.nodes, 2 * n - 1)
+        self.lt = (C.c_double * (n + 1))()
         self.s.level_csg, self.s.level_ccp, self.s.level_pairs = self.lc, self.lx, self.lp
+        self.s.level_ms = self.lt
 
     def ref(self):
         return C.byref(self.s)
@@ -185,7 +188,7 @@ class ResultBuf:
         return Result(r.cost, nodes, r.pairs_evaluated, r.ccp_pairs, r.csg_count,
                       list(self.lc), list(self.lx), list(self.lp), r.time_ms, r.gpu_launches,
                       r.probes, r.h2d_bytes, r.d2h_bytes, r.enum_ms, r.eval_ms,
-                      r.enum_launches, r.eval_launches, r.memo_kind)
+                      r.enum_launches, r.eval_launches, r.memo_kind, list(self.lt))
 
 
 class Context:
