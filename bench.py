@@ -208,6 +208,7 @@ def run_ours(args):
         ctx.mpdp_optimize(graphs[i % len(graphs)])
     # ---- timed device-resident steps: query staged, time the level loop
     step_ms, pairs_total, probes_total, launches, sets_total = [], 0, 0, 0, 0
+    kernel_ms, kernel_launches = 0.0, 0
     barrier()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -226,22 +227,9 @@ def run_ours(args):
             probes_total += r.probes
             sets_total += r.csg_count - g.n
             launches += r.gpu_launches
+            kernel_ms += r.eval_ms                    # CUDA events around the level-loop kernel
+            kernel_launches += r.eval_launches
         barrier()
-    # ---- per-kernel device time of the same steps (CUDA events around every
-    # level kernel, direct-launch path) for the roofline of the dominant kernel
-    eval_ms, enum_ms, eval_launches, prof_ms = 0.0, 0.0, 0, 0.0
-    with mpdp.Context(device=local, workspace_bytes=ws, flags=mpdp.FLAG_PROFILE_KERNELS) as pctx:
-        for i in range(min(args.warmup, 2)):
-            pctx.mpdp_optimize(graphs[i % len(graphs)])
-        for i in range(args.steps):
-            g = graphs[i % len(graphs)]
-            flush.fill_(i & 0xff)
-            torch.cuda.synchronize()
-            r = pctx.mpdp_optimize(g)
-            eval_ms += r.eval_ms
-            enum_ms += r.enum_ms
-            eval_launches += r.eval_launches
-            prof_ms += r.time_ms
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -277,26 +265,33 @@ def run_ours(args):
     else:
         e2e_value = e2e_pairs / e2e_s
 
-    # ---- roofline of the dominant kernel (k_eval): algorithmic bytes / CUDA-event time
-    # perfect-hash memo = 8 B cost per probe, per set a 4 B list
-    # read + 8 B cost + 4 B left store; open-addressing memo = 16 B slot per probe,
-    # per set list read + 16 B slot + left
+    # ---- roofline of the dominant kernel: the fused level-loop kernel (one
+    # launch per query does unrank, filter, evaluate, min and memo scatter).
+    # perfect-hash memo = 8 B cost per probe + per connected set
+    # 8 B cost + 4 B left store; open-addressing memo = 16 B slot per probe, per
+    # set list read + 16 B slot + left.
     msz = 4 if n <= 32 else 8
     if memo_kind == 1:
-        alg_bytes = 8 * probes_total + sets_total * (msz + 8 + 4)
+        alg_bytes = 8 * probes_total + sets_total * (8 + 4)
     else:
         alg_bytes = 16 * probes_total + sets_total * (msz + 16 + msz)
-    eval_s = eval_ms / 1e3
     peak, peak_kind = measured_peaks()
-    achieved = alg_bytes / eval_s / 1e9 if eval_s > 0 else 0.0
-    roof = {"bound": "hbm", "kernel": "k_eval (evaluate + min + memo insert)",
+    kern_s = kernel_ms / 1e3
+    achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(args.workload)
+    roof = {"bound": "hbm",
+            "kernel": "k_dp_fused (whole level loop, one launch per query)",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+            "traffic_source": traffic.get("source") if traffic else None,
+            "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
             "memo": "perfect-hash (colex rank)" if memo_kind == 1 else "murmur3 open addressing",
-            "algorithmic_bytes_per_launch": alg_bytes / max(1, eval_launches),
-            "avg_launch_ms": eval_ms / max(1, eval_launches),
-            "share_of_step": eval_ms / max(1e-9, prof_ms),
-            "enum_share_of_step": enum_ms / max(1e-9, prof_ms)}
+            "algorithmic_bytes_per_launch": alg_bytes / max(1, kernel_launches),
+            "avg_launch_ms": kernel_ms / max(1, kernel_launches),
+            "share_of_step": kernel_ms / max(1e-9, sum(step_ms))}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

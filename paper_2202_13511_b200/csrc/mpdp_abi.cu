@@ -65,6 +65,7 @@ struct mpdp_ctx {
     bool ran = false;
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
     int fused_occ[3] = {}, fused_n[3] = {};
+    bool fused = false;                  // last run used the fused kernel
     int occ_n[2][3][2] = {};
     unsigned int flags = 0;
     double load_factor = 0.5;
@@ -453,19 +454,24 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     if (CLS == CLS_GENERAL && c->n > 12) want = ~0ull;     // heavy work unknown up front
     const unsigned int grid = (unsigned int)std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ);
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));    // device time of the fused kernel itself
     CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3(grid), dim3(kBlock), args,
                                             smem, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
     c->launches = 2;
-    c->enum_launches = c->eval_launches = 1;
-    c->nkev = 0;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
     c->d2h_bytes = sizeof(ResultDev);
     return MPDP_OK;
 }
 
 template <typename M, int CLS, int MEMO>
 static mpdp_status run_query(mpdp_ctx* c) {
+    c->fused = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
             return run_fused<CLS>(c, make_params<M>(c));
@@ -754,7 +760,12 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     out->eval_launches = c->eval_launches;
     out->memo_kind = (uint32_t)c->lay.memo_kind;
     out->enum_ms = out->eval_ms = 0;
-    for (int i = 0; i + 1 < c->nkev; i++) {
+    if (c->fused && c->nkev == 2) {      // the fused kernel: enumeration and evaluation together
+        float t = 0;
+        cudaEventElapsedTime(&t, c->kev[0], c->kev[1]);
+        out->eval_ms = t;
+    }
+    for (int i = 0; !c->fused && i + 1 < c->nkev; i++) {
         float t = 0;
         cudaEventElapsedTime(&t, c->kev[i], c->kev[i + 1]);
         if (i % 2 == 0) out->enum_ms += t;
