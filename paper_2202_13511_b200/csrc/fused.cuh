@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t unrank_colex32(const unsigned int* bin, int 
 }
 
 template <int CLS>
-__global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ Params<uint32_t> p) {
+__global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(const __grid_constant__ Params<uint32_t> p) {
     using M = uint32_t;
     constexpr int MEMO = MEMO_DENSE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -106,20 +106,30 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
         TRACE(0);
         const unsigned int nranks = bin[n * 33 + k];
-        // adaptive tiles: small levels are spread over the whole grid (1..8 ranks
-        // per thread) so no CTA serialises a level's evaluation
-        unsigned int rpt = (nranks + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
+        const bool heavy_level = CLS != CLS_TREE && ((p.heavy_levels >> k) & 1ull);
+        // Tiles.  Small levels are spread over the whole grid (1..8 ranks per
+        // thread) so no CTA serialises a level's evaluation.  Levels without heavy
+        // sets need no global order, so each CTA gets one equal contiguous chunk
+        // of ranks (tpc tiles); heavy levels interleave tiles over CTAs so the
+        // look-back chain stays short.
+        const unsigned int per_cta = (nranks + gridDim.x - 1) / gridDim.x;
+        const unsigned int tpc = (per_cta + blockDim.x * kFusedRanksPerThread - 1) / (blockDim.x * kFusedRanksPerThread);
+        unsigned int rpt = heavy_level ? (nranks + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x)
+                                       : (per_cta + tpc * blockDim.x - 1) / (tpc * blockDim.x);
         rpt = rpt < 1 ? 1 : (rpt > kFusedRanksPerThread ? kFusedRanksPerThread : rpt);
         const unsigned int tile_ranks = rpt * blockDim.x;
         const unsigned long long ntiles = (nranks + tile_ranks - 1) / tile_ranks;
-        const bool heavy_level = (p.heavy_levels >> k) & 1ull;
         const unsigned long long item = p.item_of[k];
         const unsigned long long epoch = ((p.q->epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
         unsigned long long pairs = 0, nccp = 0, nprobe = 0, nlight = 0;
 
         // static tile assignment (all CTAs are co-resident, so the look-back
         // still makes progress); no ticket atomics on the critical path
-        for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const unsigned long long t_first = heavy_level ? blockIdx.x : (unsigned long long)blockIdx.x * tpc;
+        const unsigned long long t_step = heavy_level ? gridDim.x : 1;
+        const unsigned long long t_end = heavy_level ? ntiles
+                                         : ((unsigned long long)(blockIdx.x + 1) * tpc < ntiles ? (unsigned long long)(blockIdx.x + 1) * tpc : ntiles);
+        for (unsigned long long tile = t_first; tile < t_end; tile += t_step) {
             TRACE(1);
 
             // ---- unrank + filter + classify (registers only)
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_fused(const __grid_constant__ 
         grid_sync(p.gbar, &p.result->error);
         TRACE(6);
 
-        if (heavy_level) {
+        if (CLS != CLS_TREE && heavy_level) {
             // card(S) of every heavy set once (one thread per set)
             if (threadIdx.x == 0) d = p.desc[k];
             __syncthreads();
