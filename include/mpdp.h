@@ -110,7 +110,12 @@ typedef struct {
 
 typedef struct {
     int device;                    /* CUDA device ordinal                              */
-    int rank, world;               /* multi-GPU SPMD rank / size (1 process per GPU)   */
+    int rank, world;               /* multi-GPU SPMD rank / size (1 process per GPU).
+                                      world > 1: every level with >= 16384 k-subsets is
+                                      split into `world` contiguous colex-rank shares;
+                                      after the level each rank's memo segment is
+                                      allgathered (ncclAllGather, in place); smaller
+                                      levels are computed redundantly by every rank   */
     const void* nccl_unique_id;    /* 128 bytes (mpdp_nccl_get_unique_id on rank 0,
                                       broadcast by the caller); NULL when world == 1  */
     void* cuda_stream;             /* cudaStream_t to run on, or NULL (own stream)     */
@@ -138,6 +143,12 @@ typedef struct {
 /* flags: do not use the single persistent cooperative kernel for the level
  * loop (perfect-hash memo); launch per-level kernels instead (ablation)        */
 #define MPDP_FLAG_NO_FUSED 16u
+/* flags: world > 1 WITHOUT NCCL: the context runs all `world` ranks as shards
+ * (memo replicas) on its own device and exchanges the sharded levels by
+ * device copies -- the sharded code path minus the NCCL transport (testing)   */
+#define MPDP_FLAG_SIMULATE_WORLD 32u
+/* flags: shard every level across ranks, even small ones (testing)             */
+#define MPDP_FLAG_SHARD_ALL_LEVELS 64u
 
 typedef struct mpdp_ctx mpdp_ctx;
 
@@ -182,9 +193,11 @@ int mpdp_debug_trace(const mpdp_ctx* ctx, unsigned long long* out, int cap);
 /* Multi-GPU bootstrap: 128-byte NCCL unique id (call on rank 0 only). */
 mpdp_status mpdp_nccl_get_unique_id(void* out128);
 
-/* Contiguous share [lo, hi) of `total` work units for `rank` of `world`
- * (the per-level partition of the connected-set list). Pure host
- * arithmetic, exported so multi-process host logic is testable on CPU. */
+/* Contiguous share [lo, hi) of the `total` colex ranks of a level for `rank`
+ * of `world`: equal segments of ceil(total/world) (the last ones may be short
+ * or empty), so the sharded memo segments can be allgathered in place
+ * (SURVEY §8(e)).  Pure host arithmetic, used by the sharded level loop and
+ * exported so the multi-process host logic is testable on CPU. */
 void mpdp_share(uint64_t total, int rank, int world, uint64_t* lo, uint64_t* hi);
 
 #ifdef __cplusplus

@@ -16,6 +16,7 @@ constexpr int kSinkPairs = 2;        // join pairs whose memo probes are issued 
 constexpr int kLightBlock = 128;     // k_eval_light CTA size
 constexpr int kLightMinBlocks = 5;   // k_eval_light occupancy target -> <= 102 registers
 constexpr int kMaxN = 56;            // exact path bound (masks <= 2^56 ranks)
+constexpr int kMaxShards = 16;       // simulated multi-GPU world (one device)
 
 enum GraphClass : int { CLS_TREE = 0, CLS_CLIQUE = 1, CLS_GENERAL = 2 };
 

@@ -102,10 +102,13 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 #else
 #define TRACE(tag)
 #endif
-    for (int k = 2; k <= n; k++) {
+    for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
         TRACE(0);
-        const unsigned int nranks = bin[n * 33 + k];
+        // this launch evaluates the colex ranks [lo, hi) of level k (its share)
+        const unsigned int lo = p.share_lo[k], r_hi = p.share_hi[k];
+        const unsigned int nranks = r_hi - lo;
+        const bool counting = (p.count_levels >> k) & 1ull;
         const bool heavy_level = CLS != CLS_TREE && ((p.heavy_levels >> k) & 1ull);
         // Tiles.  Small levels are spread over the whole grid (1..8 ranks per
         // thread) so no CTA serialises a level's evaluation.  Levels without heavy
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
         const unsigned int tile_ranks = rpt * blockDim.x;
         const unsigned long long ntiles = (nranks + tile_ranks - 1) / tile_ranks;
         const unsigned long long item = p.item_of[k];
-        const unsigned long long epoch = ((p.q->epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
+        const unsigned long long epoch = lookback_epoch(p, k);
         unsigned long long pairs = 0, nccp = 0, nprobe = 0, nlight = 0;
 
         // static tile assignment (all CTAs are co-resident, so the look-back
@@ -133,16 +136,16 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             TRACE(1);
 
             // ---- unrank + filter + classify (registers only)
-            const unsigned int r0 = (unsigned int)(tile * tile_ranks) + threadIdx.x * rpt;
+            const unsigned int r0 = lo + (unsigned int)(tile * tile_ranks) + threadIdx.x * rpt;
             M S0 = 0;
             unsigned int lflag = 0, hflag = 0;
             Tri mine = {0, 0, 0};
-            if (r0 < nranks) {
+            if (r0 < r_hi) {
                 S0 = unrank_colex32(bin, n, k, r0);
                 M S = S0;
 #pragma unroll
                 for (int i = 0; i < kFusedRanksPerThread; i++) {
-                    if (i < (int)rpt && r0 + i < nranks) {
+                    if (i < (int)rpt && r0 + i < r_hi) {
                         if (connected_cls<M, CLS>(q, S, k)) {
                             unsigned long long w;
                             set_kind<M, CLS>(q, S, k, w);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                                 mine.w += w;
                             }
                         }
-                        if (i + 1 < (int)rpt && r0 + i + 1 < nranks) S = gosper(S);
+                        if (i + 1 < (int)rpt && r0 + i + 1 < r_hi) S = gosper(S);
                     }
                 }
             }
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                         wi += w;
                         hi++;
                     }
-                    if (r0 + i + 1 < nranks && i + 1 < (int)rpt) S = gosper(S);
+                    if (r0 + i + 1 < r_hi && i + 1 < (int)rpt) S = gosper(S);
                 }
             }
             __syncthreads();
@@ -270,8 +273,10 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             __syncthreads();                   // queue and scan scratch reused next tile
             TRACE(4);
         }
-        if (threadIdx.x == 0 && nlight) atomicAdd(&p.desc[k].n_light, nlight);
-        flush_counters(&p.desc[k], pairs, nccp, nprobe);
+        if (counting) {
+            if (threadIdx.x == 0 && nlight) atomicAdd(&p.desc[k].n_light, nlight);
+            flush_counters(&p.desc[k], pairs, nccp, nprobe);
+        }
         TRACE(5);
         grid_sync(p.gbar, &p.result->error);
         TRACE(6);
@@ -287,11 +292,11 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             grid_sync(p.gbar, &p.result->error);
             unsigned long long hp = 0, hc = 0, hpr = 0;
             heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, hp, hc, hpr);
-            flush_counters(&p.desc[k], hp, hc, hpr);
+            if (counting) flush_counters(&p.desc[k], hp, hc, hpr);
             grid_sync(p.gbar, &p.result->error);
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
         p.result->t_level[n + 1] = globaltimer_ns();
         extract_phase<M, MEMO>(p, q, v, rtab, gen);
     }

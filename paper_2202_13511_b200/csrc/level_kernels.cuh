@@ -28,7 +28,7 @@ struct __align__(16) LevelDesc {
 };
 
 struct __align__(64) TileRec {            // decoupled look-back record (ring slot)
-    unsigned long long flag;               // tile << 24 | epoch22 << 2 | state (1 aggregate, 2 inclusive)
+    unsigned long long flag;               // tile << 28 | epoch26 << 2 | state (1 aggregate, 2 inclusive)
     unsigned long long agg_l, agg_h, agg_w;
     unsigned long long inc_l, inc_h, inc_w, pad;
 };
@@ -66,6 +66,12 @@ template <typename M> struct Params {
     unsigned int* gbar;                    // fused kernel: grid barrier {count, generation}
     unsigned long long heavy_levels;       // bit k: level k can have heavy sets
     unsigned long long item_of[kMaxN + 1]; // heavy work-item size per level
+    // fused kernel, multi-GPU sharding: levels [k_begin, k_end]
+    // of this launch, the colex-rank share [share_lo, share_hi) of each level
+    // this rank evaluates, which levels it counts, and whether it extracts
+    int k_begin, k_end, do_extract, epoch_salt;   // salt: shard index (look-back epochs)
+    unsigned long long count_levels;
+    unsigned int share_lo[kMaxN + 1], share_hi[kMaxN + 1];
     int n;
     int memo_kind;                         // MEMO_HASH / MEMO_DENSE
     double inv_load;                       // HASH: buckets = ceil(count * inv_load / 2)
@@ -202,6 +208,15 @@ __device__ __forceinline__ Tri block_scan(Tri v, Tri& total) {
     return Tri{base.l + inc.l - v.l, base.h + inc.h - v.h, base.w + inc.w - v.w};
 }
 
+// Look-back records are tagged with (tile, epoch); the epoch is unique per
+// (query, level, local shard) over a window of 2^15 queries (the host clears
+// the ring before it wraps), so a reader never takes a stale record.
+template <typename M>
+__device__ __forceinline__ unsigned long long lookback_epoch(const Params<M>& p, int k) {
+    return (((p.q->epoch + (unsigned long long)k) * kMaxShards + (unsigned long long)p.epoch_salt) &
+            ((1ull << 26) - 1)) << 2;
+}
+
 // Warp-parallel decoupled look-back (warp 0 of the CTA): lanes read the flags of
 // the 32 preceding tiles at once; the exclusive prefix is the sum of aggregates
 // back to the nearest tile that already published its inclusive prefix.
@@ -209,7 +224,7 @@ __device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask
                                         unsigned long long epoch, Tri agg, unsigned int* err) {
     const int lane = threadIdx.x & 31;
     TileRec* tr = tiles + (tile & rmask);
-    const unsigned long long me = (tile << 24) | epoch;
+    const unsigned long long me = (tile << 28) | epoch;
     if (lane == 0) {
         if (tile == 0) {
             tr->inc_l = agg.l;
@@ -233,7 +248,7 @@ __device__ __forceinline__ Tri lookback(TileRec* tiles, unsigned long long rmask
         bool ready = true, inc = true;
         if (jj >= 0) {
             const unsigned long long f = ld_acquire(&pr->flag);
-            const bool mine = (f & ~3ull) == (((unsigned long long)jj << 24) | epoch);
+            const bool mine = (f & ~3ull) == (((unsigned long long)jj << 28) | epoch);
             ready = mine && (f & 3ull) != 0;
             inc = mine && (f & 3ull) == 2;
         }
@@ -291,7 +306,7 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
     for (int i = threadIdx.x; i < n * NB; i += blockDim.x) binom[i] = p.q->binom[i];
     if (threadIdx.x == 0) q.n = n;
     const unsigned long long rmask = p.tiles_ring - 1;
-    const unsigned long long epoch = ((p.q->epoch + (unsigned long long)k) & ((1ull << 22) - 1)) << 2;
+    const unsigned long long epoch = lookback_epoch(p, k);
 
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&p.desc[k].tile_ticket, 1u);
@@ -767,12 +782,18 @@ __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView
                               unsigned int gen) {
     ResultDev* r = p.result;
     const int n = p.n;
-    unsigned long long csg = (unsigned long long)n, ccp = 0, pairs = 0, probes = 0;
+    // bit 1 of count_levels: this rank counts the n singletons (level 1)
+    const unsigned long long n1 = ((p.count_levels >> 1) & 1ull) ? (unsigned long long)n : 0ull;
+    unsigned long long csg = n1, ccp = 0, pairs = 0, probes = 0;
     r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
-    r->lvl_csg[1] = (unsigned long long)n;
+    r->lvl_csg[1] = n1;
     r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
     for (int j = 2; j <= n; j++) {
         const LevelDesc& d = p.desc[j];
+        if (!((p.count_levels >> j) & 1ull)) {   // sharded run: another rank counts level j
+            r->lvl_csg[j] = r->lvl_ccp[j] = r->lvl_pairs[j] = 0;
+            continue;
+        }
         r->lvl_csg[j] = d.n_light + d.n_heavy;
         r->lvl_ccp[j] = d.ccp;
         r->lvl_pairs[j] = d.pairs;

@@ -31,15 +31,78 @@ struct DevLayout {
            hcard = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
+    // multi-GPU sharding: per local shard its own level descriptors, result and
+    // perfect-hash memo replica (shard 0 = the fields above)
+    int nshards = 1;
+    size_t sh_desc[kMaxShards] = {}, sh_result[kMaxShards] = {}, sh_dcost[kMaxShards] = {}, sh_dleft[kMaxShards] = {};
     unsigned long long list_cap = 0, heavy_cap = 0, tiles_cap = 0, fh_cap = 0, arena_buckets = 0;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// ---- NCCL, loaded at run time (only multi-GPU contexts need it).  The few
+// declarations below mirror nccl.h of NCCL 2.x; the library torch ships
+// (nvidia-nccl, 2.28) is the one already mapped into the process.
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclUint32 = 3, kNcclUint64 = 5, kNcclFloat64 = 8 };
+enum { kNcclSum = 0, kNcclMax = 2 };
+struct NcclApi {
+    void* lib = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl_api(std::string& err) {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) {
+        if (!api.lib) err = "libnccl.so.2 could not be loaded";
+        return api.lib ? &api : nullptr;
+    }
+    tried = true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+        api.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+        if (api.lib) break;
+    }
+    if (!api.lib) {
+        err = "libnccl.so.2 could not be loaded";
+        return nullptr;
+    }
+#define NCCL_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(api.lib, "nccl" #f))
+    NCCL_SYM(GetUniqueId);
+    NCCL_SYM(CommInitRank);
+    NCCL_SYM(CommDestroy);
+    NCCL_SYM(AllGather);
+    NCCL_SYM(AllReduce);
+    NCCL_SYM(GroupStart);
+    NCCL_SYM(GroupEnd);
+    NCCL_SYM(GetErrorString);
+#undef NCCL_SYM
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.AllReduce || !api.GroupStart || !api.GroupEnd) {
+        err = "libnccl.so.2 lacks required symbols";
+        api.lib = nullptr;
+        return nullptr;
+    }
+    return &api;
+}
+
 }  // namespace
 
 struct mpdp_ctx {
     int device = 0, rank = 0, world = 1;
+    bool simulate = false;                // world ranks simulated as shards on this device
+    NcclApi* nccl = nullptr;
+    ncclComm_t comm = nullptr;
+    ResultDev* h_results = nullptr;       // pinned, one per local shard
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     unsigned char* ws = nullptr;
@@ -66,6 +129,7 @@ struct mpdp_ctx {
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
     int fused_occ[3] = {}, fused_n[3] = {};
     bool fused = false;                  // last run used the fused kernel
+    bool sharded = false;                // last run used the sharded (multi-GPU) path
     int occ_n[2][3][2] = {};
     unsigned int flags = 0;
     double load_factor = 0.5;
@@ -255,9 +319,15 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
         off += bytes;
         return at;
     };
+    const int W = c->world, nsh = c->simulate ? c->world : 1;
+    L.nshards = nsh;
     L.query = take(sizeof(QueryDev<uint64_t>));
-    L.desc = take(sizeof(LevelDesc) * (kMaxN + 1));
-    L.result = take(sizeof(ResultDev));
+    for (int sh = 0; sh < nsh; sh++) {
+        L.sh_desc[sh] = take(sizeof(LevelDesc) * (kMaxN + 1));
+        L.sh_result[sh] = take(sizeof(ResultDev));
+    }
+    L.desc = L.sh_desc[0];
+    L.result = L.sh_result[0];
     L.gbar = take(64);
     L.rank = take(sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25));
     off = align_up(off, 256);
@@ -267,16 +337,26 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     const size_t memo0 = off;
     // memo region (fixed position): DENSE = cost[] + left[] over all C(n,k);
     // HASH = buckets + cold left[] (geometry fixed per mask width)
+    // dense levels are padded by W entries so that W equal rank segments of
+    // ceil(C(n,k)/W) fit (in-place allgather of the sharded levels)
     unsigned long long dense_entries = 0;
-    for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k);
+    for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k) + (unsigned long long)W;
+    const size_t dense_bytes = align_up(8 * dense_entries, 256) + align_up(4 * dense_entries, 256);
     const bool dense_ok = !c->wide && !(c->flags & MPDP_FLAG_HASH_MEMO) &&
-                          dense_entries * 12 + 1024 <= memo_bytes;
+                          (size_t)nsh * dense_bytes + 1024 <= memo_bytes;
     L.memo_kind = dense_ok ? MEMO_DENSE : MEMO_HASH;
+    if (W > 1 && !dense_ok)
+        return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs the perfect-hash memo (n <= 32) and " +
+                                              std::to_string(nsh * dense_bytes >> 20) + " MiB of memo space");
     const unsigned long long buckets = (unsigned long long)(memo_bytes / (sizeof(Bucket) + 2 * msz));
     L.arena = take(sizeof(Bucket) * buckets);
     L.cold = take(2 * msz * buckets);
-    L.dcost = memo0;
-    L.dleft = align_up(memo0 + 8 * dense_entries, 256);
+    for (int sh = 0; sh < nsh; sh++) {
+        L.sh_dcost[sh] = memo0 + sh * dense_bytes;
+        L.sh_dleft[sh] = align_up(L.sh_dcost[sh] + 8 * dense_entries, 256);
+    }
+    L.dcost = L.sh_dcost[0];
+    L.dleft = L.sh_dleft[0];
     L.memo_end = off;
     const size_t scratch0 = align_up(off, 256);
     const size_t scratch = c->ws_bytes - scratch0 - 1024;
@@ -314,21 +394,21 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
 }
 
 template <typename M>
-static Params<M> make_params(mpdp_ctx* c) {
+static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     Params<M> p;
     memset(&p, 0, sizeof(p));
     unsigned char* b = c->ws;
     const DevLayout& L = c->lay;
     p.q = reinterpret_cast<const QueryDev<M>*>(b + L.query);
-    p.desc = reinterpret_cast<LevelDesc*>(b + L.desc);
+    p.desc = reinterpret_cast<LevelDesc*>(b + L.sh_desc[shard]);
     p.memo.arena = reinterpret_cast<Bucket*>(b + L.arena);
     p.memo.cold = b + L.cold;
     p.memo.arena_buckets = L.arena_buckets;
-    p.memo.dcost = reinterpret_cast<double*>(b + L.dcost);
-    p.memo.dleft = reinterpret_cast<unsigned int*>(b + L.dleft);
+    p.memo.dcost = reinterpret_cast<double*>(b + L.sh_dcost[shard]);
+    p.memo.dleft = reinterpret_cast<unsigned int*>(b + L.sh_dleft[shard]);
     p.memo.rank_tab = reinterpret_cast<const unsigned int*>(b + L.rank);
     p.memo.rg = rank_geom(c->n <= 32 ? c->n : 32);
-    p.memo.error = &reinterpret_cast<ResultDev*>(b + L.result)->error;
+    p.memo.error = &reinterpret_cast<ResultDev*>(b + L.sh_result[shard])->error;
     p.memo_kind = L.memo_kind;
     p.gbar = reinterpret_cast<unsigned int*>(b + L.gbar);
     p.heavy_levels = 0;
@@ -339,7 +419,16 @@ static Params<M> make_params(mpdp_ctx* c) {
     unsigned long long acc = 0;
     for (int k = 0; k <= kMaxN; k++) {
         p.dense_off[k] = acc;
-        if (k >= 2 && k <= c->n) acc += binom_u64(c->n, k);
+        if (k >= 2 && k <= c->n) acc += binom_u64(c->n, k) + (unsigned long long)c->world;   // + padding
+    }
+    // single-launch defaults: every level, whole rank space, counted, extracted
+    p.k_begin = 2;
+    p.k_end = c->n;
+    p.do_extract = 1;
+    p.count_levels = ~0ull;
+    for (int k = 0; k <= kMaxN; k++) {
+        p.share_lo[k] = 0;
+        p.share_hi[k] = (k >= 2 && k <= c->n) ? (unsigned int)binom_u64(c->n, k) : 0u;
     }
     p.light = reinterpret_cast<M*>(b + L.light);
     p.heavy = reinterpret_cast<M*>(b + L.heavy);
@@ -353,7 +442,8 @@ static Params<M> make_params(mpdp_ctx* c) {
     p.tiles_ring = L.tiles_cap;
     p.list_cap = L.list_cap;
     p.heavy_cap = L.heavy_cap;
-    p.result = reinterpret_cast<ResultDev*>(b + L.result);
+    p.result = reinterpret_cast<ResultDev*>(b + L.sh_result[shard]);
+    p.epoch_salt = shard;
     p.n = c->n;
     p.inv_load = 1.0 / c->load_factor;
     return p;
@@ -469,8 +559,146 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     return MPDP_OK;
 }
 
+// ------------------------------------------------------------ sharded run
+// Multi-GPU: per level k, rank r evaluates the colex ranks
+// [r*seg, (r+1)*seg) of the level (seg = ceil(C(n,k)/W)) with the fused kernel
+// restricted to that share; its memo entries are then one contiguous segment
+// of the level's perfect-hash array, so the exchange is an in-place
+// ncclAllGather of `seg` costs and `seg` left masks per rank -- no packing and
+// no replica insert.  Levels below kShardMinRanks are computed redundantly by
+// every rank (counted by rank 0 only).  Counters are summed with one
+// ncclAllReduce at the end; every rank extracts the identical plan from its
+// complete replica.  In simulated mode the ranks are shards of this context
+// and the transport is device-to-device copies.
+constexpr unsigned long long kShardMinRanks = 1ull << 14;
+
+static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k, unsigned long long C,
+                                  unsigned long long seg) {
+    const unsigned long long off = P[0].dense_off[k];
+    const int W = c->world;
+    if (c->simulate) {
+        for (int s = 0; s < W; s++) {
+            const unsigned long long lo = std::min(C, s * seg), hi = std::min(C, (s + 1) * seg);
+            if (hi <= lo) continue;
+            for (int t = 0; t < W; t++) {
+                if (t == s) continue;
+                CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dcost + off + lo, P[s].memo.dcost + off + lo, (hi - lo) * 8,
+                                            cudaMemcpyDeviceToDevice, c->stream));
+                CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dleft + off + lo, P[s].memo.dleft + off + lo, (hi - lo) * 4,
+                                            cudaMemcpyDeviceToDevice, c->stream));
+            }
+        }
+        return MPDP_OK;
+    }
+    double* dc = P[0].memo.dcost + off;
+    unsigned int* dl = P[0].memo.dleft + off;
+    ncclResult_t r = c->nccl->GroupStart();
+    if (!r) r = c->nccl->AllGather(dc + c->rank * seg, dc, seg, kNcclFloat64, c->comm, c->stream);
+    if (!r) r = c->nccl->AllGather(dl + c->rank * seg, dl, seg, kNcclUint32, c->comm, c->stream);
+    const ncclResult_t r2 = c->nccl->GroupEnd();
+    if (r || r2) return fail(c, MPDP_ERR_NCCL, "ncclAllGather of level " + std::to_string(k) + " failed");
+    return MPDP_OK;
+}
+
+template <int CLS>
+static mpdp_status run_sharded(mpdp_ctx* c) {
+    if (c->wide || c->lay.memo_kind != MEMO_DENSE)
+        return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
+    const int n = c->n, W = c->world, nsh = c->lay.nshards;
+    const size_t smem = sizeof(SQ<uint32_t>) +
+                        sizeof(unsigned int) * (rank_geom(n).entries + 33 * 33 + 2 * kFusedTile);
+    int& occ = c->fused_occ[CLS];
+    if (!occ || c->fused_n[CLS] != n) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_fused<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_fused<CLS>, kBlock, smem));
+        if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
+        c->fused_n[CLS] = n;
+    }
+    const unsigned long long full = (unsigned long long)c->num_sms * occ;
+    std::vector<Params<uint32_t>> P(nsh);
+    std::vector<unsigned long long> counted(nsh, 0);
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    c->launches = 0;
+    for (int sh = 0; sh < nsh; sh++) {
+        P[sh] = make_params<uint32_t>(c, sh);
+        k_init<uint32_t><<<1, 64, 0, c->stream>>>(P[sh]);
+        c->launches++;
+    }
+    auto launch = [&](Params<uint32_t>& p, unsigned long long grid) -> mpdp_status {
+        void* args[] = {&p};
+        CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3((unsigned int)grid), dim3(kBlock),
+                                                args, smem, c->stream));
+        c->launches++;
+        return MPDP_OK;
+    };
+    const unsigned long long min_shard = (c->flags & MPDP_FLAG_SHARD_ALL_LEVELS) ? 0ull : kShardMinRanks;
+    for (int k = 2; k <= n; k++) {
+        const unsigned long long C = binom_u64(n, k);
+        const bool sharded = W > 1 && C >= min_shard;
+        const unsigned long long seg = (C + W - 1) / W;
+        for (int sh = 0; sh < nsh; sh++) {
+            const int rank = c->simulate ? sh : c->rank;
+            Params<uint32_t>& p = P[sh];
+            p.k_begin = p.k_end = k;
+            p.do_extract = 0;
+            uint64_t lo = 0, hi = C;
+            if (sharded) mpdp_share(C, rank, W, &lo, &hi);
+            p.share_lo[k] = (unsigned int)lo;
+            p.share_hi[k] = (unsigned int)hi;
+            const bool counts = sharded || rank == 0;
+            p.count_levels = counts ? (1ull << k) : 0ull;
+            if (counts) counted[sh] |= 1ull << k;
+            if (hi <= lo) continue;
+            unsigned long long grid = std::max<unsigned long long>(1, (hi - lo + 511) / 512);
+            grid = std::max(grid, heavy_pair_bound(n, k, CLS) / ((unsigned long long)W * 16384));
+            if (CLS == CLS_GENERAL) grid = full;
+            const mpdp_status st = launch(p, std::min(grid, full));
+            if (st != MPDP_OK) return st;
+        }
+        if (sharded) {
+            const mpdp_status st = exchange_level(c, P.data(), k, C, seg);
+            if (st != MPDP_OK) return st;
+        }
+        CUDA_TRY(c, cudaGetLastError());
+    }
+    for (int sh = 0; sh < nsh; sh++) {                  // extraction from each complete replica
+        const int rank = c->simulate ? sh : c->rank;
+        Params<uint32_t>& p = P[sh];
+        p.k_begin = n + 1;
+        p.k_end = n;
+        p.do_extract = 1;
+        p.count_levels = counted[sh] | (rank == 0 ? 2ull : 0ull);
+        const mpdp_status st = launch(p, 1);
+        if (st != MPDP_OK) return st;
+    }
+    if (!c->simulate) {                                 // sum the per-rank counters
+        ResultDev* r = reinterpret_cast<ResultDev*>(c->ws + c->lay.sh_result[0]);
+        ncclResult_t e = c->nccl->GroupStart();
+        if (!e) e = c->nccl->AllReduce(&r->csg, &r->csg, 4, kNcclUint64, kNcclSum, c->comm, c->stream);
+        if (!e) e = c->nccl->AllReduce(r->lvl_csg, r->lvl_csg, 3 * (kMaxN + 1), kNcclUint64, kNcclSum, c->comm, c->stream);
+        if (!e) e = c->nccl->AllReduce(&r->n_nodes, &r->n_nodes, 2, kNcclUint32, kNcclMax, c->comm, c->stream);
+        const ncclResult_t e2 = c->nccl->GroupEnd();
+        if (e || e2) return fail(c, MPDP_ERR_NCCL, "ncclAllReduce of the counters failed");
+    }
+    for (int sh = 0; sh < nsh; sh++)
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_results + sh, c->ws + c->lay.sh_result[sh], sizeof(ResultDev),
+                                    cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->enum_launches = 0;
+    c->eval_launches = (unsigned int)(nsh * (n - 1));
+    c->nkev = 0;
+    c->d2h_bytes = sizeof(ResultDev) * nsh;
+    c->sharded = true;
+    return MPDP_OK;
+}
+
 template <typename M, int CLS, int MEMO>
 static mpdp_status run_query(mpdp_ctx* c) {
+    c->sharded = false;
+    if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
+        if (c->world > 1) return run_sharded<CLS>(c);
+    }
+    if (c->world > 1) return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
     c->fused = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
@@ -566,9 +794,9 @@ const char* mpdp_last_error(const mpdp_ctx* ctx) {
 
 void mpdp_share(uint64_t total, int rank, int world, uint64_t* lo, uint64_t* hi) {
     if (world < 1) world = 1;
-    const unsigned __int128 t = total;
-    *lo = (uint64_t)(t * (unsigned)rank / (unsigned)world);
-    *hi = (uint64_t)(t * (unsigned)(rank + 1) / (unsigned)world);
+    const uint64_t seg = (total + (uint64_t)world - 1) / (uint64_t)world;   // equal segments (in-place allgather)
+    *lo = std::min<uint64_t>(total, (uint64_t)rank * seg);
+    *hi = std::min<uint64_t>(total, (uint64_t)(rank + 1) * seg);
 }
 
 mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
@@ -576,8 +804,11 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
     *out = nullptr;
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
         return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "bad rank/world");
-    if (cfg->world > 1)
-        return fail(nullptr, MPDP_ERR_UNSUPPORTED, "multi-GPU contexts are not enabled in this build");
+    const bool simulate = cfg->world > 1 && (cfg->flags & MPDP_FLAG_SIMULATE_WORLD);
+    if (simulate && (cfg->rank != 0 || cfg->world > kMaxShards))
+        return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "simulated world: rank must be 0 and world <= 16");
+    if (cfg->world > 1 && !simulate && !cfg->nccl_unique_id)
+        return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(nullptr, MPDP_ERR_CUDA, "no CUDA device (this library has no CPU path)");
@@ -588,6 +819,7 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
     c->device = cfg->device;
     c->rank = cfg->rank;
     c->world = cfg->world;
+    c->simulate = simulate;
     c->timeout_ms = cfg->timeout_ms;
     c->flags = cfg->flags;
     if (cfg->load_factor > 0.0) c->load_factor = cfg->load_factor;
@@ -620,9 +852,22 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
     }
     if (cudaMemsetAsync(c->ws, 0, c->ws_bytes, c->stream) != cudaSuccess)
         return bail(fail(nullptr, MPDP_ERR_CUDA, "workspace clear failed"));
+    const int nsh = simulate ? cfg->world : 1;
     if (cudaMallocHost(&c->h_query, sizeof(QueryDev<uint64_t>)) != cudaSuccess ||
-        cudaMallocHost(&c->h_result, sizeof(ResultDev)) != cudaSuccess)
+        cudaMallocHost(&c->h_results, sizeof(ResultDev) * nsh) != cudaSuccess)
         return bail(fail(nullptr, MPDP_ERR_OOM, "pinned host allocation failed"));
+    c->h_result = c->h_results;
+    if (cfg->world > 1 && !simulate) {     // one NCCL communicator per context
+        std::string err;
+        c->nccl = nccl_api(err);
+        if (!c->nccl) return bail(fail(nullptr, MPDP_ERR_NCCL, err));
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        const ncclResult_t r = c->nccl->CommInitRank(&c->comm, cfg->world, id, cfg->rank);
+        if (r != 0)
+            return bail(fail(nullptr, MPDP_ERR_NCCL, std::string("ncclCommInitRank: ") +
+                                                         (c->nccl->GetErrorString ? c->nccl->GetErrorString(r) : "")));
+    }
     cudaEventCreate(&c->ev0);
     cudaEventCreate(&c->ev1);
     for (auto& e : c->kev) cudaEventCreate(&e);
@@ -636,7 +881,8 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->own_ws && c->ws) cudaFree(c->ws);
     if (c->h_query) cudaFreeHost(c->h_query);
-    if (c->h_result) cudaFreeHost(c->h_result);
+    if (c->comm && c->nccl && c->nccl->CommDestroy) c->nccl->CommDestroy(c->comm);
+    if (c->h_results) cudaFreeHost(c->h_results);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto& e : c->kev)
@@ -701,8 +947,8 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
         c->rank_n = n;
     }
     c->query_counter++;
-    // look-back epochs are 22 bits wide (query * 64 + level): recycle the ring
-    // records before an epoch value can repeat
+    // look-back epochs are 26 bits wide ((query * 64 + level) * 16 + shard):
+    // recycle the ring records before an epoch value can repeat
     if ((c->query_counter & ((1ull << 15) - 1)) == 0)
         CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.tiles, 0, sizeof(TileRec) * c->lay.tiles_cap, c->stream));
     if (c->wide) {
@@ -735,6 +981,26 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
         return fail(c, MPDP_ERR_INVALID_ARGUMENT, "result capacity < 2n-1");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     CUDA_TRY(c, cudaGetLastError());
+    if (c->sharded && c->simulate) {      // sum the shards' counters; all shards must agree on the plan
+        ResultDev* r0 = c->h_results;
+        for (int sh = 1; sh < c->lay.nshards; sh++) {
+            const ResultDev* rs = c->h_results + sh;
+            r0->error |= rs->error;
+            r0->csg += rs->csg;
+            r0->ccp += rs->ccp;
+            r0->pairs += rs->pairs;
+            r0->probes += rs->probes;
+            for (int k = 0; k <= n; k++) {
+                r0->lvl_csg[k] += rs->lvl_csg[k];
+                r0->lvl_ccp[k] += rs->lvl_ccp[k];
+                r0->lvl_pairs[k] += rs->lvl_pairs[k];
+            }
+            if (!r0->error && (rs->n_nodes != r0->n_nodes ||
+                               memcmp(rs->nodes, r0->nodes, sizeof(mpdp_plan_node) * r0->n_nodes) != 0 ||
+                               memcmp(&rs->cost, &r0->cost, sizeof(double)) != 0))
+                return fail(c, MPDP_ERR_INTERNAL, "simulated ranks extracted different plans");
+        }
+    }
     const ResultDev* r = c->h_result;
     if (r->error) {
         if (r->error & ERR_HANG)
@@ -819,7 +1085,14 @@ int mpdp_debug_trace(const mpdp_ctx* c, unsigned long long* out, int cap) {
 
 mpdp_status mpdp_nccl_get_unique_id(void* out128) {
     if (!out128) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "out is NULL");
-    return fail(nullptr, MPDP_ERR_UNSUPPORTED, "multi-GPU contexts are not enabled in this build");
+    std::string err;
+    NcclApi* api = nccl_api(err);
+    if (!api) return fail(nullptr, MPDP_ERR_NCCL, err);
+    ncclUniqueId id;
+    const ncclResult_t r = api->GetUniqueId(&id);
+    if (r != 0) return fail(nullptr, MPDP_ERR_NCCL, "ncclGetUniqueId failed");
+    memcpy(out128, &id, sizeof(id));
+    return MPDP_OK;
 }
 
 }  // extern "C"

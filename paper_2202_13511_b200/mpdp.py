@@ -61,6 +61,8 @@ FLAG_PROFILE_KERNELS = 2
 FLAG_HASH_MEMO = 4
 FLAG_NO_GRAPH = 8
 FLAG_NO_FUSED = 16
+FLAG_SIMULATE_WORLD = 32
+FLAG_SHARD_ALL_LEVELS = 64
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",
@@ -197,7 +199,8 @@ class Context:
 
     def __init__(self, device: int = 0, workspace_bytes: int = 4 << 30, timeout_ms: float = 0.0,
                  use_torch: bool = True, stream: Optional[int] = None, flags: int = 0,
-                 load_factor: float = 0.0):
+                 load_factor: float = 0.0, rank: int = 0, world: int = 1,
+                 nccl_unique_id: Optional[bytes] = None):
         L = load_library()
         self._ws = None
         self.stream = None
@@ -215,7 +218,9 @@ class Context:
                 # which the C ABI reads as "create your own")
                 self.stream = torch.cuda.Stream(device=device)
                 stream_ptr = self.stream.cuda_stream
-        cfg = mpdp_ctx_config(device, 0, 1, None, stream_ptr, workspace_bytes, timeout_ms,
+        self._uid = (C.c_char * 128).from_buffer_copy(nccl_unique_id) if nccl_unique_id else None
+        cfg = mpdp_ctx_config(device, rank, world, C.cast(self._uid, C.c_void_p) if self._uid else None,
+                              stream_ptr, workspace_bytes, timeout_ms,
                               ws_ptr, workspace_bytes if ws_ptr else 0, flags, load_factor)
         h = C.c_void_p()
         st = L.mpdp_ctx_create(C.byref(cfg), C.byref(h))
@@ -263,6 +268,16 @@ class Context:
 
     def __exit__(self, *a):
         self.close()
+
+
+def mpdp_nccl_get_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it)."""
+    buf = (C.c_char * 128)()
+    L = load_library()
+    st = L.mpdp_nccl_get_unique_id(C.cast(buf, C.c_void_p))
+    if st != OK:
+        raise MPDPError(st, L.mpdp_last_error(None).decode())
+    return bytes(buf)
 
 
 def mpdp_share(total: int, rank: int, world: int):

@@ -65,11 +65,10 @@ def test_bad_config_rejected(lib):
 def test_share_partitions_exactly(lib, world, total):
     from paper_2202_13511_b200 import mpdp
     prev = 0
-    sizes = []
+    seg = (total + world - 1) // world
     for r in range(world):
         lo, hi = mpdp.mpdp_share(total, r, world)
-        assert lo == prev and hi >= lo
-        sizes.append(hi - lo)
+        assert lo == prev and hi >= lo and hi - lo <= seg
+        assert lo == min(total, r * seg)          # in-place allgather: segment r at r*seg
         prev = hi
     assert prev == total
-    assert max(sizes) - min(sizes) <= 1

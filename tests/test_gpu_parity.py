@@ -222,3 +222,27 @@ def test_fused_and_per_level_kernels_agree(topo, n, seed):
             check(r, o, g)
             if flags == 0:
                 assert r.gpu_launches == 2          # k_init + the fused level loop
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("topo,n,seed", [("star", 12, 0), ("clique", 13, 1), ("cycle", 13, 2),
+                                         ("random", 14, 3), ("snowflake", 16, 4)])
+def test_sharded_world_all_levels(world, topo, n, seed):
+    """The multi-GPU sharded level loop (per-level colex-rank shares + in-place
+    segment exchange + counter reduction), with `world` ranks simulated as memo
+    replicas on one device and EVERY level sharded (shares down to empty)."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate(topo, n, seed)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, world=world,
+                      flags=mpdp.FLAG_SIMULATE_WORLD | mpdp.FLAG_SHARD_ALL_LEVELS) as c:
+        check(c.mpdp_optimize(g), O.optimize(g), g)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_world_default_threshold(world):
+    from paper_2202_13511_b200 import mpdp
+    for g in (W.star(20, 1), W.clique(15, 2)):
+        o = O.optimize_dpccp(g)
+        with mpdp.Context(device=0, workspace_bytes=2 << 30, world=world, flags=mpdp.FLAG_SIMULATE_WORLD) as c:
+            r = c.mpdp_optimize(g)
+            check(r, o, g)
