@@ -61,7 +61,8 @@ typedef enum {
  * is relation v. */
 typedef struct {
     uint32_t n;                    /* relations, 1..56 for exact algorithms          */
-    const double* cardinalities;   /* [n], finite, > 0                               */
+    const double* cardinalities;   /* [n], finite, >= 0 (0 = empty input; composite
+                                      cards of huge sub-plans can underflow to 0)     */
     uint32_t n_edges;
     const uint32_t* edges;         /* [2*n_edges] pairs {u, v}: u < v < n, no dups    */
     const double* selectivities;   /* [n_edges], in (0, 1]                            */
@@ -103,6 +104,7 @@ typedef struct {
     uint32_t eval_launches;        /* out: k_eval launches                            */
     uint32_t memo_kind;            /* out: 1 = perfect-hash (colex rank) memo,
                                            0 = Murmur3 open-addressing memo          */
+    uint32_t inner_calls;          /* out, IDP2/UnionDP: inner exact DP calls          */
     double* level_ms;              /* optional [n+1]: device time of each level (fused
                                       kernel: %globaltimer at the level barriers; 0 on
                                       the per-level-kernel path)                       */
@@ -164,7 +166,7 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* ctx);
  * Blocks until the result is in *out.
  *   algo MPDP: k must be 0.  IDP2_MPDP / UNIONDP_MPDP: 2 <= k <= 25.
  * Errors: INVALID_ARGUMENT (NULL pointers, n == 0, u >= v, v >= n, duplicate
- * edge, selectivity outside (0,1], cardinality <= 0 or non-finite, negative or
+ * edge, selectivity outside (0,1], cardinality < 0 or non-finite, negative or
  * non-finite leaf cost, out->capacity < 2n-1 with out->nodes != NULL, sum of
  * log10 cardinalities > 300), DISCONNECTED, CAPACITY (n > 56, memo larger than
  * the budget), TIMEOUT, CUDA, UNSUPPORTED (DPSIZE_REF).  On error *out is left
@@ -180,6 +182,30 @@ mpdp_status mpdp_optimize(mpdp_ctx* ctx, const mpdp_query_graph* graph, mpdp_alg
 mpdp_status mpdp_stage(mpdp_ctx* ctx, const mpdp_query_graph* graph);
 mpdp_status mpdp_run(mpdp_ctx* ctx);
 mpdp_status mpdp_fetch(mpdp_ctx* ctx, mpdp_result* out);
+
+/* ---- IDP2 / UnionDP (algo IDP2_MPDP / UNIONDP_MPDP) ------------
+ * Heuristic plans for large queries (n up to 2^20; plan node `set` masks are
+ * only filled when n <= 64).  The driver repeatedly solves sub-problems of at
+ * most k relations exactly with the GPU MPDP (composite nodes carry
+ * card = card of their subplan and leaf_cost = its cost).  result: the final
+ * plan, its C_out cost recomputed over the whole tree, the counters summed over
+ * the inner DP calls, inner_calls, and host wall time in time_ms.
+ *
+ * With MPDP_FLAG_RECORD_SUBPROBLEMS the context keeps every inner sub-problem
+ * of the last call; mpdp_subproblem_get returns its graph (pointers into the
+ * context, valid until the next call) and its result (nodes copied when
+ * result->nodes != NULL and capacity suffices).                               */
+#define MPDP_FLAG_RECORD_SUBPROBLEMS 128u
+int mpdp_subproblem_count(const mpdp_ctx* ctx);
+mpdp_status mpdp_subproblem_get(const mpdp_ctx* ctx, uint32_t i, mpdp_query_graph* graph,
+                                mpdp_result* result);
+
+/* The IDP2/UnionDP driver with a caller-supplied inner exact solver (host
+ * logic only, no device needed; the product path is mpdp_optimize).  Used by
+ * the tests to check the driver on machines without a GPU. */
+typedef mpdp_status (*mpdp_inner_solver)(void* user, const mpdp_query_graph* sub, mpdp_result* out);
+mpdp_status mpdp_heuristic_optimize(const mpdp_query_graph* graph, mpdp_algo algo, uint32_t k,
+                                    mpdp_inner_solver solver, void* user, mpdp_result* out);
 
 /* Thread-local description of the last error on this context (never NULL). */
 const char* mpdp_last_error(const mpdp_ctx* ctx);

@@ -54,7 +54,7 @@ static int load_graph(const oracle_graph* in, G* g) {
     g->n = (int)in->n;
     for (int v = 0; v < g->n; v++) {
         double c = in->card[v];
-        if (!(c > 0.0) || !isfinite(c)) return ORACLE_ERR_ARG;
+        if (!(c >= 0.0) || !isfinite(c)) return ORACLE_ERR_ARG;   /* reading R18: 0 allowed */
         g->card[v] = c;
         g->leaf[v] = in->leaf_cost ? in->leaf_cost[v] : 0.0;
         if (!isfinite(g->leaf[v]) || g->leaf[v] < 0.0) return ORACLE_ERR_ARG;

@@ -23,7 +23,7 @@ extern "C" {
 
 typedef struct {
     uint32_t n;                 /* relations, 1..64 (optimisers: 1..28)        */
-    const double* card;         /* [n] base cardinalities, > 0                 */
+    const double* card;         /* [n] base cardinalities, >= 0 (R18)          */
     uint32_t n_edges;
     const uint32_t* edges;      /* [2*n_edges] pairs {u, v}, u < v             */
     const double* sel;          /* [n_edges] selectivities in (0, 1]           */

@@ -8,11 +8,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmpdp.so")
-SOURCES = ["mpdp_abi.cu"]
+SOURCES = ["mpdp_abi.cu", "heuristics.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-fmad=false",                   # reading R6: no FMA contraction anywhere
               "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared",
-              f"-I{os.path.join(ROOT, 'include')}"]
+              f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 
 def _stale():

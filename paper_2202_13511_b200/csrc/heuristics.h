@@ -1,0 +1,11 @@
+// heuristics.h — internal interface of the IDP2 / UnionDP drivers.
+#pragma once
+#include <string>
+
+#include "mpdp.h"
+
+namespace mpdp_heur {
+typedef mpdp_status (*InnerSolver)(void* user, const mpdp_query_graph* sub, mpdp_result* out);
+mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolver solve, void* user,
+                mpdp_result* out, std::string& err);
+}  // namespace mpdp_heur

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "fused.cuh"
+#include "heuristics.h"
 
 using namespace mpdp;
 
@@ -130,6 +131,13 @@ struct mpdp_ctx {
     int fused_occ[3] = {}, fused_n[3] = {};
     bool fused = false;                  // last run used the fused kernel
     bool sharded = false;                // last run used the sharded (multi-GPU) path
+    struct SubProblem {                  // MPDP_FLAG_RECORD_SUBPROBLEMS
+        std::vector<double> card, sel, leaf;
+        std::vector<uint32_t> edges;
+        std::vector<mpdp_plan_node> nodes;
+        mpdp_result res;
+    };
+    std::vector<SubProblem> subs;
     int occ_n[2][3][2] = {};
     unsigned int flags = 0;
     double load_factor = 0.5;
@@ -189,8 +197,8 @@ static mpdp_status validate(mpdp_ctx* c, const mpdp_query_graph* g, std::vector<
     double lsum = 0;
     for (int v = 0; v < n; v++) {
         const double x = g->cardinalities[v];
-        if (!(x > 0.0) || !std::isfinite(x))
-            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "cardinality[" + std::to_string(v) + "] not finite > 0");
+        if (!(x >= 0.0) || !std::isfinite(x))
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "cardinality[" + std::to_string(v) + "] not finite >= 0");
         lsum += std::log10(std::max(x, 1.0));
         if (g->leaf_costs && (!(g->leaf_costs[v] >= 0.0) || !std::isfinite(g->leaf_costs[v])))
             return fail(c, MPDP_ERR_INVALID_ARGUMENT, "leaf_costs[" + std::to_string(v) + "] not finite >= 0");
@@ -766,8 +774,68 @@ static mpdp_status run_typed(mpdp_ctx* c) {
     return run_memo<M, MEMO_HASH>(c);
 }
 
+// ------------------------------------------------------------ heuristics
+extern "C" mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo, uint32_t k,
+                                     mpdp_result* out);
+
+// inner exact DP of IDP2/UnionDP: the GPU MPDP on the same context
+static mpdp_status gpu_inner_solver(void* user, const mpdp_query_graph* sub, mpdp_result* out) {
+    mpdp_ctx* c = static_cast<mpdp_ctx*>(user);
+    const mpdp_status st = mpdp_optimize(c, sub, MPDP_ALGO_MPDP, 0, out);
+    if (st == MPDP_OK && (c->flags & MPDP_FLAG_RECORD_SUBPROBLEMS)) {
+        mpdp_ctx::SubProblem sp;
+        sp.card.assign(sub->cardinalities, sub->cardinalities + sub->n);
+        sp.sel.assign(sub->selectivities, sub->selectivities + sub->n_edges);
+        sp.edges.assign(sub->edges, sub->edges + 2 * sub->n_edges);
+        if (sub->leaf_costs) sp.leaf.assign(sub->leaf_costs, sub->leaf_costs + sub->n);
+        sp.nodes.assign(out->nodes, out->nodes + out->n_nodes);
+        sp.res = *out;
+        sp.res.nodes = nullptr;
+        sp.res.level_csg = sp.res.level_ccp = sp.res.level_pairs = nullptr;
+        sp.res.level_ms = nullptr;
+        c->subs.push_back(std::move(sp));
+    }
+    return st;
+}
+
 // ------------------------------------------------------------ C ABI
 extern "C" {
+
+int mpdp_subproblem_count(const mpdp_ctx* c) { return c ? (int)c->subs.size() : 0; }
+
+mpdp_status mpdp_subproblem_get(const mpdp_ctx* c, uint32_t i, mpdp_query_graph* g, mpdp_result* r) {
+    if (!c || i >= c->subs.size()) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "no such sub-problem");
+    const mpdp_ctx::SubProblem& sp = c->subs[i];
+    if (g) {
+        g->n = (uint32_t)sp.card.size();
+        g->cardinalities = sp.card.data();
+        g->n_edges = (uint32_t)sp.sel.size();
+        g->edges = sp.edges.data();
+        g->selectivities = sp.sel.data();
+        g->leaf_costs = sp.leaf.empty() ? nullptr : sp.leaf.data();
+    }
+    if (r) {
+        mpdp_plan_node* nodes = r->nodes;
+        const uint32_t cap = r->capacity;
+        *r = sp.res;
+        r->nodes = nodes;
+        r->capacity = cap;
+        if (nodes && cap >= sp.nodes.size()) memcpy(nodes, sp.nodes.data(), sizeof(mpdp_plan_node) * sp.nodes.size());
+    }
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_heuristic_optimize(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k,
+                                    mpdp_inner_solver solver, void* user, mpdp_result* out) {
+    if (!solver) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "solver is NULL");
+    if (algo != MPDP_ALGO_IDP2_MPDP && algo != MPDP_ALGO_UNIONDP_MPDP)
+        return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "algo must be IDP2_MPDP or UNIONDP_MPDP");
+    std::string err;
+    const mpdp_status st = mpdp_heur::run(g, algo, k, solver, user, out, err);
+    if (st != MPDP_OK) return fail(nullptr, st, err);
+    return MPDP_OK;
+}
+
 
 int mpdp_abi_version(void) { return MPDP_ABI_VERSION; }
 
@@ -1060,8 +1128,13 @@ mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo
                         "DPSIZE_REF is the CPU reference; it lives in the test oracle (oracle/liboracle.so), "
                         "not in this GPU library");
         case MPDP_ALGO_IDP2_MPDP:
-        case MPDP_ALGO_UNIONDP_MPDP:
-            return fail(c, MPDP_ERR_UNSUPPORTED, "IDP2/UnionDP drivers are not built yet");
+        case MPDP_ALGO_UNIONDP_MPDP: {
+            c->subs.clear();
+            std::string err;
+            const mpdp_status st = mpdp_heur::run(g, algo, k, gpu_inner_solver, c, out, err);
+            if (st != MPDP_OK) return fail(c, st, err.empty() ? c->err : err);
+            return MPDP_OK;
+        }
         default:
             return fail(c, MPDP_ERR_INVALID_ARGUMENT, "unknown algorithm");
     }

@@ -46,7 +46,8 @@ class mpdp_result(C.Structure):
                 ("probes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("enum_ms", C.c_double), ("eval_ms", C.c_double),
                 ("enum_launches", C.c_uint32), ("eval_launches", C.c_uint32),
-                ("memo_kind", C.c_uint32), ("level_ms", C.POINTER(C.c_double))]
+                ("memo_kind", C.c_uint32), ("inner_calls", C.c_uint32),
+                ("level_ms", C.POINTER(C.c_double))]
 
 
 class mpdp_ctx_config(C.Structure):
@@ -63,11 +64,13 @@ FLAG_NO_GRAPH = 8
 FLAG_NO_FUSED = 16
 FLAG_SIMULATE_WORLD = 32
 FLAG_SHARD_ALL_LEVELS = 64
+FLAG_RECORD_SUBPROBLEMS = 128
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",
            "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
-           "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace"]
+           "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace", "mpdp_subproblem_count",
+           "mpdp_subproblem_get", "mpdp_heuristic_optimize"]
 
 _lib = None
 
@@ -142,6 +145,7 @@ class Result:
     eval_launches: int = 0
     memo_kind: int = 0
     level_ms: List[float] = field(default_factory=list)
+    inner_calls: int = 0
 
     def tree(self):
         """Nested tuples: leaves are relation ids, internal nodes (left, right)."""
@@ -190,7 +194,7 @@ class ResultBuf:
         return Result(r.cost, nodes, r.pairs_evaluated, r.ccp_pairs, r.csg_count,
                       list(self.lc), list(self.lx), list(self.lp), r.time_ms, r.gpu_launches,
                       r.probes, r.h2d_bytes, r.d2h_bytes, r.enum_ms, r.eval_ms,
-                      r.enum_launches, r.eval_launches, r.memo_kind, list(self.lt))
+                      r.enum_launches, r.eval_launches, r.memo_kind, list(self.lt), r.inner_calls)
 
 
 class Context:

@@ -125,6 +125,7 @@ def test_edge_cases(ctx):
     assert e.value.status == mpdp.ERR_DISCONNECTED
     for bad in [W.QueryGraph(2, [4.0, 8.0], [(0, 1)], [0.0]),
                 W.QueryGraph(2, [4.0, -8.0], [(0, 1)], [0.5]),
+                W.QueryGraph(2, [4.0, float("inf")], [(0, 1)], [0.5]),
                 W.QueryGraph(2, [4.0, 8.0], [(1, 0)], [0.5]),
                 W.QueryGraph(3, [4.0, 8.0, 1.0], [(0, 1), (0, 1), (1, 2)], [0.5, 0.5, 0.5])]:
         with pytest.raises(mpdp.MPDPError) as e:
