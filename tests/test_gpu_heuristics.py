@@ -1,0 +1,87 @@
+"""IDP2 / UnionDP on the GPU (BASELINE config 5 shape): every inner sub-problem
+the GPU MPDP solved is re-solved by the oracle and must match it exactly
+(north_star: "matching the oracle on every inner subproblem"), and the final
+plans are valid with consistent costs."""
+import ctypes as C
+
+import pytest
+
+from oracle import pyoracle as O
+import workload as W
+from test_gpu_parity import check
+from test_heuristics_cpu import recompute
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rctx():
+    from paper_2202_13511_b200 import mpdp
+    with mpdp.Context(device=0, workspace_bytes=2 << 30, flags=mpdp.FLAG_RECORD_SUBPROBLEMS) as c:
+        yield c
+
+
+def subproblems(ctx):
+    from paper_2202_13511_b200 import mpdp
+    L = mpdp.load_library()
+    out = []
+    for i in range(L.mpdp_subproblem_count(ctx.h)):
+        sg = mpdp.mpdp_query_graph()
+        L.mpdp_subproblem_get(ctx.h, i, C.byref(sg), None)
+        n, m = sg.n, sg.n_edges
+        q = W.QueryGraph(n, [sg.cardinalities[j] for j in range(n)],
+                         [(sg.edges[2 * j], sg.edges[2 * j + 1]) for j in range(m)],
+                         [sg.selectivities[j] for j in range(m)],
+                         leaf_cost=[sg.leaf_costs[j] for j in range(n)] if sg.leaf_costs else None)
+        rb = mpdp.ResultBuf(n)
+        L.mpdp_subproblem_get(ctx.h, i, None, rb.ref())
+        r = rb.to_result()
+        r.level_csg = r.level_ccp = r.level_pairs = None
+        out.append((q, r))
+    return out
+
+
+def check_sub(q, r):
+    o = O.optimize(q)
+    assert r.cost == o.cost
+    assert r.tree() == O.tree_of(o.nodes)
+    assert (r.csg_count, r.ccp_pairs, r.pairs_evaluated) == (o.csg_count, o.ccp_pairs, o.pairs_evaluated)
+
+
+@pytest.mark.parametrize("algo", ["IDP2_MPDP", "UNIONDP_MPDP"])
+@pytest.mark.parametrize("n,k,seed", [(60, 12, 0), (150, 14, 1), (400, 16, 2)])
+def test_every_inner_subproblem_matches_oracle(rctx, algo, n, k, seed):
+    g = W.snowflake(n, seed)
+    res = rctx.mpdp_optimize(g, algo=algo, k=k)
+    assert recompute(g, res) == res.cost
+    subs = subproblems(rctx)
+    assert len(subs) == res.inner_calls >= 1
+    for q, r in subs:
+        assert q.n <= k
+        check_sub(q, r)
+
+
+@pytest.mark.parametrize("algo", ["IDP2_MPDP", "UNIONDP_MPDP"])
+def test_config5_thousand_relations_k25(rctx, algo):
+    """BASELINE config 5: 1000-relation snowflake, k = 25.  Every inner
+    sub-problem with <= 22 relations is re-solved by the oracle (larger ones are
+    checked on their counters' closed-form invariants: trees waste no pairs)."""
+    g = W.snowflake(1000, 0)
+    res = rctx.mpdp_optimize(g, algo=algo, k=25)
+    assert recompute(g, res) == res.cost
+    subs = subproblems(rctx)
+    assert len(subs) == res.inner_calls
+    for q, r in subs:
+        assert q.n <= 25
+        if q.n <= 22:
+            check_sub(q, r)
+        else:
+            assert r.pairs_evaluated == r.ccp_pairs            # Lemma 8 on tree sub-problems
+
+
+def test_heuristic_small_query_equals_exact(rctx):
+    g = W.random_connected(14, 5, extra=0.3)
+    o = O.optimize(g)
+    for algo in ("IDP2_MPDP", "UNIONDP_MPDP"):
+        r = rctx.mpdp_optimize(g, algo=algo, k=20)
+        assert abs(r.cost - o.cost) <= 1e-9 * o.cost
