@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     unsigned int* qrank = qmask + kFusedTile;
     __shared__ MemoView v;
     __shared__ LevelDesc d;
-    __shared__ unsigned long long s_tile;
+    __shared__ unsigned long long s_next;
     __shared__ Tri s_excl, s_agg;
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
@@ -97,7 +97,10 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 
 #ifdef MPDP_TRACE
     int trace_i = 0;
-#define TRACE(tag) if (blockIdx.x == 0 && threadIdx.x == 0 && trace_i < kTraceCap) \
+#ifndef MPDP_TRACE_KMIN
+#define MPDP_TRACE_KMIN 0
+#endif
+#define TRACE(tag) if (blockIdx.x == 0 && threadIdx.x == 0 && trace_i < kTraceCap && k >= MPDP_TRACE_KMIN) \
         p.result->trace[trace_i++] = (globaltimer_ns() << 8) | ((unsigned long long)k << 3) | (unsigned long long)(tag)
 #else
 #define TRACE(tag)
@@ -111,32 +114,35 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
         const bool counting = (p.count_levels >> k) & 1ull;
         const bool heavy_level = CLS != CLS_TREE && ((p.heavy_levels >> k) & 1ull);
         // Tiles.  Small levels are spread over the whole grid (1..8 ranks per
-        // thread) so no CTA serialises a level's evaluation.  Levels without heavy
-        // sets need no global order, so each CTA gets one equal contiguous chunk
-        // of ranks (tpc tiles); heavy levels interleave tiles over CTAs so the
-        // look-back chain stays short.
-        const unsigned int per_cta = (nranks + gridDim.x - 1) / gridDim.x;
-        const unsigned int tpc = (per_cta + blockDim.x * kFusedRanksPerThread - 1) / (blockDim.x * kFusedRanksPerThread);
-        unsigned int rpt = heavy_level ? (nranks + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x)
-                                       : (per_cta + tpc * blockDim.x - 1) / (tpc * blockDim.x);
+        // thread) so no CTA serialises a level's evaluation.  Heavy levels
+        // interleave tiles statically over CTAs so the look-back chain stays
+        // short.  Other levels hand out tiles dynamically: CTA b starts with
+        // tile b, then claims the next tile from a per-level counter; the claim
+        // for the next tile is issued at the START of the current one, so its
+        // latency hides behind the tile.  Static equal chunks are unbalanced
+        // because the density of connected sets varies along colex order (star:
+        // the sets with maximum element j contain the hub with probability
+        // (k-1)/j).  (Guided self-scheduling with shrinking chunks measured
+        // slower: the per-tile enumeration overhead outweighs the better tail.)
+        unsigned int rpt = (nranks + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
         rpt = rpt < 1 ? 1 : (rpt > kFusedRanksPerThread ? kFusedRanksPerThread : rpt);
         const unsigned int tile_ranks = rpt * blockDim.x;
         const unsigned long long ntiles = (nranks + tile_ranks - 1) / tile_ranks;
         const unsigned long long item = p.item_of[k];
         const unsigned long long epoch = lookback_epoch(p, k);
         unsigned long long pairs = 0, nccp = 0, nprobe = 0, nlight = 0;
+        const unsigned long long dyn_base = (unsigned long long)gridDim.x * tile_ranks;
 
-        // static tile assignment (all CTAs are co-resident, so the look-back
-        // still makes progress); no ticket atomics on the critical path
-        const unsigned long long t_first = heavy_level ? blockIdx.x : (unsigned long long)blockIdx.x * tpc;
-        const unsigned long long t_step = heavy_level ? gridDim.x : 1;
-        const unsigned long long t_end = heavy_level ? ntiles
-                                         : ((unsigned long long)(blockIdx.x + 1) * tpc < ntiles ? (unsigned long long)(blockIdx.x + 1) * tpc : ntiles);
-        for (unsigned long long tile = t_first; tile < t_end; tile += t_step) {
+        unsigned long long tile = blockIdx.x;                  // heavy levels: tile index
+        unsigned long long t0 = tile * tile_ranks;             // first rank (offset from lo) of this tile
+        while (t0 < nranks) {
+            unsigned long long next_t0 = t0 + dyn_base;
+            if (!heavy_level && threadIdx.x == 0 && nranks > dyn_base)
+                next_t0 = dyn_base + atomicAdd(&p.desc[k].tile_ticket, tile_ranks);   // consumed at the end
             TRACE(1);
 
             // ---- unrank + filter + classify (registers only)
-            const unsigned int r0 = lo + (unsigned int)(tile * tile_ranks) + threadIdx.x * rpt;
+            const unsigned int r0 = lo + (unsigned int)t0 + threadIdx.x * rpt;
             M S0 = 0;
             unsigned int lflag = 0, hflag = 0;
             Tri mine = {0, 0, 0};
@@ -245,6 +251,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                         const unsigned long long idx = v.off[k] + qrank[e];
                         p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
                         p.memo.dleft[idx] = (unsigned int)best.l;
+                        p.memo.dcard[idx] = sink.cS;
                     }
                 }
             }
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                 pairs += w;
                 if constexpr (CLS == CLS_TREE) {
                     if (k > 2) {
-                        eval_tree_dense<MEMO>(p.memo, gen, v, rtab, bin, q, S, k, nprobe);
+                        eval_tree_dense<MEMO>(p.memo, gen, v, rtab, bin, q, S, k, qrank[e], nprobe);
                         nccp += w;
                         continue;
                     }
@@ -268,9 +275,15 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                 const unsigned long long idx = v.off[k] + qrank[e];
                 p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
                 p.memo.dleft[idx] = (unsigned int)sink.best.l;
+                p.memo.dcard[idx] = sink.cS;
             }
-            if (threadIdx.x == 0) nlight += nq;
+            if (threadIdx.x == 0) {
+                nlight += nq;
+                s_next = next_t0;
+            }
             __syncthreads();                   // queue and scan scratch reused next tile
+            t0 = s_next;
+            tile += gridDim.x;
             TRACE(4);
         }
         if (counting) {

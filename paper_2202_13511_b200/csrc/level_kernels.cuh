@@ -501,31 +501,28 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
 }
 
 // Tree fast path (CLS_TREE, DENSE memo; 32-bit masks).  For a set S with
-// elements p_0 < ... < p_{k-1}, rank(S) = sum_i C(p_i, i+1) and removing a
-// single element p_m gives
-//     rank(S \ {p_m}) = rank(S) - C(p_m, m+1) - sum_{i>m} (C(p_i, i+1) - C(p_i, i)),
+// elements p_0 < ... < p_{k-1} and colex rank R = sum_i C(p_i, i+1) (passed in:
+// the fused kernel knows it from the enumeration), removing a single element
+// p_m gives
+//     rank(S \ {p_m}) = R - C(p_m, m+1) - sum_{i>m} (C(p_i, i+1) - C(p_i, i)),
 // so every split of S along an edge (v, parent v) whose lower side is the single
 // vertex v (all splits of a star) costs two binomial lookups instead of a rank
-// computation; card(S) (reading R5) is folded into the same ascending pass and
-// rank(S) is reused for the insert.  Other splits go through the generic sink.
+// computation.  Other splits go through the generic sink.
+//
+// card(S) comes from the memo: reading R5's product is a left fold over the
+// ascending elements in which the factors of p_0..p_{k-2} only involve edges
+// among them, so for p = p_{k-1} = max(S)
+//     card(S) = (..((card(S \ {p}) * card[p]) * sel(u_1, p)) * ..)   (u_i in S, u_i < p, ascending)
+// bit for bit.  S \ {p} is connected (and therefore in the level k-1 memo)
+// exactly when p is a leaf split of G[S], which is the first element of the
+// descending walk; its card load travels with the first batch of probes.
+// Otherwise the product is evaluated in full.
 template <int MEMO>
 __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int gen, const MemoView& v,
                                                 const unsigned int* rtab, const unsigned int* bin, const SQ<uint32_t>& q,
-                                                uint32_t S, int k, unsigned long long& nprobe) {
+                                                uint32_t S, int k, unsigned int R, unsigned long long& nprobe) {
     constexpr int BS = 33;                 // binomial row stride
     constexpr int U = 4;                   // elements per unrolled step = probes in flight
-    // ---- ascending pass: rank(S) and card(S)
-    unsigned int R = 0;
-    double x = 1.0;
-    int i = 0;
-    for (uint32_t T = S; T; T &= T - 1, i++) {
-        const int vtx = __ffs(T) - 1;
-        R += bin[vtx * BS + i + 1];
-        x = __dmul_rn(x, q.card[vtx]);
-        for (uint32_t W = S & q.adj[vtx] & ((1u << vtx) - 1u); W; W &= W - 1)
-            x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + vtx]);
-    }
-    const double cS = x;
     uint32_t top = 0;
     for (int d = 0; d <= q.max_depth; d++) {
         const uint32_t T = S & q.depth_mask[d];
@@ -537,13 +534,15 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
     double best_c = __longlong_as_double(0x7ff0000000000000ll);
     uint32_t best_l = 0xffffffffu;
     const bool leaf_costs = q.pad != 0;    // any non-zero leaf cost in this query
-    // ---- descending pass, U elements per step: leaf splits with incremental
+    // ---- descending walk, U elements per step: leaf splits with incremental
     // ranks, all their probes issued before any is consumed; splits at
     // internal vertices are only recorded here
     const double* lvl = P.dcost + v.off[k - 1];
     unsigned int SD = 0;
     uint32_t internal = 0;
     int m = k - 1;
+    double cS = 0.0;
+    bool first = true;
     for (uint32_t T = S; T;) {
         unsigned int rk[U];
         uint32_t lb[U];
@@ -571,6 +570,26 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
         double dv[U];
 #pragma unroll
         for (int u = 0; u < U; u++) dv[u] = lb[u] ? lvl[rk[u]] : 0.0;
+        if (first) {                       // lb[0] / rk[0] belong to max(S)
+            first = false;
+            const int p = 31 - __clz(S);
+            double x;
+            if (lb[0]) {
+                x = __dmul_rn(P.dcard[v.off[k - 1] + rk[0]], q.card[p]);
+            } else {
+                x = 1.0;
+                for (uint32_t A = S ^ (1u << p); A; A &= A - 1) {
+                    const int a = __ffs(A) - 1;
+                    x = __dmul_rn(x, q.card[a]);
+                    for (uint32_t W = S & q.adj[a] & ((1u << a) - 1u); W; W &= W - 1)
+                        x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + a]);
+                }
+                x = __dmul_rn(x, q.card[p]);
+            }
+            for (uint32_t W = S & q.adj[p] & ((1u << p) - 1u); W; W &= W - 1)
+                x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + p]);
+            cS = x;
+        }
 #pragma unroll
         for (int u = 0; u < U; u++) {
             if (lb[u]) {
@@ -602,6 +621,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
     const unsigned long long idx = v.off[k] + R;
     P.dcost[idx] = __longlong_as_double((long long)best.c);
     P.dleft[idx] = (unsigned int)best.l;
+    P.dcard[idx] = cS;
 }
 
 // Shared prologue of the evaluate / extract kernels: the query, the memo view
@@ -669,7 +689,8 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(con
             const int kind = set_kind<M, CLS>(q, S, k, w);
             if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE && sizeof(M) == 4) {
                 if (k > 2) {                   // k = 2: both sides are leaves (no level-1 table)
-                    eval_tree_dense<MEMO>(p.memo, gen, v, rtab, rtab + p.memo.rg.entries, q, S, k, nprobe);
+                    eval_tree_dense<MEMO>(p.memo, gen, v, rtab, rtab + p.memo.rg.entries, q, S, k,
+                                           rank_of(p.memo.rg, rtab, S), nprobe);
                     nccp += w;
                     pairs += w;
                     continue;
@@ -681,7 +702,7 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(con
             sink.flush();
             nprobe += sink.nprobe;
             pairs += w;
-            memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, sink.best);
+            memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, sink.best, sink.cS);
         }
     }
     // card(S) of the heavy sets, one thread per set, for k_eval_heavy (next in
@@ -741,7 +762,7 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
             if (lane == 0) {
                 pairs += cnt;
                 if (a == 0 && b == w) {
-                    memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, best);
+                    memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, best, p.hcard[h]);
                 } else {
                     atomic_key_min(&p.bkey[h], best);
                     __threadfence();
@@ -750,7 +771,7 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                         __threadfence();
                         const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&p.bkey[h]);
                         const Key fin{ld_relaxed(kp), ld_relaxed(kp + 1)};
-                        memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, fin);
+                        memo_insert<M, MEMO>(p.memo, gen, v, rtab, k, S, fin, p.hcard[h]);
                     }
                 }
             }

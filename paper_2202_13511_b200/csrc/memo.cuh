@@ -64,6 +64,7 @@ struct MemoView {
 struct MemoPtrs {
     // DENSE
     double* dcost;                         // [sum_j C(n,j)] cost by (level offset + rank)
+    double* dcard;                         // [sum_j C(n,j)] card(S) (reading R5), same index
     unsigned int* dleft;                   // [sum_j C(n,j)] left(S) (32-bit masks)
     const unsigned int* rank_tab;          // [RankGeom::entries]
     // HASH
@@ -248,11 +249,12 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, unsigned int gen,
 // scatter (S, best(S)) into the level-k table
 template <typename M, int MEMO>
 __device__ __forceinline__ void memo_insert(const MemoPtrs& P, unsigned int gen, const MemoView& v,
-                                            const unsigned int* rtab, int k, M S, const Key& best) {
+                                            const unsigned int* rtab, int k, M S, const Key& best, double card) {
     if (MEMO == MEMO_DENSE) {
         const unsigned long long idx = v.off[k] + rank_of(P.rg, rtab, (uint32_t)S);
         P.dcost[idx] = __longlong_as_double((long long)best.c);
         P.dleft[idx] = (unsigned int)best.l;
+        P.dcard[idx] = card;
     } else {
         hash_insert(P, gen, v.off[k], v.nb[k], S, best);
     }

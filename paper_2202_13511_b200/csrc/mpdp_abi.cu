@@ -35,7 +35,8 @@ struct DevLayout {
     // multi-GPU sharding: per local shard its own level descriptors, result and
     // perfect-hash memo replica (shard 0 = the fields above)
     int nshards = 1;
-    size_t sh_desc[kMaxShards] = {}, sh_result[kMaxShards] = {}, sh_dcost[kMaxShards] = {}, sh_dleft[kMaxShards] = {};
+    size_t sh_desc[kMaxShards] = {}, sh_result[kMaxShards] = {}, sh_dcost[kMaxShards] = {}, sh_dleft[kMaxShards] = {},
+           sh_dcard[kMaxShards] = {};
     unsigned long long list_cap = 0, heavy_cap = 0, tiles_cap = 0, fh_cap = 0, arena_buckets = 0;
 };
 
@@ -343,13 +344,13 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     const size_t body = c->ws_bytes - off - 1024;
     const size_t memo_bytes = body * 3 / 4;
     const size_t memo0 = off;
-    // memo region (fixed position): DENSE = cost[] + left[] over all C(n,k);
+    // memo region (fixed position): DENSE = cost[] + card[] + left[] over all C(n,k);
     // HASH = buckets + cold left[] (geometry fixed per mask width)
     // dense levels are padded by W entries so that W equal rank segments of
     // ceil(C(n,k)/W) fit (in-place allgather of the sharded levels)
     unsigned long long dense_entries = 0;
     for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k) + (unsigned long long)W;
-    const size_t dense_bytes = align_up(8 * dense_entries, 256) + align_up(4 * dense_entries, 256);
+    const size_t dense_bytes = 2 * align_up(8 * dense_entries, 256) + align_up(4 * dense_entries, 256);
     const bool dense_ok = !c->wide && !(c->flags & MPDP_FLAG_HASH_MEMO) &&
                           (size_t)nsh * dense_bytes + 1024 <= memo_bytes;
     L.memo_kind = dense_ok ? MEMO_DENSE : MEMO_HASH;
@@ -361,7 +362,8 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.cold = take(2 * msz * buckets);
     for (int sh = 0; sh < nsh; sh++) {
         L.sh_dcost[sh] = memo0 + sh * dense_bytes;
-        L.sh_dleft[sh] = align_up(L.sh_dcost[sh] + 8 * dense_entries, 256);
+        L.sh_dcard[sh] = align_up(L.sh_dcost[sh] + 8 * dense_entries, 256);
+        L.sh_dleft[sh] = align_up(L.sh_dcard[sh] + 8 * dense_entries, 256);
     }
     L.dcost = L.sh_dcost[0];
     L.dleft = L.sh_dleft[0];
@@ -414,6 +416,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.memo.arena_buckets = L.arena_buckets;
     p.memo.dcost = reinterpret_cast<double*>(b + L.sh_dcost[shard]);
     p.memo.dleft = reinterpret_cast<unsigned int*>(b + L.sh_dleft[shard]);
+    p.memo.dcard = reinterpret_cast<double*>(b + L.sh_dcard[shard]);
     p.memo.rank_tab = reinterpret_cast<const unsigned int*>(b + L.rank);
     p.memo.rg = rank_geom(c->n <= 32 ? c->n : 32);
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.sh_result[shard])->error;
@@ -572,7 +575,8 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
 // [r*seg, (r+1)*seg) of the level (seg = ceil(C(n,k)/W)) with the fused kernel
 // restricted to that share; its memo entries are then one contiguous segment
 // of the level's perfect-hash array, so the exchange is an in-place
-// ncclAllGather of `seg` costs and `seg` left masks per rank -- no packing and
+// ncclAllGather of `seg` costs and `seg` left masks (plus `seg` cards on trees,
+// read by the tree fast path) per rank -- no packing and
 // no replica insert.  Levels below kShardMinRanks are computed redundantly by
 // every rank (counted by rank 0 only).  Counters are summed with one
 // ncclAllReduce at the end; every rank extracts the identical plan from its
@@ -581,7 +585,7 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
 constexpr unsigned long long kShardMinRanks = 1ull << 14;
 
 static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k, unsigned long long C,
-                                  unsigned long long seg) {
+                                  unsigned long long seg, bool with_card) {
     const unsigned long long off = P[0].dense_off[k];
     const int W = c->world;
     if (c->simulate) {
@@ -594,6 +598,9 @@ static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k,
                                             cudaMemcpyDeviceToDevice, c->stream));
                 CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dleft + off + lo, P[s].memo.dleft + off + lo, (hi - lo) * 4,
                                             cudaMemcpyDeviceToDevice, c->stream));
+                if (with_card)
+                    CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dcard + off + lo, P[s].memo.dcard + off + lo, (hi - lo) * 8,
+                                                cudaMemcpyDeviceToDevice, c->stream));
             }
         }
         return MPDP_OK;
@@ -603,6 +610,8 @@ static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k,
     ncclResult_t r = c->nccl->GroupStart();
     if (!r) r = c->nccl->AllGather(dc + c->rank * seg, dc, seg, kNcclFloat64, c->comm, c->stream);
     if (!r) r = c->nccl->AllGather(dl + c->rank * seg, dl, seg, kNcclUint32, c->comm, c->stream);
+    double* dk = P[0].memo.dcard + off;    // card(S) feeds the tree fast path only
+    if (!r && with_card) r = c->nccl->AllGather(dk + c->rank * seg, dk, seg, kNcclFloat64, c->comm, c->stream);
     const ncclResult_t r2 = c->nccl->GroupEnd();
     if (r || r2) return fail(c, MPDP_ERR_NCCL, "ncclAllGather of level " + std::to_string(k) + " failed");
     return MPDP_OK;
@@ -664,7 +673,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
             if (st != MPDP_OK) return st;
         }
         if (sharded) {
-            const mpdp_status st = exchange_level(c, P.data(), k, C, seg);
+            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, CLS == CLS_TREE);
             if (st != MPDP_OK) return st;
         }
         CUDA_TRY(c, cudaGetLastError());
