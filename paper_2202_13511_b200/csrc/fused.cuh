@@ -18,6 +18,7 @@ namespace mpdp {
 
 constexpr int kFusedRanksPerThread = 8;
 constexpr int kFusedTile = kBlock * kFusedRanksPerThread;   // 2048 ranks, queue of 2048 sets
+constexpr bool kDeferRemainder = false;     // defer nq mod blockDim light sets (else only nq < blockDim)
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
     unsigned int v;
@@ -74,6 +75,154 @@ __device__ __forceinline__ uint32_t unrank_colex32(const unsigned int* bin, int 
     return S;
 }
 
+
+// Min of a Key over aligned groups of G lanes (G a power of two <= 32); every
+// lane of the warp must call it.
+__device__ __forceinline__ Key group_min(Key k, unsigned int G) {
+    for (unsigned int o = 1; o < G; o <<= 1) {
+        Key t;
+        t.c = __shfl_xor_sync(0xffffffffu, k.c, o);
+        t.l = __shfl_xor_sync(0xffffffffu, k.l, o);
+        if (key_less(t, k)) k = t;
+    }
+    return k;
+}
+
+// card(S) for a set of level k >= 3 with colex rank R.  Reading R5's product is
+// a left fold over the ascending elements, so with p = max(S)
+//     card(S) = (..((card(S \ {p}) * card[p]) * sel(u_1, p)) * ..)   (u_i in S, u_i < p, ascending)
+// bit for bit; card(S \ {p}) is read from the level k-1 memo (colex rank
+// R - C(p, k)) when S \ {p} is connected: p is a leaf of G[S] on trees (S and
+// desc[p] meet only in p), always on cliques.  Otherwise the full product.
+template <int CLS>
+__device__ __forceinline__ double card_fast(const MemoPtrs& P, const MemoView& v, const unsigned int* bin,
+                                            const SQ<uint32_t>& q, uint32_t S, int k, unsigned int R) {
+    const int p = 31 - __clz(S);
+    const uint32_t b = 1u << p;
+    const bool in_memo = k >= 3 && ((CLS == CLS_TREE && (S & q.desc[p]) == b) || CLS == CLS_CLIQUE);
+    if (!in_memo) return card_of(q, S);
+    double x = __dmul_rn(P.dcard[v.off[k - 1] + (R - bin[p * 33 + k])], q.card[p]);
+    for (uint32_t W = S & q.adj[p] & (b - 1u); W; W &= W - 1) x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + p]);
+    return x;
+}
+
+// Deferred light sets of level k (tiles that found fewer sets than threads push
+// theirs to the grid-wide small list instead of evaluating them in place):
+// after the level barrier every CTA takes a share, G lanes per set with G the
+// largest power of two that still gives every set a group (G = 32: one warp
+// per set, lanes = join pairs).  Sparse and small levels thus use the whole
+// grid instead of the few CTAs whose tiles held the sets.
+struct DenseLocate {
+    __device__ __forceinline__ unsigned long long operator()(unsigned long long e) const { return e; }
+    __device__ __forceinline__ unsigned int seek(unsigned long long) const { return 0; }
+    __device__ __forceinline__ unsigned long long at(unsigned long long e, unsigned int&) const { return e; }
+};
+
+// One thread per set (G = 1): the CTA's run is walked in rounds of blockDim;
+// the next list entry is loaded before the current set is evaluated (the set
+// evaluation is a latency chain, the list load should not add to it).
+template <int CLS, typename Locate>
+__device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q,
+                                                   const MemoView& v, const unsigned int* rtab, const unsigned int* bin,
+                                                   unsigned int gen, const unsigned long long* list, const Locate& loc,
+                                                   unsigned long long c_lo, unsigned long long c_hi,
+                                                   unsigned long long& pairs, unsigned long long& nccp,
+                                                   unsigned long long& nprobe) {
+    constexpr int MEMO = MEMO_DENSE;
+    unsigned long long e = c_lo + threadIdx.x;
+    if (e >= c_hi) return;
+    unsigned int cur = loc.seek(e);
+    unsigned long long nxt = list[loc.at(e, cur)];
+    for (; e < c_hi; e += blockDim.x) {
+        const unsigned long long ent = nxt;
+        if (e + blockDim.x < c_hi) nxt = list[loc.at(e + blockDim.x, cur)];
+        const uint32_t S = (uint32_t)ent;
+        const unsigned int R = (unsigned int)(ent >> 32);
+        unsigned long long w;
+        const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
+        pairs += w;
+        if constexpr (CLS == CLS_TREE) {
+            if (k > 2) {
+                eval_tree_dense<MEMO>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe);
+                nccp += w;
+                continue;
+            }
+        }
+        PairSink<uint32_t, MEMO> sink;
+        sink.init(&p.memo, gen, &v, rtab, &q, card_fast<CLS>(p.memo, v, bin, q, S, k, R));
+        eval_range<uint32_t, CLS>(q, S, k, kind, 0, w, sink, nccp);
+        sink.flush();
+        nprobe += sink.nprobe;
+        const unsigned long long idx = v.off[k] + R;
+        p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
+        p.memo.dleft[idx] = (unsigned int)sink.best.l;
+        p.memo.dcard[idx] = sink.cS;
+    }
+}
+
+template <int CLS, typename Locate>
+__device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                            const unsigned int* rtab, const unsigned int* bin, unsigned int gen,
+                            const unsigned long long* list, const Locate& loc, unsigned long long nsmall,
+                            unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe) {
+    constexpr int MEMO = MEMO_DENSE;
+    const unsigned long long total = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned int G = 1;
+    while (G < 32 && 2ull * G * nsmall <= total) G <<= 1;
+    // CTA b takes the contiguous run [N*b/grid, N*(b+1)/grid) of the list, so
+    // consecutive rounds of a CTA evaluate colex-near sets whose subsets share
+    // L1 lines (the list is a concatenation of warp runs of consecutive ranks)
+    const unsigned long long c_lo = nsmall * blockIdx.x / gridDim.x, c_hi = nsmall * (blockIdx.x + 1) / gridDim.x;
+    if (G == 1) {
+        small_phase_thread<CLS>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe);
+        return;
+    }
+    const unsigned int sub = threadIdx.x & (G - 1);
+    const unsigned int gpc = blockDim.x / G;                 // groups per CTA
+    for (unsigned long long base = c_lo; base < c_hi; base += gpc) {      // same trip count on every lane
+        const unsigned long long e = base + threadIdx.x / G;
+        const bool act = e < c_hi;
+        const unsigned long long ent = act ? list[loc(e)] : 0ull;
+        const uint32_t S = (uint32_t)ent;
+        const unsigned int R = (unsigned int)(ent >> 32);
+        Key best = key_inf();
+        unsigned long long w = 0;
+        double cS = 0.0;
+        if (act) {
+            const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
+            cS = card_fast<CLS>(p.memo, v, bin, q, S, k, R);
+            PairSink<uint32_t, MEMO> sink;
+            sink.init(&p.memo, gen, &v, rtab, &q, cS);
+            const unsigned long long per = (w + G - 1) / G;
+            unsigned long long j0 = per * sub, j1 = j0 + per;
+            if (j0 > w) j0 = w;
+            if (j1 > w) j1 = w;
+            eval_range<uint32_t, CLS>(q, S, k, kind, j0, j1, sink, nccp);
+            sink.flush();
+            nprobe += sink.nprobe;
+            best = sink.best;
+        }
+        best = group_min(best, G);
+        if (act && sub == 0) {
+            pairs += w;
+            const unsigned long long idx = v.off[k] + R;
+            p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
+            p.memo.dleft[idx] = (unsigned int)best.l;
+            p.memo.dcard[idx] = cS;
+        }
+    }
+}
+
+#ifdef MPDP_TRACE
+// per-CTA arrival time at each level's barrier (debug builds only)
+constexpr int kCtaTraceMax = 1024;
+constexpr int kCtaTraceSlots = 8;          // level start, sum enum, sum queue, sum eval, tiles, arrival
+__device__ unsigned long long g_cta_arrive[(kMaxN + 1) * kCtaTraceMax * kCtaTraceSlots];
+#define CT_NOW(var) unsigned long long var = (threadIdx.x == 0) ? globaltimer_ns() : 0ull
+#else
+#define CT_NOW(var)
+#endif
+
 template <int CLS>
 __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(const __grid_constant__ Params<uint32_t> p) {
     using M = uint32_t;
@@ -87,6 +236,8 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     __shared__ MemoView v;
     __shared__ LevelDesc d;
     __shared__ unsigned long long s_next;
+    __shared__ unsigned int s_small;
+    unsigned long long* small_list = reinterpret_cast<unsigned long long*>(p.light);
     __shared__ Tri s_excl, s_agg;
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
@@ -108,6 +259,10 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
         TRACE(0);
+#ifdef MPDP_TRACE
+        CT_NOW(ct_lvl0);
+        unsigned long long ct_enum = 0, ct_queue = 0, ct_eval = 0, ct_tiles = 0;
+#endif
         // this launch evaluates the colex ranks [lo, hi) of level k (its share)
         const unsigned int lo = p.share_lo[k], r_hi = p.share_hi[k];
         const unsigned int nranks = r_hi - lo;
@@ -140,6 +295,9 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             if (!heavy_level && threadIdx.x == 0 && nranks > dyn_base)
                 next_t0 = dyn_base + atomicAdd(&p.desc[k].tile_ticket, tile_ranks);   // consumed at the end
             TRACE(1);
+#ifdef MPDP_TRACE
+            CT_NOW(ct_a);
+#endif
 
             // ---- unrank + filter + classify (registers only)
             const unsigned int r0 = lo + (unsigned int)t0 + threadIdx.x * rpt;
@@ -169,6 +327,10 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             mine.l = __popc(lflag);
             mine.h = __popc(hflag);
             TRACE(2);
+#ifdef MPDP_TRACE
+            CT_NOW(ct_b);
+            ct_enum += ct_b - ct_a;
+#endif
 
             // ---- block scan; global look-back only where heavy sets can exist
             Tri agg;
@@ -195,7 +357,17 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             }
             const Tri excl = heavy_level ? s_excl : Tri{0, 0, 0};
 
-            // ---- light sets -> CTA queue (slot = colex rank); heavy sets -> global list
+            // ---- light sets -> CTA queue (slot = colex rank), except the last
+            // nq mod blockDim (all of them when nq < blockDim), which go to the
+            // grid-wide small list so that every local round keeps all threads
+            // busy; heavy sets -> global list
+            const unsigned int nq = (unsigned int)agg.l;
+            const unsigned int ndef = kDeferRemainder ? nq % blockDim.x : (nq < blockDim.x ? nq : 0u);
+            const unsigned int nloc = nq - ndef;
+            if (ndef) {
+                if (threadIdx.x == 0) s_small = atomicAdd(&p.desc[k].n_small, ndef);
+                __syncthreads();
+            }
             if (lflag | hflag) {
                 unsigned int li = (unsigned int)ex.l;
                 unsigned long long hi = excl.h + ex.h, wi = excl.w + ex.w;
@@ -203,8 +375,16 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 #pragma unroll
                 for (int i = 0; i < kFusedRanksPerThread; i++) {
                     if ((lflag >> i) & 1) {
-                        qmask[li] = S;
-                        qrank[li] = r0 + i;
+                        if (li < nloc) {
+                            qmask[li] = S;
+                            qrank[li] = r0 + i;
+                        } else {
+                            const unsigned long long d = s_small + (li - nloc);
+                            if (d < p.list_cap)
+                                small_list[d] = ((unsigned long long)(r0 + i) << 32) | S;
+                            else
+                                atomicOr(&p.result->error, ERR_CAPACITY);
+                        }
                         li++;
                     }
                     if ((hflag >> i) & 1) {
@@ -228,34 +408,12 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             __syncthreads();
 
             TRACE(3);
-            // ---- evaluate the tile's light sets: warp per set (lanes = join pairs)
-            // when the queue is short, else thread per set
-            const unsigned int nq = (unsigned int)agg.l;
-            const bool warp_mode = nq * 4 <= blockDim.x;
-            if (warp_mode) {
-                const unsigned int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-                for (unsigned int e = wid; e < nq; e += blockDim.x >> 5) {
-                    const M S = qmask[e];
-                    unsigned long long w;
-                    const int kind = set_kind<M, CLS>(q, S, k, w);
-                    PairSink<M, MEMO> sink;
-                    sink.init(&p.memo, gen, &v, rtab, &q, card_of(q, S));
-                    unsigned long long ccp_l = 0;
-                    if (lane < w) eval_range<M, CLS>(q, S, k, kind, lane, lane + 1, sink, ccp_l);
-                    sink.flush();
-                    nprobe += sink.nprobe;
-                    nccp += ccp_l;
-                    const Key best = warp_min(sink.best);
-                    if (lane == 0) {
-                        pairs += w;
-                        const unsigned long long idx = v.off[k] + qrank[e];
-                        p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
-                        p.memo.dleft[idx] = (unsigned int)best.l;
-                        p.memo.dcard[idx] = sink.cS;
-                    }
-                }
-            }
-            for (unsigned int e = threadIdx.x; e < (warp_mode ? 0u : nq); e += blockDim.x) {
+#ifdef MPDP_TRACE
+            CT_NOW(ct_c);
+            ct_queue += ct_c - ct_b;
+#endif
+            // ---- evaluate the tile's local light sets, thread per set
+            for (unsigned int e = threadIdx.x; e < nloc; e += blockDim.x) {
                 const M S = qmask[e];
                 unsigned long long w;
                 const int kind = set_kind<M, CLS>(q, S, k, w);
@@ -285,27 +443,60 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             t0 = s_next;
             tile += gridDim.x;
             TRACE(4);
+#ifdef MPDP_TRACE
+            CT_NOW(ct_d);
+            ct_eval += ct_d - ct_c;
+            ct_tiles++;
+#endif
         }
         if (counting) {
             if (threadIdx.x == 0 && nlight) atomicAdd(&p.desc[k].n_light, nlight);
             flush_counters(&p.desc[k], pairs, nccp, nprobe);
         }
         TRACE(5);
+#ifdef MPDP_TRACE
+        if (threadIdx.x == 0 && blockIdx.x < kCtaTraceMax) {
+            unsigned long long* o = g_cta_arrive + ((unsigned long long)k * kCtaTraceMax + blockIdx.x) * kCtaTraceSlots;
+            o[0] = ct_lvl0;
+            o[1] = ct_enum;
+            o[2] = ct_queue;
+            o[3] = ct_eval;
+            o[4] = ct_tiles;
+            o[5] = globaltimer_ns();
+        }
+#endif
         grid_sync(p.gbar, &p.result->error);
         TRACE(6);
 
+        // deferred light sets (small list) and, on heavy levels, heavy-set cards
+        // share the window after the level barrier: both read levels < k only
+        if (threadIdx.x == 0) d = p.desc[k];
+        __syncthreads();
+        const unsigned long long nsmall = d.n_small < p.list_cap ? d.n_small : p.list_cap;
+        unsigned long long sp = 0, sc = 0, spr = 0;
+#ifdef MPDP_TRACE
+        CT_NOW(ct_s0);
+#endif
+        if (nsmall) small_phase<CLS>(p, k, q, v, rtab, bin, gen, small_list, DenseLocate{}, nsmall, sp, sc, spr);
+#ifdef MPDP_TRACE
+        if (threadIdx.x == 0 && blockIdx.x < kCtaTraceMax) {
+            unsigned long long* o = g_cta_arrive + ((unsigned long long)k * kCtaTraceMax + blockIdx.x) * kCtaTraceSlots;
+            o[6] = globaltimer_ns() - ct_s0;
+            o[7] = nsmall;
+        }
+#endif
         if (CLS != CLS_TREE && heavy_level) {
             // card(S) of every heavy set once (one thread per set)
-            if (threadIdx.x == 0) d = p.desc[k];
-            __syncthreads();
             const unsigned long long nh = d.n_heavy < p.heavy_cap ? d.n_heavy : p.heavy_cap;
             const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
             for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride)
                 p.hcard[h] = card_of(q, p.heavy[h]);
             grid_sync(p.gbar, &p.result->error);
-            unsigned long long hp = 0, hc = 0, hpr = 0;
-            heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, hp, hc, hpr);
-            if (counting) flush_counters(&p.desc[k], hp, hc, hpr);
+            heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, sp, sc, spr);
+            if (counting) flush_counters(&p.desc[k], sp, sc, spr);
+            grid_sync(p.gbar, &p.result->error);
+        } else if (nsmall) {
+            if (counting) flush_counters(&p.desc[k], sp, sc, spr);
             grid_sync(p.gbar, &p.result->error);
         }
     }

@@ -24,7 +24,9 @@ struct __align__(16) LevelDesc {
     unsigned long long pairs, ccp;         // counters (R3, R2)
     unsigned long long probes;             // memo probes of non-singleton sets
     unsigned long long bucket_off, n_buckets;   // HASH: this level's table
-    unsigned int tile_ticket, work_ticket, pad0, pad1;
+    unsigned int tile_ticket, work_ticket;
+    unsigned int n_small;                  // fused: light sets deferred to the grid-wide small list
+    unsigned int pad1;
 };
 
 struct __align__(64) TileRec {            // decoupled look-back record (ring slot)
@@ -34,6 +36,7 @@ struct __align__(64) TileRec {            // decoupled look-back record (ring sl
 };
 
 constexpr int kTraceCap = 512;
+constexpr int kMaxGrid = 2048;            // CTAs of a persistent whole-query kernel
 
 struct ResultDev {
     double cost;
@@ -64,6 +67,7 @@ template <typename M> struct Params {
     unsigned long long heavy_cap;          // heavy list capacity
     ResultDev* result;
     unsigned int* gbar;                    // fused kernel: grid barrier {count, generation}
+    unsigned int* seg_cnt;                 // list kernel: [2][kMaxGrid] per-CTA level-list counts
     unsigned long long heavy_levels;       // bit k: level k can have heavy sets
     unsigned long long item_of[kMaxN + 1]; // heavy work-item size per level
     // fused kernel, multi-GPU sharding: levels [k_begin, k_end]

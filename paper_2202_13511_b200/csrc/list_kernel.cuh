@@ -1,0 +1,223 @@
+// list_kernel.cuh — the level loop of Alg. mpdp_gpu for tree
+// queries (CLS_TREE: every set is light, k-1 join pairs) as ONE persistent
+// cooperative kernel with level lists and enumerate-ahead.
+//
+// Phase k (between two grid barriers) does two independent things:
+//   * unrank + connectivity filter of level k+1 into the
+//     other level list -- enumeration does not read the memo, so it runs one
+//     level ahead;
+//   * evaluation of level k's list (csg-cmp pairs, C_out, per-set min, memo
+//     scatter), G lanes per set (small_phase).
+// The stream compaction of P:889 is a warp-aggregated reservation: a warp's
+// survivors are written contiguously at an offset from one atomicAdd on the
+// level counter (list order is irrelevant: every entry carries its colex rank,
+// which is its memo slot).  Compared with the tile kernel (fused.cuh) the work
+// of both halves is split evenly over all threads of the grid, so the CTAs
+// reach the barrier within one set evaluation of each other, and there is one
+// grid barrier per level.
+#pragma once
+#include "fused.cuh"
+
+namespace mpdp {
+
+constexpr int kListChunk = 32;             // ranks per thread per reservation pass
+
+// Level k's share [share_lo, share_hi) -> segmented list `out` (entries
+// rank << 32 | mask): CTA b owns the segment [b * seg, (b + 1) * seg) with
+// seg = blockDim * rpt (its ranks); cnt[b] (zeroed beforehand) counts its
+// survivors.  Every thread walks a contiguous run of rpt ranks (one unrank,
+// then Gosper); per pass of kListChunk ranks a warp reserves its survivors with
+// one atomic on its CTA's counter.  No CTA-wide synchronisation, so warps can
+// interleave enumeration and evaluation.  (One grid-wide counter serialised
+// thousands of same-address atomics at one L2 slice: the last warps waited
+// ~200 us.)
+__device__ __forceinline__ unsigned long long list_rpt(unsigned long long nranks) {
+    const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
+    return (nranks + T - 1) / T;
+}
+
+template <int CLS>
+__device__ void enum_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const unsigned int* bin,
+                             unsigned long long* out, unsigned int* cnt) {
+    const unsigned int lo = p.share_lo[k], hi = p.share_hi[k];
+    const unsigned long long rpt = list_rpt(hi - lo);
+    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long b0 = lo + gtid * rpt;
+    const unsigned long long b1 = b0 + rpt < hi ? b0 + rpt : hi;
+    unsigned long long* seg = out + (unsigned long long)blockIdx.x * blockDim.x * rpt;
+    const unsigned int lane = threadIdx.x & 31;
+    uint32_t S = b0 < b1 ? unrank_colex32(bin, p.n, k, (unsigned int)b0) : 0u;
+    for (unsigned long long pass = 0; pass < rpt; pass += kListChunk) {   // same trip count on every lane
+        const unsigned long long r0 = b0 + pass;
+        const uint32_t S0 = S;
+        unsigned int flags = 0;
+#pragma unroll 4
+        for (int i = 0; i < kListChunk; i++) {
+            if (r0 + i < b1) {
+                if (connected_cls<uint32_t, CLS>(q, S, k)) flags |= 1u << i;
+                if (r0 + i + 1 < b1) S = gosper(S);
+            }
+        }
+        const unsigned int c = __popc(flags);
+        unsigned int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (unsigned int)o) inc += t;
+        }
+        const unsigned int total = __shfl_sync(0xffffffffu, inc, 31);
+        unsigned int base = 0;
+        if (lane == 31 && total) base = atomicAdd(cnt + blockIdx.x, total);   // only this CTA's warps contend
+        base = __shfl_sync(0xffffffffu, base, 31);
+        if (c) {
+            unsigned long long d = base + inc - c;
+            uint32_t X = S0;
+            for (int i = 0; i < kListChunk && r0 + i < b1; i++) {
+                if ((flags >> i) & 1u) seg[d++] = ((r0 + i) << 32) | X;
+                if (r0 + i + 1 < b1) X = gosper(X);
+            }
+        }
+    }
+}
+
+// Locate entry e of a segmented level list: s_pre holds the exclusive prefix of
+// the per-CTA counts (grid + 1 entries, in shared memory).
+struct SegLocate {
+    const unsigned int* pre;
+    unsigned int nseg;
+    unsigned long long seg;
+    __device__ __forceinline__ unsigned int seek(unsigned long long e) const {
+        unsigned int lo = 0, hi = nseg;            // largest b with pre[b] <= e
+        while (hi - lo > 1) {
+            const unsigned int mid = (lo + hi) >> 1;
+            if (pre[mid] <= e) lo = mid; else hi = mid;
+        }
+        return lo;
+    }
+    // sequential access with a cursor (e never decreases)
+    __device__ __forceinline__ unsigned long long at(unsigned long long e, unsigned int& b) const {
+        while (b + 1 < nseg && pre[b + 1] <= e) b++;
+        return (unsigned long long)b * seg + (e - pre[b]);
+    }
+    __device__ __forceinline__ unsigned long long operator()(unsigned long long e) const {
+        unsigned int b = seek(e);
+        return at(e, b);
+    }
+};
+
+// Exclusive prefix of cnt[0..g) into pre[0..g] (shared memory), block-wide:
+// per-thread partial sums, warp shuffle scans, one scan of the warp totals.
+__device__ __forceinline__ void seg_prefix(const unsigned int* cnt, unsigned int g, unsigned int* pre) {
+    __shared__ unsigned int s_warp[kBlock / 32];
+    const unsigned int per = (g + blockDim.x - 1) / blockDim.x;
+    const unsigned int i0 = threadIdx.x * per;
+    const unsigned int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned int sum = 0;
+    for (unsigned int i = i0; i < i0 + per && i < g; i++) sum += ld_relaxed_u32(cnt + i);
+    unsigned int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (unsigned int)o) inc += t;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const unsigned int nw = blockDim.x >> 5;
+        unsigned int x = lane < nw ? s_warp[lane] : 0u, y = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int t = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= (unsigned int)o) y += t;
+        }
+        if (lane < nw) s_warp[lane] = y - x;      // exclusive
+        if (lane == nw - 1) pre[g] = y;
+    }
+    __syncthreads();
+    unsigned int acc = s_warp[wid] + inc - sum;
+    for (unsigned int i = i0; i < i0 + per && i < g; i++) {
+        pre[i] = acc;
+        acc += ld_relaxed_u32(cnt + i);
+    }
+    __syncthreads();
+}
+
+template <int CLS>
+__global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ Params<uint32_t> p) {
+    constexpr int MEMO = MEMO_DENSE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));
+    unsigned int* bin = rtab + p.memo.rg.entries;                  // 33 x 33 binomials
+    __shared__ MemoView v;
+
+    memo_prologue<uint32_t, MEMO>(p, p.n, q, v, rtab);
+    const unsigned int gen = p.q->gen;
+    __syncthreads();
+    unsigned long long* lists[2] = {reinterpret_cast<unsigned long long*>(p.light),
+                                    reinterpret_cast<unsigned long long*>(p.light) + p.list_cap};
+    unsigned int* cnts[2] = {p.seg_cnt, p.seg_cnt + kMaxGrid};
+    __shared__ unsigned int s_pre[kMaxGrid + 1];
+
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[p.k_begin] = globaltimer_ns();
+    if (threadIdx.x == 0) cnts[p.k_begin & 1][blockIdx.x] = 0;
+    __syncthreads();
+    enum_to_list<CLS>(p, p.k_begin, q, bin, lists[p.k_begin & 1], cnts[p.k_begin & 1]);
+    grid_sync(p.gbar, &p.result->error);
+    for (int k = p.k_begin; k <= p.k_end; k++) {
+        if (blockIdx.x == 0 && threadIdx.x == 0 && k > p.k_begin) p.result->t_level[k] = globaltimer_ns();
+        if (threadIdx.x == 0 && k < p.k_end) cnts[(k + 1) & 1][blockIdx.x] = 0;   // read by every CTA in phase k-1 only
+        seg_prefix(cnts[k & 1], gridDim.x, s_pre);                                 // (its syncs publish the zero)
+        const unsigned long long N = s_pre[gridDim.x];
+        const SegLocate loc{s_pre, gridDim.x, (unsigned long long)blockDim.x * list_rpt(p.share_hi[k] - p.share_lo[k])};
+        const bool counting = (p.count_levels >> k) & 1ull;
+#ifdef MPDP_TRACE
+        __shared__ unsigned long long s_me, s_mv;
+        if (threadIdx.x == 0) s_me = s_mv = 0;
+        __syncthreads();
+        const unsigned long long ct_a = globaltimer_ns();
+#endif
+        // even warps enumerate level k+1 first, odd warps evaluate level k
+        // first: ALU-bound enumeration overlaps latency-bound evaluation
+        const bool enum_first = ((threadIdx.x >> 5) & 1) == 0;
+        unsigned long long pairs = 0, nccp = 0, nprobe = 0;
+        if (enum_first && k < p.k_end) enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
+#ifdef MPDP_TRACE
+        const unsigned long long ct_b = globaltimer_ns();
+#endif
+        if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe);
+        if (!enum_first && k < p.k_end) enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
+#ifdef MPDP_TRACE
+        const unsigned long long ct_c = globaltimer_ns();
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&s_me, ct_b - ct_a);
+            atomicMax(&s_mv, ct_c - ct_b);
+        }
+#endif
+        if (counting) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) p.desc[k].n_light = N;
+            flush_counters(&p.desc[k], pairs, nccp, nprobe);
+        }
+#ifdef MPDP_TRACE
+        __syncthreads();
+        if (threadIdx.x == 0 && blockIdx.x < kCtaTraceMax) {
+            unsigned long long* o = g_cta_arrive + ((unsigned long long)k * kCtaTraceMax + blockIdx.x) * kCtaTraceSlots;
+            o[0] = ct_a;
+            o[1] = ct_b - ct_a;                // enumerate ahead (thread 0's warp)
+            o[2] = s_me;                       // slowest warp: enumerate
+            o[3] = ct_c - ct_b;                // evaluate (thread 0's warp)
+            o[4] = 1;
+            o[5] = globaltimer_ns();           // whole CTA done
+            o[6] = s_mv;                       // slowest warp: evaluate
+            o[7] = N;
+        }
+#endif
+        grid_sync(p.gbar, &p.result->error);
+    }
+    if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
+        p.result->t_level[p.n + 1] = globaltimer_ns();
+        extract_phase<uint32_t, MEMO>(p, q, v, rtab, gen);
+    }
+}
+
+}  // namespace mpdp

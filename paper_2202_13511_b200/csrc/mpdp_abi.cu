@@ -18,7 +18,7 @@
 #include <string>
 #include <vector>
 
-#include "fused.cuh"
+#include "list_kernel.cuh"
 #include "heuristics.h"
 
 using namespace mpdp;
@@ -28,7 +28,7 @@ namespace {
 thread_local std::string g_tls_error;
 
 struct DevLayout {
-    size_t query = 0, desc = 0, result = 0, gbar = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
+    size_t query = 0, desc = 0, result = 0, gbar = 0, segcnt = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
            hcard = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
@@ -338,6 +338,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.desc = L.sh_desc[0];
     L.result = L.sh_result[0];
     L.gbar = take(64);
+    L.segcnt = take(4 * 2 * kMaxGrid);
     L.rank = take(sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25));
     off = align_up(off, 256);
     if (off + (64u << 20) > c->ws_bytes) return fail(c, MPDP_ERR_CAPACITY, "workspace smaller than 64 MiB");
@@ -382,10 +383,13 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     const size_t fixed = sizeof(TileRec) * tiles_cap + 4 * fh_need + 4096;
     if (fixed >= scratch) return fail(c, MPDP_ERR_CAPACITY, "workspace too small for n = " + std::to_string(n));
     const size_t avail = scratch - fixed;
-    list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / msz);
+    // the list kernel's level lists are segmented per CTA (segments of blockDim *
+    // ranks-per-thread entries), which can exceed C(n,k) by one rank per thread
+    list_cap += (unsigned long long)kMaxGrid * kBlock;
+    list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / 16);   // fused: two lists of (rank << 32 | mask)
     heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 40));
     L.tiles = take(sizeof(TileRec) * tiles_cap);
-    L.light = take(msz * list_cap);
+    L.light = take(16 * list_cap);
     L.heavy = take(msz * heavy_cap);
     L.wh = take(8 * (heavy_cap + 1));
     L.bkey = take(16 * heavy_cap);
@@ -422,6 +426,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.sh_result[shard])->error;
     p.memo_kind = L.memo_kind;
     p.gbar = reinterpret_cast<unsigned int*>(b + L.gbar);
+    p.seg_cnt = reinterpret_cast<unsigned int*>(b + L.segcnt);
     p.heavy_levels = 0;
     for (int k = 2; k <= c->n; k++) {
         if (heavy_pair_bound(c->n, k, c->cls)) p.heavy_levels |= 1ull << k;
@@ -529,16 +534,30 @@ static mpdp_status enqueue_query(mpdp_ctx* c, const Params<M>& p, bool sync_leve
     return MPDP_OK;
 }
 
+// The whole-query kernel of a class: trees (no heavy sets) use the level-list
+// kernel with enumerate-ahead, the other classes the tile kernel.
+template <int CLS>
+static const void* level_loop_kernel() {
+    if constexpr (CLS == CLS_TREE)
+        return (const void*)k_dp_list<CLS>;
+    else
+        return (const void*)k_dp_fused<CLS>;
+}
+template <int CLS>
+static size_t level_loop_smem(int n) {
+    return sizeof(SQ<uint32_t>) +
+           sizeof(unsigned int) * (rank_geom(n).entries + 33 * 33 + (CLS == CLS_TREE ? 0 : 2 * kFusedTile));
+}
+
 // The fused path: k_init, ONE cooperative persistent kernel for every level
 // and the extraction, then the D2H copy of the result.
 template <int CLS>
 static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
-    const size_t smem = sizeof(SQ<uint32_t>) +
-                        sizeof(unsigned int) * (rank_geom(c->n).entries + 33 * 33 + 2 * kFusedTile);
+    const size_t smem = level_loop_smem<CLS>(c->n);
     int& occ = c->fused_occ[CLS];
     if (!occ || c->fused_n[CLS] != c->n) {
-        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_fused<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_fused<CLS>, kBlock, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(level_loop_kernel<CLS>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, level_loop_kernel<CLS>(), kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
         c->fused_n[CLS] = c->n;
     }
@@ -553,11 +572,11 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
         want = std::max(want, heavy_pair_bound(c->n, k, CLS) / 16384);
     }
     if (CLS == CLS_GENERAL && c->n > 12) want = ~0ull;     // heavy work unknown up front
-    const unsigned int grid = (unsigned int)std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ);
+    const unsigned int grid = (unsigned int)std::min<unsigned long long>(
+        std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ), (unsigned long long)kMaxGrid);
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
     CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));    // device time of the fused kernel itself
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3(grid), dim3(kBlock), args,
-                                            smem, c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel(level_loop_kernel<CLS>(), dim3(grid), dim3(kBlock), args, smem, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
@@ -575,8 +594,8 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
 // [r*seg, (r+1)*seg) of the level (seg = ceil(C(n,k)/W)) with the fused kernel
 // restricted to that share; its memo entries are then one contiguous segment
 // of the level's perfect-hash array, so the exchange is an in-place
-// ncclAllGather of `seg` costs and `seg` left masks (plus `seg` cards on trees,
-// read by the tree fast path) per rank -- no packing and
+// ncclAllGather of `seg` costs and `seg` left masks (plus `seg` cards on trees
+// and cliques, where card(S) is derived from card(S \ max)) per rank -- no packing and
 // no replica insert.  Levels below kShardMinRanks are computed redundantly by
 // every rank (counted by rank 0 only).  Counters are summed with one
 // ncclAllReduce at the end; every rank extracts the identical plan from its
@@ -610,7 +629,7 @@ static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k,
     ncclResult_t r = c->nccl->GroupStart();
     if (!r) r = c->nccl->AllGather(dc + c->rank * seg, dc, seg, kNcclFloat64, c->comm, c->stream);
     if (!r) r = c->nccl->AllGather(dl + c->rank * seg, dl, seg, kNcclUint32, c->comm, c->stream);
-    double* dk = P[0].memo.dcard + off;    // card(S) feeds the tree fast path only
+    double* dk = P[0].memo.dcard + off;    // card(S \ max) feeds card_fast (trees, cliques)
     if (!r && with_card) r = c->nccl->AllGather(dk + c->rank * seg, dk, seg, kNcclFloat64, c->comm, c->stream);
     const ncclResult_t r2 = c->nccl->GroupEnd();
     if (r || r2) return fail(c, MPDP_ERR_NCCL, "ncclAllGather of level " + std::to_string(k) + " failed");
@@ -622,16 +641,15 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     if (c->wide || c->lay.memo_kind != MEMO_DENSE)
         return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
     const int n = c->n, W = c->world, nsh = c->lay.nshards;
-    const size_t smem = sizeof(SQ<uint32_t>) +
-                        sizeof(unsigned int) * (rank_geom(n).entries + 33 * 33 + 2 * kFusedTile);
+    const size_t smem = level_loop_smem<CLS>(n);
     int& occ = c->fused_occ[CLS];
     if (!occ || c->fused_n[CLS] != n) {
-        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_fused<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_fused<CLS>, kBlock, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(level_loop_kernel<CLS>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, level_loop_kernel<CLS>(), kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
         c->fused_n[CLS] = n;
     }
-    const unsigned long long full = (unsigned long long)c->num_sms * occ;
+    const unsigned long long full = std::min<unsigned long long>((unsigned long long)c->num_sms * occ, kMaxGrid);
     std::vector<Params<uint32_t>> P(nsh);
     std::vector<unsigned long long> counted(nsh, 0);
     CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
@@ -643,7 +661,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     }
     auto launch = [&](Params<uint32_t>& p, unsigned long long grid) -> mpdp_status {
         void* args[] = {&p};
-        CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_fused<CLS>, dim3((unsigned int)grid), dim3(kBlock),
+        CUDA_TRY(c, cudaLaunchCooperativeKernel(level_loop_kernel<CLS>(), dim3((unsigned int)grid), dim3(kBlock),
                                                 args, smem, c->stream));
         c->launches++;
         return MPDP_OK;
@@ -673,7 +691,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
             if (st != MPDP_OK) return st;
         }
         if (sharded) {
-            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, CLS == CLS_TREE);
+            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, CLS == CLS_TREE || CLS == CLS_CLIQUE);
             if (st != MPDP_OK) return st;
         }
         CUDA_TRY(c, cudaGetLastError());
@@ -1153,6 +1171,21 @@ mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo
     if (st != MPDP_OK) return st;
     return mpdp_fetch(c, out);
 }
+
+#ifdef MPDP_TRACE
+// Debug: per-CTA barrier arrival times of the last fused run, [level][cta].
+int mpdp_debug_cta_trace(unsigned long long* out, int cap) {
+    const int n = (kMaxN + 1) * kCtaTraceMax * kCtaTraceSlots;
+    if (cap < n) return 0;
+    if (cudaMemcpyFromSymbol(out, g_cta_arrive, sizeof(unsigned long long) * n) != cudaSuccess) return 0;
+    return kCtaTraceMax;
+}
+void mpdp_debug_cta_trace_clear() {
+    void* a = nullptr;
+    if (cudaGetSymbolAddress(&a, g_cta_arrive) == cudaSuccess) cudaMemset(a, 0, sizeof(g_cta_arrive));
+    cudaDeviceSynchronize();
+}
+#endif
 
 // Debug: copy the block-0 phase trace of the last fused run (MPDP_TRACE builds).
 int mpdp_debug_trace(const mpdp_ctx* c, unsigned long long* out, int cap) {
