@@ -26,7 +26,7 @@ struct __align__(16) LevelDesc {
     unsigned long long bucket_off, n_buckets;   // HASH: this level's table
     unsigned int tile_ticket, work_ticket;
     unsigned int n_small;                  // fused: light sets deferred to the grid-wide small list
-    unsigned int pad1;
+    unsigned int seg;                      // list kernel: per-CTA segment size of this level's list
 };
 
 struct __align__(64) TileRec {            // decoupled look-back record (ring slot)

@@ -80,6 +80,76 @@ __device__ void enum_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t
     }
 }
 
+// Sparse generation of level k+1 from level k's list (trees; SURVEY §8(f)
+// NEXT-4), used when a thread's share of the candidates (n - k per set) is
+// well below its share of the C(n, k+1) ranks: every connected
+// S' of size k+1 is S u {v} for a connected S and a neighbour v of S, and is
+// emitted exactly once -- from S = S' \ {u*}, u* the largest leaf of G[S'] (a
+// new vertex v is always a leaf of the tree G[S u {v}]; the leaves are the
+// vertices whose removal keeps the set connected).  Replaces the scan of all
+// C(n, k+1) ranks, whose survivors are a vanishing fraction on sparse graphs
+// (chain: n - k of C(n, k+1)).  CTA b expands the inputs [N*b/grid,
+// N*(b+1)/grid) into its output segment of `seg` entries.
+template <typename Locate>
+__device__ void expand_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const unsigned int* bin,
+                               const unsigned long long* src, const Locate& loc, unsigned long long N,
+                               unsigned long long* out, unsigned int* cnt, unsigned long long seg) {
+    // G lanes per input set (largest power of two <= 32 that keeps every set a
+    // group); lane `sub` tests the candidates v with index = sub (mod G)
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    unsigned int G = 1;
+    while (G < 32 && 2ull * G * N <= nthreads) G <<= 1;
+    const unsigned int sub = threadIdx.x & (G - 1), gpc = blockDim.x / G;
+    const unsigned long long c_lo = N * blockIdx.x / gridDim.x, c_hi = N * (blockIdx.x + 1) / gridDim.x;
+    unsigned long long* segp = out + (unsigned long long)blockIdx.x * seg;
+    const unsigned int lane = threadIdx.x & 31;
+    for (unsigned long long base = c_lo; base < c_hi; base += gpc) {   // same trip count on every lane
+        const unsigned long long e = base + threadIdx.x / G;
+        uint32_t S = 0, em = 0;
+        if (e < c_hi) {
+            S = (uint32_t)src[loc(e)];
+            uint32_t Nb = 0;
+            for (uint32_t T = S; T; T &= T - 1) Nb |= q.adj[__ffs(T) - 1];
+            unsigned int j = 0;
+            for (uint32_t V = Nb & ~S; V; V &= V - 1, j++) {
+                if ((j & (G - 1)) != sub) continue;
+                const int v = __ffs(V) - 1;
+                const uint32_t Sp = S | (1u << v);
+                bool ok = true;                     // no leaf of G[S'] above v
+                for (uint32_t U = S & ~((2u << v) - 1u); U; U &= U - 1)
+                    if (__popc(q.adj[__ffs(U) - 1] & Sp) == 1) {
+                        ok = false;
+                        break;
+                    }
+                if (ok) em |= 1u << v;
+            }
+        }
+        const unsigned int c = __popc(em);
+        unsigned int inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (unsigned int)o) inc += t;
+        }
+        const unsigned int total = __shfl_sync(0xffffffffu, inc, 31);
+        unsigned int wbase = 0;
+        if (lane == 31 && total) wbase = atomicAdd(cnt + blockIdx.x, total);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        unsigned long long d = wbase + inc - c;
+        for (uint32_t E = em; E; E &= E - 1) {
+            const uint32_t Sp = S | (E & (0u - E));
+            unsigned int R = 0;                     // colex rank of S'
+            int i = 1;
+            for (uint32_t T = Sp; T; T &= T - 1, i++) R += bin[(__ffs(T) - 1) * 33 + i];
+            if (d < seg)
+                segp[d] = ((unsigned long long)R << 32) | Sp;
+            else
+                atomicOr(&p.result->error, ERR_CAPACITY);
+            d++;
+        }
+    }
+}
+
 // Locate entry e of a segmented level list: s_pre holds the exclusive prefix of
 // the per-CTA counts (grid + 1 entries, in shared memory).
 struct SegLocate {
@@ -161,6 +231,8 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
 
     if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[p.k_begin] = globaltimer_ns();
     if (threadIdx.x == 0) cnts[p.k_begin & 1][blockIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        p.desc[p.k_begin].seg = (unsigned int)(blockDim.x * list_rpt(p.share_hi[p.k_begin] - p.share_lo[p.k_begin]));
     __syncthreads();
     enum_to_list<CLS>(p, p.k_begin, q, bin, lists[p.k_begin & 1], cnts[p.k_begin & 1]);
     grid_sync(p.gbar, &p.result->error);
@@ -169,8 +241,27 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
         if (threadIdx.x == 0 && k < p.k_end) cnts[(k + 1) & 1][blockIdx.x] = 0;   // read by every CTA in phase k-1 only
         seg_prefix(cnts[k & 1], gridDim.x, s_pre);                                 // (its syncs publish the zero)
         const unsigned long long N = s_pre[gridDim.x];
-        const SegLocate loc{s_pre, gridDim.x, (unsigned long long)blockDim.x * list_rpt(p.share_hi[k] - p.share_lo[k])};
+        const SegLocate loc{s_pre, gridDim.x, ld_relaxed_u32(&p.desc[k].seg)};
         const bool counting = (p.count_levels >> k) & 1ull;
+        // level k+1: sparse expansion of this list when its candidates are far
+        // fewer than the ranks (whole levels only: a rank share of a sharded
+        // level is not closed under expansion)
+        bool expand = false;
+        unsigned long long seg_next = 0;
+        if (k < p.k_end) {
+            const unsigned long long C1 = p.share_hi[k + 1] - p.share_lo[k + 1];
+            const bool whole = p.share_lo[k] == 0 && p.share_lo[k + 1] == 0 && p.share_hi[k] == bin[p.n * 33 + k] &&
+                               p.share_hi[k + 1] == bin[p.n * 33 + k + 1];
+            // fewer candidates than ranks, and per-thread work ((sets per
+            // thread) * (n - k) candidates over up to 32 lanes per set) below
+            // the per-thread share of the ranks
+            const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
+            expand = CLS == CLS_TREE && whole && 4ull * N * (unsigned long long)(p.n - k) <= C1 &&
+                     2ull * ((32ull * N + T - 1) / T) * (unsigned long long)(p.n - k) <= 32ull * ((C1 + T - 1) / T);
+            seg_next = expand ? ((N + gridDim.x - 1) / gridDim.x + 1) * (unsigned long long)(p.n - k)
+                              : (unsigned long long)blockDim.x * list_rpt(C1);
+            if (blockIdx.x == 0 && threadIdx.x == 0) p.desc[k + 1].seg = (unsigned int)seg_next;
+        }
 #ifdef MPDP_TRACE
         __shared__ unsigned long long s_me, s_mv;
         if (threadIdx.x == 0) s_me = s_mv = 0;
@@ -181,12 +272,19 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
         // first: ALU-bound enumeration overlaps latency-bound evaluation
         const bool enum_first = ((threadIdx.x >> 5) & 1) == 0;
         unsigned long long pairs = 0, nccp = 0, nprobe = 0;
-        if (enum_first && k < p.k_end) enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
+        auto next_level = [&]() {
+            if (k >= p.k_end) return;
+            if (expand)
+                expand_to_list(p, k, q, bin, lists[k & 1], loc, N, lists[(k + 1) & 1], cnts[(k + 1) & 1], seg_next);
+            else
+                enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
+        };
+        if (enum_first) next_level();
 #ifdef MPDP_TRACE
         const unsigned long long ct_b = globaltimer_ns();
 #endif
         if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe);
-        if (!enum_first && k < p.k_end) enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
+        if (!enum_first) next_level();
 #ifdef MPDP_TRACE
         const unsigned long long ct_c = globaltimer_ns();
         if ((threadIdx.x & 31) == 0) {
