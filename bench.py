@@ -193,6 +193,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     graphs = workload_graphs(args.workload, args.seeds)           # every rank: the same queries
+    topo_is_tree = args.workload.rsplit("-", 1)[0] in ("star", "snowflake", "chain")
     n = graphs[0].n
     ws = 6 << 30 if n >= 24 else 2 << 30
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)    # > 126 MB L2
@@ -269,16 +270,20 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_value = e2e_pairs / e2e_s
 
-    # ---- roofline of the dominant kernel: the fused level-loop kernel (one
-    # launch per query does unrank, filter, evaluate, min and memo scatter).
-    # perfect-hash memo = 8 B cost per probe + per connected set
-    # 8 B cost + 4 B left store; open-addressing memo = 16 B slot per probe, per
-    # set list read + 16 B slot + left.
+    # ---- roofline of the dominant kernel: the whole-query level-loop kernel
+    # (one launch per query does unrank, filter, compaction, evaluate, min and
+    # memo scatter for every level; k_dp_list for tree queries, k_dp_fused
+    # otherwise).  DESIGN.md §6: perfect-hash memo = 8 B cost per probe + per
+    # connected set 16 B level-list write + read (the compaction of P:889) and
+    # 8 B cost + 4 B left insert; open-addressing memo = 16 B slot per probe,
+    # per set list write + read + 16 B slot + left.
     msz = 4 if n <= 32 else 8
     if memo_kind == 1:
-        alg_bytes = 8 * probes_total + sets_total * (8 + 4)
+        alg_bytes = 8 * probes_total + sets_total * (16 + 8 + 4)
     else:
-        alg_bytes = 16 * probes_total + sets_total * (msz + 16 + msz)
+        alg_bytes = 16 * probes_total + sets_total * (2 * msz + 16 + msz)
+    kernel_name = ("k_dp_list (tree queries: whole level loop, one launch per query)" if topo_is_tree
+                   else "k_dp_fused (whole level loop, one launch per query)")
     peak, peak_kind = measured_peaks()
     kern_s = kernel_ms / 1e3
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
@@ -287,7 +292,7 @@ def run_ours(args):
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(args.workload)
     roof = {"bound": "hbm",
-            "kernel": "k_dp_fused (whole level loop, one launch per query)",
+            "kernel": kernel_name,
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
             "traffic_source": traffic.get("source") if traffic else None,
