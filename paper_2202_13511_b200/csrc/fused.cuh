@@ -32,33 +32,31 @@ __device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
     return v;
 }
 
-// Sense-free grid barrier: bar[0] counts arrivals, bar[1] is the generation.
-// All CTAs are co-resident (cooperative launch).  Thread 0 releases (fence)
-// before arriving, spins with relaxed loads, then issues ONE acq_rel fence at
-// gpu scope, which also invalidates this SM's L1 (CCTL.IVALL): no thread of the
-// CTA can then read a stale line of memo entries another SM wrote before the
-// barrier.  bar.sync propagates the ordering to the rest of the CTA.
-__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int* err) {
+// Grid barrier over a monotonic arrival counter (zeroed before every launch:
+// k_init, or a memset before each sharded launch).  All CTAs are co-resident
+// (cooperative launch).  Thread 0 of each CTA counts the barriers it has passed
+// (`nbar`), arrives with ONE fire-and-forget red.release (which, after the
+// bar.sync, orders the whole CTA's prior writes), and polls with ld.acquire
+// until all gridDim.x arrivals of this barrier are in; bar.sync then extends
+// the acquire to the CTA.  No last-arriver reset chain: the barrier costs one
+// reduction landing in L2 plus one poll.
+__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& nbar, unsigned int* err) {
     __syncthreads();
     if (gridDim.x == 1) return;        // one CTA: bar.sync already orders its global accesses
     if (threadIdx.x == 0) {
-        const unsigned int g = ld_relaxed_u32(bar + 1);
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
+        nbar++;
+        const unsigned int target = nbar * gridDim.x;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        if (ld_acquire_u32(bar) < target) {
             const unsigned long long t0 = globaltimer_ns();
-            while (ld_relaxed_u32(bar + 1) == g) {
-                __nanosleep(32);
+            while (ld_acquire_u32(bar) < target) {
+                __nanosleep(20);
                 if (watchdog_expired(t0)) {   // never hang the device: flag and fall through
                     atomicOr(err, ERR_HANG);
                     break;
                 }
             }
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }
@@ -101,7 +99,7 @@ __device__ __forceinline__ double card_fast(const MemoPtrs& P, const MemoView& v
     const uint32_t b = 1u << p;
     const bool in_memo = k >= 3 && ((CLS == CLS_TREE && (S & q.desc[p]) == b) || CLS == CLS_CLIQUE);
     if (!in_memo) return card_of(q, S);
-    double x = __dmul_rn(P.dcard[v.off[k - 1] + (R - bin[p * 33 + k])], q.card[p]);
+    double x = __dmul_rn(__ldcs(P.dcard + v.off[k - 1] + (R - bin[p * 33 + k])), q.card[p]);
     for (uint32_t W = S & q.adj[p] & (b - 1u); W; W &= W - 1) x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + p]);
     return x;
 }
@@ -127,15 +125,15 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
                                                    unsigned int gen, const unsigned long long* list, const Locate& loc,
                                                    unsigned long long c_lo, unsigned long long c_hi,
                                                    unsigned long long& pairs, unsigned long long& nccp,
-                                                   unsigned long long& nprobe) {
+                                                   unsigned long long& nprobe, const uint2* binp) {
     constexpr int MEMO = MEMO_DENSE;
     unsigned long long e = c_lo + threadIdx.x;
     if (e >= c_hi) return;
     unsigned int cur = loc.seek(e);
-    unsigned long long nxt = list[loc.at(e, cur)];
+    unsigned long long nxt = __ldcs(list + loc.at(e, cur));
     for (; e < c_hi; e += blockDim.x) {
         const unsigned long long ent = nxt;
-        if (e + blockDim.x < c_hi) nxt = list[loc.at(e + blockDim.x, cur)];
+        if (e + blockDim.x < c_hi) nxt = __ldcs(list + loc.at(e + blockDim.x, cur));
         const uint32_t S = (uint32_t)ent;
         const unsigned int R = (unsigned int)(ent >> 32);
         unsigned long long w;
@@ -143,7 +141,7 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
         pairs += w;
         if constexpr (CLS == CLS_TREE) {
             if (k > 2) {
-                eval_tree_dense<MEMO>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe);
+                eval_tree_dense<MEMO, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp);
                 nccp += w;
                 continue;
             }
@@ -155,7 +153,7 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
         nprobe += sink.nprobe;
         const unsigned long long idx = v.off[k] + R;
         p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
-        p.memo.dleft[idx] = (unsigned int)sink.best.l;
+        __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
         p.memo.dcard[idx] = sink.cS;
     }
 }
@@ -164,7 +162,8 @@ template <int CLS, typename Locate>
 __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
                             const unsigned int* rtab, const unsigned int* bin, unsigned int gen,
                             const unsigned long long* list, const Locate& loc, unsigned long long nsmall,
-                            unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe) {
+                            unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe,
+                            const uint2* binp = nullptr) {
     constexpr int MEMO = MEMO_DENSE;
     const unsigned long long total = (unsigned long long)gridDim.x * blockDim.x;
     unsigned int G = 1;
@@ -174,7 +173,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     // L1 lines (the list is a concatenation of warp runs of consecutive ranks)
     const unsigned long long c_lo = nsmall * blockIdx.x / gridDim.x, c_hi = nsmall * (blockIdx.x + 1) / gridDim.x;
     if (G == 1) {
-        small_phase_thread<CLS>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe);
+        small_phase_thread<CLS>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp);
         return;
     }
     const unsigned int sub = threadIdx.x & (G - 1);
@@ -182,7 +181,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     for (unsigned long long base = c_lo; base < c_hi; base += gpc) {      // same trip count on every lane
         const unsigned long long e = base + threadIdx.x / G;
         const bool act = e < c_hi;
-        const unsigned long long ent = act ? list[loc(e)] : 0ull;
+        const unsigned long long ent = act ? __ldcs(list + loc(e)) : 0ull;
         const uint32_t S = (uint32_t)ent;
         const unsigned int R = (unsigned int)(ent >> 32);
         Key best = key_inf();
@@ -207,7 +206,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
             pairs += w;
             const unsigned long long idx = v.off[k] + R;
             p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
-            p.memo.dleft[idx] = (unsigned int)best.l;
+            __stcs(p.memo.dleft + idx, (unsigned int)best.l);
             p.memo.dcard[idx] = cS;
         }
     }
@@ -241,6 +240,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     __shared__ Tri s_excl, s_agg;
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
+    unsigned int nbar = 0;                 // grid barriers passed (thread 0)
     const unsigned int gen = p.q->gen;
     const int n = p.n;
     __syncthreads();
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                 nprobe += sink.nprobe;
                 const unsigned long long idx = v.off[k] + qrank[e];
                 p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
-                p.memo.dleft[idx] = (unsigned int)sink.best.l;
+                __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
                 p.memo.dcard[idx] = sink.cS;
             }
             if (threadIdx.x == 0) {
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             o[5] = globaltimer_ns();
         }
 #endif
-        grid_sync(p.gbar, &p.result->error);
+        grid_sync(p.gbar, nbar, &p.result->error);
         TRACE(6);
 
         // deferred light sets (small list) and, on heavy levels, heavy-set cards
@@ -491,13 +491,13 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
             for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride)
                 p.hcard[h] = card_of(q, p.heavy[h]);
-            grid_sync(p.gbar, &p.result->error);
+            grid_sync(p.gbar, nbar, &p.result->error);
             heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, sp, sc, spr);
             if (counting) flush_counters(&p.desc[k], sp, sc, spr);
-            grid_sync(p.gbar, &p.result->error);
+            grid_sync(p.gbar, nbar, &p.result->error);
         } else if (nsmall) {
             if (counting) flush_counters(&p.desc[k], sp, sc, spr);
-            grid_sync(p.gbar, &p.result->error);
+            grid_sync(p.gbar, nbar, &p.result->error);
         }
     }
     if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {

@@ -66,7 +66,7 @@ template <typename M> struct Params {
     unsigned long long list_cap;           // light list capacity
     unsigned long long heavy_cap;          // heavy list capacity
     ResultDev* result;
-    unsigned int* gbar;                    // fused kernel: grid barrier {count, generation}
+    unsigned int* gbar;                    // whole-query kernels: grid barrier arrival counter
     unsigned int* seg_cnt;                 // list kernel: [2][kMaxGrid] per-CTA level-list counts
     unsigned long long heavy_levels;       // bit k: level k can have heavy sets
     unsigned long long item_of[kMaxN + 1]; // heavy work-item size per level
@@ -168,7 +168,10 @@ __global__ void k_init(const __grid_constant__ Params<M> p) {
         LevelDesc d = {};
         p.desc[i] = d;
     }
-    if (threadIdx.x == 0) p.result->error = 0;
+    if (threadIdx.x == 0) {
+        p.result->error = 0;
+        if (p.gbar) p.gbar[0] = 0;         // grid barrier arrival counter of the next launch
+    }
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) p.result->t_level[i] = 0;
     for (int i = threadIdx.x; i < kTraceCap; i += blockDim.x) p.result->trace[i] = 0;
 }
@@ -521,12 +524,25 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
 // exactly when p is a leaf split of G[S], which is the first element of the
 // descending walk; its card load travels with the first batch of probes.
 // Otherwise the product is evaluated in full.
-template <int MEMO>
+// Binomial pair of element position m of vertex v for the descending walk:
+// x = C(v, m+1), y = C(v, m+1) - C(v, m).  Either from a precomputed uint2
+// table (one 8-byte shared load) or from the plain 33 x 33 table.
+template <bool PAIRS>
+__device__ __forceinline__ uint2 tree_bin(const unsigned int* bin, const uint2* binp, int v, int m) {
+    if constexpr (PAIRS) {
+        return binp[v * 33 + m];
+    } else {
+        const unsigned int c1 = bin[v * 33 + m + 1], c0 = bin[v * 33 + m];
+        return make_uint2(c1, c1 - c0);
+    }
+}
+
+template <int MEMO, bool PAIRS = false>
 __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int gen, const MemoView& v,
                                                 const unsigned int* rtab, const unsigned int* bin, const SQ<uint32_t>& q,
-                                                uint32_t S, int k, unsigned int R, unsigned long long& nprobe) {
-    constexpr int BS = 33;                 // binomial row stride
-    constexpr int U = 4;                   // elements per unrolled step = probes in flight
+                                                uint32_t S, int k, unsigned int R, unsigned long long& nprobe,
+                                                const uint2* binp = nullptr) {
+    constexpr int U = 4;                   // elements per step = probes in flight
     uint32_t top = 0;
     for (int d = 0; d <= q.max_depth; d++) {
         const uint32_t T = S & q.depth_mask[d];
@@ -535,80 +551,82 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
             break;
         }
     }
+    const bool leaf_costs = q.pad != 0;    // any non-zero leaf cost in this query
+    const double* lvl = P.dcost + v.off[k - 1];
+    // ---- descending walk, U elements per step, branch-free: leaf splits get
+    // their incremental rank, splits at internal vertices are only recorded
+    unsigned int SD = 0;
+    uint32_t internal = 0, leaves = 0;
+    int m = k - 1;
+    uint32_t T = S;
     double best_c = __longlong_as_double(0x7ff0000000000000ll);
     uint32_t best_l = 0xffffffffu;
-    const bool leaf_costs = q.pad != 0;    // any non-zero leaf cost in this query
-    // ---- descending walk, U elements per step: leaf splits with incremental
-    // ranks, all their probes issued before any is consumed; splits at
-    // internal vertices are only recorded here
-    const double* lvl = P.dcost + v.off[k - 1];
-    unsigned int SD = 0;
-    uint32_t internal = 0;
-    int m = k - 1;
     double cS = 0.0;
-    bool first = true;
-    for (uint32_t T = S; T;) {
+    auto step = [&](bool guard, unsigned int* rk, uint32_t* lb) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool ok = !guard || T != 0;
+            const int vtx = ok ? 31 - __clz(T) : 0;
+            const uint32_t b = ok ? 1u << vtx : 0u;
+            T ^= b;
+            const uint2 cc = tree_bin<PAIRS>(bin, binp, vtx, ok ? m : 0);
+            const bool leaf = ok && b != top && (S & q.desc[vtx]) == b;   // v is a leaf of G[S]: B = S \ {v}
+            lb[u] = leaf ? b : 0u;
+            internal |= (ok && b != top && !leaf) ? b : 0u;
+            rk[u] = R - cc.x - SD;
+            SD += ok ? cc.y : 0u;
+            m -= ok ? 1 : 0;
+        }
+    };
+    auto consume = [&](const uint32_t* lb, const double* dv) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const double a = leaf_costs && lb[u] ? __dadd_rn(q.leaf[__ffs(lb[u]) - 1], dv[u]) : dv[u];
+            const double c = __dadd_rn(a, cS);
+            const uint32_t Bm = S ^ lb[u];
+            const uint32_t l = lb[u] < Bm ? lb[u] : Bm;
+            const bool better = lb[u] != 0u && (c < best_c || (c == best_c && l < best_l));
+            best_c = better ? c : best_c;
+            best_l = better ? l : best_l;
+            leaves |= lb[u];
+        }
+    };
+    {   // first step: its element 0 is max(S); card(S) from card(S \ max) (R19)
         unsigned int rk[U];
         uint32_t lb[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            lb[u] = 0;
-            rk[u] = 0;
-            if (T) {
-                const int vtx = 31 - __clz(T);
-                const uint32_t b = 1u << vtx;
-                T ^= b;
-                const unsigned int c1 = bin[vtx * BS + m + 1], c0 = bin[vtx * BS + m];
-                if (b != top) {
-                    if ((S & q.desc[vtx]) == b) {   // v is a leaf of G[S]: B = S \ {v}
-                        lb[u] = b;
-                        rk[u] = R - c1 - SD;
-                    } else {
-                        internal |= b;
-                    }
-                }
-                SD += c1 - c0;
-                m--;
-            }
-        }
         double dv[U];
+        step(k < U, rk, lb);
 #pragma unroll
         for (int u = 0; u < U; u++) dv[u] = lb[u] ? lvl[rk[u]] : 0.0;
-        if (first) {                       // lb[0] / rk[0] belong to max(S)
-            first = false;
-            const int p = 31 - __clz(S);
-            double x;
-            if (lb[0]) {
-                x = __dmul_rn(P.dcard[v.off[k - 1] + rk[0]], q.card[p]);
-            } else {
-                x = 1.0;
-                for (uint32_t A = S ^ (1u << p); A; A &= A - 1) {
-                    const int a = __ffs(A) - 1;
-                    x = __dmul_rn(x, q.card[a]);
-                    for (uint32_t W = S & q.adj[a] & ((1u << a) - 1u); W; W &= W - 1)
-                        x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + a]);
-                }
-                x = __dmul_rn(x, q.card[p]);
+        const int p = 31 - __clz(S);
+        double x;
+        if (lb[0]) {
+            x = __dmul_rn(__ldcs(P.dcard + v.off[k - 1] + rk[0]), q.card[p]);
+        } else {
+            x = 1.0;
+            for (uint32_t A = S ^ (1u << p); A; A &= A - 1) {
+                const int a = __ffs(A) - 1;
+                x = __dmul_rn(x, q.card[a]);
+                for (uint32_t W = S & q.adj[a] & ((1u << a) - 1u); W; W &= W - 1)
+                    x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + a]);
             }
-            for (uint32_t W = S & q.adj[p] & ((1u << p) - 1u); W; W &= W - 1)
-                x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + p]);
-            cS = x;
+            x = __dmul_rn(x, q.card[p]);
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (lb[u]) {
-                const double a = leaf_costs ? __dadd_rn(q.leaf[__ffs(lb[u]) - 1], dv[u]) : dv[u];
-                const double c = __dadd_rn(a, cS);
-                const uint32_t Bm = S ^ lb[u];
-                const uint32_t l = lb[u] < Bm ? lb[u] : Bm;
-                if (c < best_c || (c == best_c && l < best_l)) {
-                    best_c = c;
-                    best_l = l;
-                }
-                nprobe++;
-            }
-        }
+        for (uint32_t W = S & q.adj[p] & ((1u << p) - 1u); W; W &= W - 1)
+            x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + p]);
+        cS = x;
+        consume(lb, dv);
     }
+    for (int rem = k - U; rem > 0; rem -= U) {
+        unsigned int rk[U];
+        uint32_t lb[U];
+        double dv[U];
+        step(rem < U, rk, lb);
+#pragma unroll
+        for (int u = 0; u < U; u++) dv[u] = lb[u] ? lvl[rk[u]] : 0.0;
+        consume(lb, dv);
+    }
+    nprobe += __popc(leaves);
     Key best{(unsigned long long)__double_as_longlong(best_c), (unsigned long long)best_l};
     if (internal) {                        // generic splits: both sides are multi-vertex
         PairSink<uint32_t, MEMO> sink;
@@ -624,7 +642,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
     // ---- scatter with the rank already known
     const unsigned long long idx = v.off[k] + R;
     P.dcost[idx] = __longlong_as_double((long long)best.c);
-    P.dleft[idx] = (unsigned int)best.l;
+    __stcs(P.dleft + idx, (unsigned int)best.l);
     P.dcard[idx] = cS;
 }
 

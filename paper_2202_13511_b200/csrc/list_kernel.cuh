@@ -219,9 +219,17 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
     SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));
     unsigned int* bin = rtab + p.memo.rg.entries;                  // 33 x 33 binomials
+    // (C(v, m+1), C(v, m+1) - C(v, m)) pairs of the tree walk, 8-byte aligned
+    uint2* binp = reinterpret_cast<uint2*>(bin + 33 * 33 + ((p.memo.rg.entries + 33 * 33) & 1u));
     __shared__ MemoView v;
 
     memo_prologue<uint32_t, MEMO>(p, p.n, q, v, rtab);
+    unsigned int nbar = 0;                 // grid barriers passed (thread 0)
+    __syncthreads();
+    for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x) {
+        const int a = i / 32, b = i % 32;
+        binp[a * 33 + b] = make_uint2(bin[a * 33 + b + 1], bin[a * 33 + b + 1] - bin[a * 33 + b]);
+    }
     const unsigned int gen = p.q->gen;
     __syncthreads();
     unsigned long long* lists[2] = {reinterpret_cast<unsigned long long*>(p.light),
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
         p.desc[p.k_begin].seg = (unsigned int)(blockDim.x * list_rpt(p.share_hi[p.k_begin] - p.share_lo[p.k_begin]));
     __syncthreads();
     enum_to_list<CLS>(p, p.k_begin, q, bin, lists[p.k_begin & 1], cnts[p.k_begin & 1]);
-    grid_sync(p.gbar, &p.result->error);
+    grid_sync(p.gbar, nbar, &p.result->error);
     for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && k > p.k_begin) p.result->t_level[k] = globaltimer_ns();
         if (threadIdx.x == 0 && k < p.k_end) cnts[(k + 1) & 1][blockIdx.x] = 0;   // read by every CTA in phase k-1 only
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
 #ifdef MPDP_TRACE
         const unsigned long long ct_b = globaltimer_ns();
 #endif
-        if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe);
+        if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp);
         if (!enum_first) next_level();
 #ifdef MPDP_TRACE
         const unsigned long long ct_c = globaltimer_ns();
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
             o[7] = N;
         }
 #endif
-        grid_sync(p.gbar, &p.result->error);
+        grid_sync(p.gbar, nbar, &p.result->error);
     }
     if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
         p.result->t_level[p.n + 1] = globaltimer_ns();

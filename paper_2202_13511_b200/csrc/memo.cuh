@@ -253,7 +253,7 @@ __device__ __forceinline__ void memo_insert(const MemoPtrs& P, unsigned int gen,
     if (MEMO == MEMO_DENSE) {
         const unsigned long long idx = v.off[k] + rank_of(P.rg, rtab, (uint32_t)S);
         P.dcost[idx] = __longlong_as_double((long long)best.c);
-        P.dleft[idx] = (unsigned int)best.l;
+        __stcs(P.dleft + idx, (unsigned int)best.l);
         P.dcard[idx] = card;
     } else {
         hash_insert(P, gen, v.off[k], v.nb[k], S, best);

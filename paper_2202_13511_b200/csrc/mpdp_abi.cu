@@ -546,7 +546,7 @@ static const void* level_loop_kernel() {
 template <int CLS>
 static size_t level_loop_smem(int n) {
     return sizeof(SQ<uint32_t>) +
-           sizeof(unsigned int) * (rank_geom(n).entries + 33 * 33 + (CLS == CLS_TREE ? 0 : 2 * kFusedTile));
+           sizeof(unsigned int) * (rank_geom(n).entries + 33 * 33 + (CLS == CLS_TREE ? 1 + 2 * 33 * 33 : 2 * kFusedTile));
 }
 
 // The fused path: k_init, ONE cooperative persistent kernel for every level
@@ -661,6 +661,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     }
     auto launch = [&](Params<uint32_t>& p, unsigned long long grid) -> mpdp_status {
         void* args[] = {&p};
+        CUDA_TRY(c, cudaMemsetAsync(p.gbar, 0, sizeof(unsigned int), c->stream));   // barrier counter per launch
         CUDA_TRY(c, cudaLaunchCooperativeKernel(level_loop_kernel<CLS>(), dim3((unsigned int)grid), dim3(kBlock),
                                                 args, smem, c->stream));
         c->launches++;
