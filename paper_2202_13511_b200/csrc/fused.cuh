@@ -178,8 +178,11 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     }
     const unsigned int sub = threadIdx.x & (G - 1);
     const unsigned int gpc = blockDim.x / G;                 // groups per CTA
+    // groups in reverse thread order: with only a few sets per CTA the set and
+    // the level-ahead expansion (forward order) land on different warps
+    const unsigned int grp = gpc - 1 - threadIdx.x / G;
     for (unsigned long long base = c_lo; base < c_hi; base += gpc) {      // same trip count on every lane
-        const unsigned long long e = base + threadIdx.x / G;
+        const unsigned long long e = base + grp;
         const bool act = e < c_hi;
         const unsigned long long ent = act ? __ldcs(list + loc(e)) : 0ull;
         const uint32_t S = (uint32_t)ent;
