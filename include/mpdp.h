@@ -151,6 +151,13 @@ typedef struct {
 #define MPDP_FLAG_SIMULATE_WORLD 32u
 /* flags: shard every level across ranks, even small ones (testing)             */
 #define MPDP_FLAG_SHARD_ALL_LEVELS 64u
+/* Ablation: enumerate every set as Alg. generic_dpsub does
+ * (P:233-272): all 2^(|S|-1)-1 unordered splits with the CCP check on both
+ * sides, no Find-Blocks and no tree/complete fast paths.  The plan and cost are
+ * those of MPDP; pairs_evaluated becomes sum over connected S of
+ * (2^(|S|-1) - 1) (reading R3's unordered convention; "2805x" of P:319 is the
+ * ordered ratio).  The query runs through the general-graph kernels.           */
+#define MPDP_FLAG_DPSUB_ENUM 256u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

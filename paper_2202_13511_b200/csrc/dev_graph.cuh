@@ -15,7 +15,8 @@ template <typename M> struct QueryDev {
     static constexpr int N = MaxN<M>::value;
     int n, cls, max_depth, has_leaf_costs;
     unsigned long long epoch;   // look-back epoch base of this query (query counter << 6)
-    unsigned int gen, pad2;     // HASH memo tag of this query
+    unsigned int gen;           // HASH memo tag of this query
+    int dpsub;                  // MPDP_FLAG_DPSUB_ENUM ablation: every set is one CCP-checked block
     M adj[N];            // adjacency bitmaps ("adjacency lists ... as bitmap sets")
     M desc[N];           // CLS_TREE: vertices of the subtree rooted at v (root = 0)
     M depth_mask[N];     // CLS_TREE: vertices at depth d
@@ -29,6 +30,7 @@ template <typename M> struct QueryDev {
 template <typename M> struct SQ {
     static constexpr int N = MaxN<M>::value;
     int n, cls, max_depth, pad;            // pad = has_leaf_costs (any leaf cost != 0)
+    int dpsub, pad1;                       // DPSUB-enumeration ablation (QueryDev::dpsub)
     M adj[N];
     M desc[N];
     M depth_mask[N];
@@ -45,6 +47,7 @@ __device__ __forceinline__ void load_query(SQ<M>& s, const QueryDev<M>* q) {
         s.cls = q->cls;
         s.max_depth = q->max_depth;
         s.pad = q->has_leaf_costs;
+        s.dpsub = q->dpsub;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         s.adj[i] = q->adj[i];
@@ -189,6 +192,10 @@ __device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned lon
     if (CLS == CLS_CLIQUE) {
         w = (1ull << (k - 1)) - 1;
         return KIND_COMPLETE;
+    }
+    if (q.dpsub) {                         // ablation: Alg. generic_dpsub's enumeration
+        w = (1ull << (k - 1)) - 1;
+        return KIND_BLOCKS;
     }
     const int e2 = induced_degree_sum(q, S);
     if (e2 == 2 * (k - 1)) {

@@ -481,7 +481,13 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
     if (CLS != CLS_GENERAL) return;        // cliques are one complete block
     // KIND_BLOCKS
     M blk[MaxN<M>::value];
-    const int nb = find_blocks(q, S, blk);
+    int nb;
+    if (q.dpsub) {                         // ablation: the whole set is the only "block"
+        blk[0] = S;
+        nb = 1;
+    } else {
+        nb = find_blocks(q, S, blk);
+    }
     unsigned long long base = 0;
     for (int bi = 0; bi < nb && base < j1; bi++) {
         const M Bm = blk[bi];
@@ -491,7 +497,7 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
             base += wb;
             continue;
         }
-        const bool complete = induced_degree_sum(q, Bm) == b * (b - 1);
+        const bool complete = !q.dpsub && induced_degree_sum(q, Bm) == b * (b - 1);
         const unsigned long long a0 = (j0 > base ? j0 - base : 0), a1 = (j1 - base < wb ? j1 - base : wb);
         const M lo = lowbit(Bm), R = Bm ^ lo;
         M sub = deposit<M>(a0, R);

@@ -238,6 +238,7 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
     memset(q, 0, sizeof(QueryDev<M>));
     q->n = n;
     q->cls = c->cls;
+    q->dpsub = (c->flags & MPDP_FLAG_DPSUB_ENUM) ? 1 : 0;
     q->epoch = c->query_counter << 6;     // + level k (k <= 56 < 64)
     q->gen = c->wide ? c->gen8 : c->gen32;
     q->has_leaf_costs = 0;
@@ -1006,6 +1007,7 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
     if (n >= 3 && m == (unsigned long long)n * (n - 1) / 2) c->cls = CLS_CLIQUE;
     else if (m == (unsigned long long)(n - 1)) c->cls = CLS_TREE;
     else c->cls = CLS_GENERAL;
+    if (c->flags & MPDP_FLAG_DPSUB_ENUM) c->cls = CLS_GENERAL;   // ablation: the generic kernels
     const DevLayout prev = c->lay;
     st = plan_layout(c);
     if (st != MPDP_OK) return st;

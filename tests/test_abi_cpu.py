@@ -13,7 +13,8 @@ from conftest import ROOT
 def header_functions():
     text = open(os.path.join(ROOT, "include", "mpdp.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(mpdp_[a-z0-9_]+)\s*\(", text)))
+    # declared functions; not the function-pointer typedef "mpdp_status (*mpdp_inner_solver)(...)"
+    return sorted(set(re.findall(r"\b(mpdp_[a-z0-9_]+)\s*\((?!\s*\*)", text)))
 
 
 @pytest.fixture(scope="module")

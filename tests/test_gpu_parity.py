@@ -247,3 +247,34 @@ def test_sharded_world_default_threshold(world):
         with mpdp.Context(device=0, workspace_bytes=2 << 30, world=world, flags=mpdp.FLAG_SIMULATE_WORLD) as c:
             r = c.mpdp_optimize(g)
             check(r, o, g)
+
+
+@pytest.fixture(scope="module")
+def dpsub_ctx():
+    from paper_2202_13511_b200 import mpdp
+    with mpdp.Context(device=0, workspace_bytes=2 << 30, flags=mpdp.FLAG_DPSUB_ENUM) as c:
+        yield c
+
+
+@pytest.mark.parametrize("topo,n,seed", [("star", 9, 0), ("snowflake", 12, 1), ("chain", 10, 2), ("cycle", 9, 3),
+                                         ("clique", 8, 4), ("random", 11, 5), ("star", 2, 0), ("clique", 3, 1)])
+def test_dpsub_enumeration_ablation(dpsub_ctx, topo, n, seed):
+    """MPDP_FLAG_DPSUB_ENUM (NEXT-3 ablation, Alg. generic_dpsub):
+    same plan, cost and CCP pairs as MPDP; evaluated pairs = sum over connected
+    S of 2^(|S|-1) - 1 (unordered, reading R3), from the oracle's csg levels."""
+    g = W.generate(topo, n, seed)
+    r, o = dpsub_ctx.mpdp_optimize(g), O.optimize(g)
+    assert r.cost == o.cost and r.tree() == O.tree_of(o.nodes)
+    assert r.csg_count == o.csg_count and r.ccp_pairs == o.ccp_pairs and r.level_ccp == o.level_ccp
+    want = [c * ((1 << (k - 1)) - 1) if k >= 2 else 0 for k, c in enumerate(o.level_csg)]
+    assert r.level_pairs == want
+    assert r.pairs_evaluated == sum(want)
+
+
+def test_dpsub_star_closed_form(dpsub_ctx):
+    """Star-20 under DPSUB enumeration: sum_j C(19,j)(2^j - 1) = 3^19 - 2^19
+    evaluated pairs against MPDP's 19 * 2^18 (P:319's ratio, unordered)."""
+    g = W.star(20, 0)
+    r = dpsub_ctx.mpdp_optimize(g)
+    assert r.pairs_evaluated == 3 ** 19 - 2 ** 19
+    assert r.ccp_pairs == 19 * 2 ** 18
