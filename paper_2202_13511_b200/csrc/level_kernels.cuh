@@ -302,7 +302,7 @@ template <typename M, int CLS>
 __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<M> p, int k, unsigned long long nranks,
                                                  unsigned long long ntiles, unsigned long long item) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);    // only n and adj[] are used here
+    SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);    // only n, dpsub and adj[] are used here
     constexpr int NB = MaxN<M>::value + 1;
     unsigned long long* binom = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(SQ<M>));
     __shared__ unsigned long long s_tile;
@@ -311,7 +311,10 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
     const int n = p.q->n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) q.adj[i] = p.q->adj[i];
     for (int i = threadIdx.x; i < n * NB; i += blockDim.x) binom[i] = p.q->binom[i];
-    if (threadIdx.x == 0) q.n = n;
+    if (threadIdx.x == 0) {
+        q.n = n;
+        q.dpsub = p.q->dpsub;              // set_kind reads it
+    }
     const unsigned long long rmask = p.tiles_ring - 1;
     const unsigned long long epoch = lookback_epoch(p, k);
 
