@@ -570,7 +570,7 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     unsigned long long want = 1;
     for (int k = 2; k <= c->n; k++) {
         want = std::max(want, (binom_u64(c->n, k) + 511) / 512);
-        want = std::max(want, heavy_pair_bound(c->n, k, CLS) / 16384);
+        want = std::max(want, heavy_pair_bound(c->n, k, CLS) / 2048);
     }
     if (CLS == CLS_GENERAL && c->n > 12) want = ~0ull;     // heavy work unknown up front
     const unsigned int grid = (unsigned int)std::min<unsigned long long>(
