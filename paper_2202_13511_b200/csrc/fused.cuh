@@ -116,6 +116,77 @@ struct DenseLocate {
     __device__ __forceinline__ unsigned long long at(unsigned long long e, unsigned int&) const { return e; }
 };
 
+// Fused generation of level k+1 from an evaluated tree set S (list kernel;
+// the tree case of expand_to_list): a connected S' of size k+1
+// is emitted exactly once, from S = S' \ {u*} with u* its largest leaf.  For
+// S' = S u {v} (v adjacent to exactly one u in S) the leaves are
+// (leaves(S) \ {u}) u {v}, so v is accepted iff v > max(leaves(S) \ {u}).
+// The children are counted, reserved with one shared-memory atomic and written
+// to this CTA's segment of the next list; rank(S u {v}) = R + C(v, k+1) when v
+// is above max(S), else it is recomputed.
+struct EmitCtx {
+    unsigned long long* seg;               // this CTA's segment of the next level list
+    unsigned long long cap;                // its capacity
+    unsigned int* count;                   // shared-memory fill counter
+};
+
+__device__ __forceinline__ uint32_t children_of(const SQ<uint32_t>& q, uint32_t S, const TreeSetInfo& in) {
+    const uint32_t L = in.leaves;
+    const int m1 = 31 - __clz(L);                         // largest leaf (k >= 2: at least two leaves)
+    const uint32_t L2 = L & ~(1u << m1);
+    const int m2 = L2 ? 31 - __clz(L2) : -1;              // second largest
+    uint32_t cand = in.nb & ~S;
+    if (m2 >= 0) cand &= ~((2u << m2) - 1u);              // every accepted v exceeds the second largest leaf
+    uint32_t acc = 0;
+    for (uint32_t V = cand; V; V &= V - 1) {
+        const int v = __ffs(V) - 1;
+        const uint32_t u = q.adj[v] & S;                  // its one neighbour in S (tree)
+        const int thr = (u == (1u << m1)) ? m2 : m1;
+        if (v > thr) acc |= 1u << v;
+    }
+    return acc;
+}
+
+// Warp-cooperative write of the children (all active lanes call it together):
+// one shared-memory reservation per warp, children written vertex-major
+// (for each v, the lanes' S u {v} side by side), so the next level's list keeps
+// runs of colex-near sets -- consecutive parents give consecutive child ranks.
+__device__ __forceinline__ void emit_children(const unsigned int* bin, uint32_t S, unsigned int R, int k, uint32_t acc,
+                                              const EmitCtx& ec, unsigned int* err) {
+    const unsigned int act = __activemask();
+    const unsigned int lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
+    const unsigned int tot = __reduce_add_sync(act, (unsigned int)__popc(acc));
+    if (!tot) return;
+    const uint32_t any = __reduce_or_sync(act, acc);
+    const int leader = __ffs(act) - 1;
+    unsigned int base = 0;
+    if ((int)lane == leader) base = atomicAdd(ec.count, tot);
+    base = __shfl_sync(act, base, leader);
+    const int mx = 31 - __clz(S);
+    for (uint32_t V = any; V; V &= V - 1) {
+        const int v = __ffs(V) - 1;
+        const bool mine = (acc >> v) & 1u;
+        const unsigned int bal = __ballot_sync(act, mine);
+        if (mine) {
+            const unsigned long long d = base + __popc(bal & lt);
+            const uint32_t Sp = S | (1u << v);
+            unsigned int Rp;
+            if (v > mx) {
+                Rp = R + bin[v * 33 + k + 1];
+            } else {
+                Rp = 0;
+                int i = 1;
+                for (uint32_t T = Sp; T; T &= T - 1, i++) Rp += bin[(__ffs(T) - 1) * 33 + i];
+            }
+            if (d < ec.cap)
+                ec.seg[d] = ((unsigned long long)Rp << 32) | Sp;
+            else
+                atomicOr(err, ERR_CAPACITY);
+        }
+        base += __popc(bal);
+    }
+}
+
 // One thread per set (G = 1): the CTA's run is walked in rounds of blockDim;
 // the next list entry is loaded before the current set is evaluated (the set
 // evaluation is a latency chain, the list load should not add to it).
@@ -125,7 +196,8 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
                                                    unsigned int gen, const unsigned long long* list, const Locate& loc,
                                                    unsigned long long c_lo, unsigned long long c_hi,
                                                    unsigned long long& pairs, unsigned long long& nccp,
-                                                   unsigned long long& nprobe, const uint2* binp) {
+                                                   unsigned long long& nprobe, const uint2* binp,
+                                                   const EmitCtx* emit) {
     constexpr int MEMO = MEMO_DENSE;
     unsigned long long e = c_lo + threadIdx.x;
     if (e >= c_hi) return;
@@ -141,7 +213,14 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
         pairs += w;
         if constexpr (CLS == CLS_TREE) {
             if (k > 2) {
-                eval_tree_dense<MEMO, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp);
+                if (emit) {
+                    TreeSetInfo info;
+                    eval_tree_dense<MEMO, true, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp, &info);
+                    __syncwarp(__activemask());
+                    emit_children(bin, S, R, k, children_of(q, S, info), *emit, &p.result->error);
+                } else {
+                    eval_tree_dense<MEMO, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp);
+                }
                 nccp += w;
                 continue;
             }
@@ -163,7 +242,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
                             const unsigned int* rtab, const unsigned int* bin, unsigned int gen,
                             const unsigned long long* list, const Locate& loc, unsigned long long nsmall,
                             unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe,
-                            const uint2* binp = nullptr) {
+                            const uint2* binp = nullptr, const EmitCtx* emit = nullptr) {
     constexpr int MEMO = MEMO_DENSE;
     const unsigned long long total = (unsigned long long)gridDim.x * blockDim.x;
     unsigned int G = 1;
@@ -173,7 +252,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     // L1 lines (the list is a concatenation of warp runs of consecutive ranks)
     const unsigned long long c_lo = nsmall * blockIdx.x / gridDim.x, c_hi = nsmall * (blockIdx.x + 1) / gridDim.x;
     if (G == 1) {
-        small_phase_thread<CLS>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp);
+        small_phase_thread<CLS>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp, emit);
         return;
     }
     const unsigned int sub = threadIdx.x & (G - 1);

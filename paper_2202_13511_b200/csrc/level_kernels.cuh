@@ -546,11 +546,18 @@ __device__ __forceinline__ uint2 tree_bin(const unsigned int* bin, const uint2* 
     }
 }
 
-template <int MEMO, bool PAIRS = false>
+// Leaves and neighbourhood of a tree set, reported by the evaluation walk for
+// the fused generation of the next level (list kernel).
+struct TreeSetInfo {
+    uint32_t leaves;                       // degree-1 vertices of G[S]
+    uint32_t nb;                           // OR of the adjacency of S's vertices
+};
+
+template <int MEMO, bool PAIRS = false, bool INFO = false>
 __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int gen, const MemoView& v,
                                                 const unsigned int* rtab, const unsigned int* bin, const SQ<uint32_t>& q,
                                                 uint32_t S, int k, unsigned int R, unsigned long long& nprobe,
-                                                const uint2* binp = nullptr) {
+                                                const uint2* binp = nullptr, TreeSetInfo* info = nullptr) {
     constexpr int U = 4;                   // elements per step = probes in flight
     uint32_t top = 0;
     for (int d = 0; d <= q.max_depth; d++) {
@@ -565,7 +572,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
     // ---- descending walk, U elements per step, branch-free: leaf splits get
     // their incremental rank, splits at internal vertices are only recorded
     unsigned int SD = 0;
-    uint32_t internal = 0, leaves = 0;
+    uint32_t internal = 0, leaves = 0, nbm = 0;
     int m = k - 1;
     uint32_t T = S;
     double best_c = __longlong_as_double(0x7ff0000000000000ll);
@@ -580,6 +587,7 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
             T ^= b;
             const uint2 cc = tree_bin<PAIRS>(bin, binp, vtx, ok ? m : 0);
             const bool leaf = ok && b != top && (S & q.desc[vtx]) == b;   // v is a leaf of G[S]: B = S \ {v}
+            if constexpr (INFO) nbm |= ok ? q.adj[vtx] : 0u;
             lb[u] = leaf ? b : 0u;
             internal |= (ok && b != top && !leaf) ? b : 0u;
             rk[u] = R - cc.x - SD;
@@ -636,6 +644,10 @@ __device__ __forceinline__ void eval_tree_dense(const MemoPtrs& P, unsigned int 
         consume(lb, dv);
     }
     nprobe += __popc(leaves);
+    if constexpr (INFO) {                  // the top vertex is a leaf too when it has one neighbour in S
+        info->leaves = leaves | (__popc(q.adj[__ffs(top) - 1] & S) == 1 ? top : 0u);
+        info->nb = nbm;
+    }
     Key best{(unsigned long long)__double_as_longlong(best_c), (unsigned long long)best_l};
     if (internal) {                        // generic splits: both sides are multi-vertex
         PairSink<uint32_t, MEMO> sink;

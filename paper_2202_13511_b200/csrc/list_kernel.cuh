@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
         // level k+1: sparse expansion of this list when its candidates are far
         // fewer than the ranks (whole levels only: a rank share of a sharded
         // level is not closed under expansion)
-        bool expand = false;
+        bool expand = false, fused_grow = false;
         unsigned long long seg_next = 0;
         if (k < p.k_end) {
             const unsigned long long C1 = p.share_hi[k + 1] - p.share_lo[k + 1];
@@ -266,8 +266,16 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
             const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
             expand = CLS == CLS_TREE && whole && 4ull * N * (unsigned long long)(p.n - k) <= C1 &&
                      2ull * ((32ull * N + T - 1) / T) * (unsigned long long)(p.n - k) <= 32ull * ((C1 + T - 1) / T);
-            seg_next = expand ? ((N + gridDim.x - 1) / gridDim.x + 1) * (unsigned long long)(p.n - k)
-                              : (unsigned long long)blockDim.x * list_rpt(C1);
+            // dense tree levels (one thread per set): the evaluation walk itself
+            // generates level k+1 (emit_children), no rank scan
+            const unsigned long long seg_grow = ((N + gridDim.x - 1) / gridDim.x + 1) * (unsigned long long)(p.n - k);
+            // (only where the candidates are few next to the ranks: the rank scan
+            // writes the next list in colex order, which the star levels' probes
+            // need for locality -- measured 1.42 vs 1.59 ms on star-25)
+            fused_grow = CLS == CLS_TREE && whole && k >= 3 && 2ull * N > T && seg_grow * gridDim.x <= p.list_cap &&
+                         4ull * N * (unsigned long long)(p.n - k) <= C1;
+            if (fused_grow) expand = false;
+            seg_next = (expand || fused_grow) ? seg_grow : (unsigned long long)blockDim.x * list_rpt(C1);
             if (blockIdx.x == 0 && threadIdx.x == 0) p.desc[k + 1].seg = (unsigned int)seg_next;
         }
 #ifdef MPDP_TRACE
@@ -280,8 +288,12 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
         // first: ALU-bound enumeration overlaps latency-bound evaluation
         const bool enum_first = ((threadIdx.x >> 5) & 1) == 0;
         unsigned long long pairs = 0, nccp = 0, nprobe = 0;
+        __shared__ unsigned int s_emit;
+        if (threadIdx.x == 0) s_emit = 0;
+        __syncthreads();
+        const EmitCtx ectx{lists[(k + 1) & 1] + (unsigned long long)blockIdx.x * seg_next, seg_next, &s_emit};
         auto next_level = [&]() {
-            if (k >= p.k_end) return;
+            if (k >= p.k_end || fused_grow) return;
             if (expand)
                 expand_to_list(p, k, q, bin, lists[k & 1], loc, N, lists[(k + 1) & 1], cnts[(k + 1) & 1], seg_next);
             else
@@ -291,8 +303,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
 #ifdef MPDP_TRACE
         const unsigned long long ct_b = globaltimer_ns();
 #endif
-        if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp);
+        if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp,
+                                fused_grow ? &ectx : nullptr);
         if (!enum_first) next_level();
+        if (fused_grow) {
+            __syncthreads();
+            if (threadIdx.x == 0) cnts[(k + 1) & 1][blockIdx.x] = s_emit;
+        }
 #ifdef MPDP_TRACE
         const unsigned long long ct_c = globaltimer_ns();
         if ((threadIdx.x & 31) == 0) {

@@ -387,6 +387,12 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     // the list kernel's level lists are segmented per CTA (segments of blockDim *
     // ranks-per-thread entries), which can exceed C(n,k) by one rank per thread
     list_cap += (unsigned long long)kMaxGrid * kBlock;
+    // tree queries: the list kernel generates level k+1 from level k's sets in
+    // per-CTA segments of (sets per CTA + 1) * (n - k) entries (emit_children /
+    // expand_to_list); when this does not fit, it falls back to the rank scan
+    if (c->cls == CLS_TREE)
+        for (int k = 2; k < n; k++)
+            list_cap = std::max(list_cap, sat_mul(binom_u64(n, k) + 2ull * kMaxGrid, (unsigned long long)(n - k)));
     list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / 16);   // fused: two lists of (rank << 32 | mask)
     heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 40));
     L.tiles = take(sizeof(TileRec) * tiles_cap);
