@@ -24,6 +24,13 @@ def ctx():
 
 
 @pytest.fixture(scope="module")
+def big_ctx():
+    from paper_2202_13511_b200 import mpdp
+    with mpdp.Context(device=0, workspace_bytes=12 << 30) as c:
+        yield c
+
+
+@pytest.fixture(scope="module")
 def wide_ctx():
     from paper_2202_13511_b200 import mpdp
     with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_FORCE_WIDE_MASKS) as c:
@@ -88,6 +95,16 @@ def test_full_size_parity(ctx, topo, n, seed):
     ctx.mpdp_run()
     r = ctx.mpdp_fetch()
     check(r, O.optimize_dpccp(g), g)
+
+
+@pytest.mark.parametrize("topo,n,seed", [("snowflake", 24, 2), ("snowflake", 28, 3), ("chain", 28, 4)])
+def test_large_sparse_tree_parity(big_ctx, topo, n, seed):
+    """Sparse trees beyond the BASELINE sizes: the list kernel generates most
+    levels from the previous level's sets (expand_to_list with G lanes per set,
+    or the evaluation walk's emit_children for levels with more sets than half
+    the grid's threads) instead of scanning C(n, k+1) ranks."""
+    g = W.generate(topo, n, seed)
+    check(big_ctx.mpdp_optimize(g), O.optimize_dpccp(g), g)
 
 
 @pytest.mark.parametrize("topo,n,seed", [("star", 9, 0), ("clique", 10, 1), ("cycle", 12, 2),
