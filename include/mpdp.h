@@ -103,7 +103,8 @@ typedef struct {
     uint32_t enum_launches;        /* out: k_enum launches                            */
     uint32_t eval_launches;        /* out: k_eval launches                            */
     uint32_t memo_kind;            /* out: 1 = perfect-hash (colex rank) memo,
-                                           0 = Murmur3 open-addressing memo          */
+                                           0 = Murmur3 open-addressing memo,
+                                           2 = bitmask-indexed memo (MEMO_MASK)      */
     uint32_t inner_calls;          /* out, IDP2/UnionDP: inner exact DP calls          */
     double* level_ms;              /* optional [n+1]: device time of each level (fused
                                       kernel: %globaltimer at the level barriers; 0 on
@@ -158,6 +159,10 @@ typedef struct {
  * (2^(|S|-1) - 1) (reading R3's unordered convention; "2805x" of P:319 is the
  * ordered ratio).  The query runs through the general-graph kernels.           */
 #define MPDP_FLAG_DPSUB_ENUM 256u
+/* flags: keep the colex-rank memo layout on clique / general queries instead of
+ * the bitmask-indexed one (MEMO_MASK, used for n <= 24 on one GPU by the
+ * whole-query kernel); for ablations                                           */
+#define MPDP_FLAG_RANK_MEMO 512u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

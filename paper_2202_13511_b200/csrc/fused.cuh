@@ -92,14 +92,14 @@ __device__ __forceinline__ Key group_min(Key k, unsigned int G) {
 // bit for bit; card(S \ {p}) is read from the level k-1 memo (colex rank
 // R - C(p, k)) when S \ {p} is connected: p is a leaf of G[S] on trees (S and
 // desc[p] meet only in p), always on cliques.  Otherwise the full product.
-template <int CLS>
+template <int CLS, int MEMO = MEMO_DENSE>
 __device__ __forceinline__ double card_fast(const MemoPtrs& P, const MemoView& v, const unsigned int* bin,
                                             const SQ<uint32_t>& q, uint32_t S, int k, unsigned int R) {
     const int p = 31 - __clz(S);
     const uint32_t b = 1u << p;
     const bool in_memo = k >= 3 && ((CLS == CLS_TREE && (S & q.desc[p]) == b) || CLS == CLS_CLIQUE);
     if (!in_memo) return card_of(q, S);
-    double x = __dmul_rn(__ldcs(P.dcard + v.off[k - 1] + (R - bin[p * 33 + k])), q.card[p]);
+    double x = __dmul_rn(__ldcs(P.dcard + memo_slot_r<MEMO>(v, k - 1, R - bin[p * 33 + k], S ^ b)), q.card[p]);
     for (uint32_t W = S & q.adj[p] & (b - 1u); W; W &= W - 1) x = __dmul_rn(x, q.sel[(__ffs(W) - 1) * q.n + p]);
     return x;
 }
@@ -190,7 +190,7 @@ __device__ __forceinline__ void emit_children(const unsigned int* bin, uint32_t 
 // One thread per set (G = 1): the CTA's run is walked in rounds of blockDim;
 // the next list entry is loaded before the current set is evaluated (the set
 // evaluation is a latency chain, the list load should not add to it).
-template <int CLS, typename Locate>
+template <int CLS, int MEMO, typename Locate>
 __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q,
                                                    const MemoView& v, const unsigned int* rtab, const unsigned int* bin,
                                                    unsigned int gen, const unsigned long long* list, const Locate& loc,
@@ -198,7 +198,6 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
                                                    unsigned long long& pairs, unsigned long long& nccp,
                                                    unsigned long long& nprobe, const uint2* binp,
                                                    const EmitCtx* emit) {
-    constexpr int MEMO = MEMO_DENSE;
     unsigned long long e = c_lo + threadIdx.x;
     if (e >= c_hi) return;
     unsigned int cur = loc.seek(e);
@@ -211,7 +210,7 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
         unsigned long long w;
         const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
         pairs += w;
-        if constexpr (CLS == CLS_TREE) {
+        if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE) {
             if (k > 2) {
                 if (emit) {
                     TreeSetInfo info;
@@ -226,24 +225,23 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
             }
         }
         PairSink<uint32_t, MEMO> sink;
-        sink.init(&p.memo, gen, &v, rtab, &q, card_fast<CLS>(p.memo, v, bin, q, S, k, R));
+        sink.init(&p.memo, gen, &v, rtab, &q, card_fast<CLS, MEMO>(p.memo, v, bin, q, S, k, R));
         eval_range<uint32_t, CLS>(q, S, k, kind, 0, w, sink, nccp);
         sink.flush();
         nprobe += sink.nprobe;
-        const unsigned long long idx = v.off[k] + R;
+        const unsigned long long idx = memo_slot_r<MEMO>(v, k, R, S);
         p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
         __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
         p.memo.dcard[idx] = sink.cS;
     }
 }
 
-template <int CLS, typename Locate>
+template <int CLS, int MEMO, typename Locate>
 __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
                             const unsigned int* rtab, const unsigned int* bin, unsigned int gen,
                             const unsigned long long* list, const Locate& loc, unsigned long long nsmall,
                             unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe,
                             const uint2* binp = nullptr, const EmitCtx* emit = nullptr) {
-    constexpr int MEMO = MEMO_DENSE;
     const unsigned long long total = (unsigned long long)gridDim.x * blockDim.x;
     unsigned int G = 1;
     while (G < 32 && 2ull * G * nsmall <= total) G <<= 1;
@@ -252,7 +250,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     // L1 lines (the list is a concatenation of warp runs of consecutive ranks)
     const unsigned long long c_lo = nsmall * blockIdx.x / gridDim.x, c_hi = nsmall * (blockIdx.x + 1) / gridDim.x;
     if (G == 1) {
-        small_phase_thread<CLS>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp, emit);
+        small_phase_thread<CLS, MEMO>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp, emit);
         return;
     }
     const unsigned int sub = threadIdx.x & (G - 1);
@@ -271,7 +269,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
         double cS = 0.0;
         if (act) {
             const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
-            cS = card_fast<CLS>(p.memo, v, bin, q, S, k, R);
+            cS = card_fast<CLS, MEMO>(p.memo, v, bin, q, S, k, R);
             PairSink<uint32_t, MEMO> sink;
             sink.init(&p.memo, gen, &v, rtab, &q, cS);
             const unsigned long long per = (w + G - 1) / G;
@@ -286,7 +284,7 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
         best = group_min(best, G);
         if (act && sub == 0) {
             pairs += w;
-            const unsigned long long idx = v.off[k] + R;
+            const unsigned long long idx = memo_slot_r<MEMO>(v, k, R, S);
             p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
             __stcs(p.memo.dleft + idx, (unsigned int)best.l);
             p.memo.dcard[idx] = cS;
@@ -304,10 +302,10 @@ __device__ unsigned long long g_cta_arrive[(kMaxN + 1) * kCtaTraceMax * kCtaTrac
 #define CT_NOW(var)
 #endif
 
-template <int CLS>
+template <int CLS, int MEMO = MEMO_DENSE>
 __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(const __grid_constant__ Params<uint32_t> p) {
     using M = uint32_t;
-    constexpr int MEMO = MEMO_DENSE;
+    static_assert(MEMO != MEMO_HASH, "the whole-query kernels use the dense-layout memo");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<M>& q = *reinterpret_cast<SQ<M>*>(smem_raw);
     unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<M>));
@@ -500,7 +498,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                 unsigned long long w;
                 const int kind = set_kind<M, CLS>(q, S, k, w);
                 pairs += w;
-                if constexpr (CLS == CLS_TREE) {
+                if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE) {
                     if (k > 2) {
                         eval_tree_dense<MEMO>(p.memo, gen, v, rtab, bin, q, S, k, qrank[e], nprobe);
                         nccp += w;
@@ -512,7 +510,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                 eval_range<M, CLS>(q, S, k, kind, 0, w, sink, nccp);
                 sink.flush();
                 nprobe += sink.nprobe;
-                const unsigned long long idx = v.off[k] + qrank[e];
+                const unsigned long long idx = memo_slot_r<MEMO>(v, k, qrank[e], S);
                 p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
                 __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
                 p.memo.dcard[idx] = sink.cS;
@@ -559,7 +557,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 #ifdef MPDP_TRACE
         CT_NOW(ct_s0);
 #endif
-        if (nsmall) small_phase<CLS>(p, k, q, v, rtab, bin, gen, small_list, DenseLocate{}, nsmall, sp, sc, spr);
+        if (nsmall) small_phase<CLS, MEMO>(p, k, q, v, rtab, bin, gen, small_list, DenseLocate{}, nsmall, sp, sc, spr);
 #ifdef MPDP_TRACE
         if (threadIdx.x == 0 && blockIdx.x < kCtaTraceMax) {
             unsigned long long* o = g_cta_arrive + ((unsigned long long)k * kCtaTraceMax + blockIdx.x) * kCtaTraceSlots;

@@ -77,7 +77,7 @@ template <typename M> struct Params {
     unsigned long long count_levels;
     unsigned int share_lo[kMaxN + 1], share_hi[kMaxN + 1];
     int n;
-    int memo_kind;                         // MEMO_HASH / MEMO_DENSE
+    int memo_kind;                         // MEMO_HASH / MEMO_DENSE / MEMO_MASK
     double inv_load;                       // HASH: buckets = ceil(count * inv_load / 2)
 };
 
@@ -102,7 +102,7 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
 // keeping the lexicographic (cost, min(A, B)) minimum (reading R7).
 template <typename M, int MEMO>
 struct PairSink {
-    static constexpr int NP = (MEMO == MEMO_DENSE) ? 4 : 2;
+    static constexpr int NP = (MEMO != MEMO_HASH) ? 4 : 2;
     const MemoPtrs* P;                     // kernel parameter space
     const MemoView* v;
     const unsigned int* rtab;
@@ -674,15 +674,15 @@ __device__ __forceinline__ void memo_prologue(const Params<M>& p, int kmax, SQ<M
                                               unsigned int* rtab) {
     load_query(q, p.q);
     for (int j = threadIdx.x; j <= kmax; j += blockDim.x) {
-        if (MEMO == MEMO_DENSE) {
-            v.off[j] = p.dense_off[j];
+        if (MEMO != MEMO_HASH) {
+            v.off[j] = p.dense_off[j];         // (unused by MEMO_MASK)
             v.nb[j] = 0;
         } else {
             v.off[j] = (j >= 2) ? p.desc[j].bucket_off : 0;
             v.nb[j] = (j >= 2) ? p.desc[j].n_buckets : 0;
         }
     }
-    if (MEMO == MEMO_DENSE) {
+    if (MEMO != MEMO_HASH) {
         for (unsigned int i = threadIdx.x; i < p.memo.rg.entries; i += blockDim.x) rtab[i] = p.memo.rank_tab[i];
         // 32-bit binomials C(i, j), i < 33, j < 33, after the rank tables (tree fast path)
         unsigned int* bin = rtab + p.memo.rg.entries;

@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ P
 #ifdef MPDP_TRACE
         const unsigned long long ct_b = globaltimer_ns();
 #endif
-        if (N) small_phase<CLS>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp,
+        if (N) small_phase<CLS, MEMO>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp,
                                 fused_grow ? &ectx : nullptr);
         if (!enum_first) next_level();
         if (fused_grow) {

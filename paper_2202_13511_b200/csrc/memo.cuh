@@ -10,6 +10,12 @@
 //      8-bit chunks with tables in shared memory:
 //         rank(T) = sum_c R_c[popc(T below chunk c)][byte_c(T)],
 //         R_c[o][b] = sum_{bit i of b} C(8c + i, o + #(bits of b below i) + 1).
+//  MEMO_MASK   (clique / general queries, n <= kMaskMaxN, one GPU): the same
+//      three arrays indexed by the relation bitmask itself (2^n entries, all
+//      levels in one array).  A probe is one load with no rank arithmetic;
+//      the whole cost array (2 MB at n = 18) is L2-resident.  Trees keep the
+//      colex layout: their level-k-1 arrays are contiguous, bitmask slots of
+//      one level are scattered over all 2^n.
 //  MEMO_HASH   (n > 32, and as an ablation): Murmur3-finalised open addressing
 //      with linear probing over 32-byte buckets of two 16-byte slots
 //      {tagged key, cost}; a per-query tag in the key word makes stale slots of
@@ -19,7 +25,7 @@
 
 namespace mpdp {
 
-enum MemoKind : int { MEMO_HASH = 0, MEMO_DENSE = 1 };
+enum MemoKind : int { MEMO_HASH = 0, MEMO_DENSE = 1, MEMO_MASK = 2 };
 
 enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u, ERR_HANG = 16u };
 
@@ -35,6 +41,7 @@ __device__ __forceinline__ bool watchdog_expired(unsigned long long t0) {
 }
 
 constexpr int kRankChunks = 4;             // 4 x 8 bits cover n <= 32
+constexpr int kMaskMaxN = 24;              // MEMO_MASK: 2^24 x 20 B = 336 MB of arrays at most
 
 // Host/device-shared geometry of the chunked rank tables for n relations.
 struct RankGeom {
@@ -89,6 +96,18 @@ __device__ __forceinline__ unsigned int rank_of(const RankGeom& g, const unsigne
         }
     }
     return r;
+}
+
+// Slot of set T of size j in the dense-layout arrays (DENSE: level offset +
+// colex rank; MASK: the bitmask), and the same when the rank R is known.
+template <int MEMO>
+__device__ __forceinline__ unsigned long long memo_slot(const MemoView& v, const RankGeom& g, const unsigned int* tab,
+                                                         int j, uint32_t T) {
+    return MEMO == MEMO_MASK ? (unsigned long long)T : v.off[j] + rank_of(g, tab, T);
+}
+template <int MEMO>
+__device__ __forceinline__ unsigned long long memo_slot_r(const MemoView& v, int j, unsigned int R, uint32_t T) {
+    return MEMO == MEMO_MASK ? (unsigned long long)T : v.off[j] + R;
 }
 
 // -------------------------------------------------------------- hash memo
@@ -169,14 +188,14 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, unsigned int gen,
                                             const unsigned int* rtab,
                                             const SQ<M>& q, const M (&X)[NP], unsigned valid, double (&c)[NP],
                                             unsigned long long& nprobe) {
-    if (MEMO == MEMO_DENSE) {
+    if (MEMO != MEMO_HASH) {
         double d[NP];
 #pragma unroll
         for (int i = 0; i < NP; i++) {
             const int j = popc(X[i]);
             d[i] = 0.0;
             if (((valid >> i) & 1) && j > 1)
-                d[i] = P.dcost[v.off[j] + rank_of(P.rg, rtab, (uint32_t)X[i])];   // coherent load
+                d[i] = P.dcost[memo_slot<MEMO>(v, P.rg, rtab, j, (uint32_t)X[i])];   // coherent load
         }
 #pragma unroll
         for (int i = 0; i < NP; i++) {
@@ -250,8 +269,8 @@ __device__ __forceinline__ void memo_lookup(const MemoPtrs& P, unsigned int gen,
 template <typename M, int MEMO>
 __device__ __forceinline__ void memo_insert(const MemoPtrs& P, unsigned int gen, const MemoView& v,
                                             const unsigned int* rtab, int k, M S, const Key& best, double card) {
-    if (MEMO == MEMO_DENSE) {
-        const unsigned long long idx = v.off[k] + rank_of(P.rg, rtab, (uint32_t)S);
+    if (MEMO != MEMO_HASH) {
+        const unsigned long long idx = memo_slot<MEMO>(v, P.rg, rtab, k, (uint32_t)S);
         P.dcost[idx] = __longlong_as_double((long long)best.c);
         __stcs(P.dleft + idx, (unsigned int)best.l);
         P.dcard[idx] = card;
@@ -265,8 +284,8 @@ template <typename M, int MEMO>
 __device__ __forceinline__ double memo_get(const MemoPtrs& P, unsigned int gen, const MemoView& v,
                                            const unsigned int* rtab, M S, M& left) {
     const int j = popc(S);
-    if (MEMO == MEMO_DENSE) {
-        const unsigned long long idx = v.off[j] + rank_of(P.rg, rtab, (uint32_t)S);
+    if (MEMO != MEMO_HASH) {
+        const unsigned long long idx = memo_slot<MEMO>(v, P.rg, rtab, j, (uint32_t)S);
         left = (M)P.dleft[idx];
         return P.dcost[idx];
     } else {

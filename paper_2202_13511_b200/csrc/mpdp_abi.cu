@@ -32,6 +32,7 @@ struct DevLayout {
            hcard = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
+    bool mask_memo = false;               // dense arrays indexed by bitmask (MEMO_MASK)
     // multi-GPU sharding: per local shard its own level descriptors, result and
     // perfect-hash memo replica (shard 0 = the fields above)
     int nshards = 1;
@@ -129,7 +130,7 @@ struct mpdp_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool ran = false;
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
-    int fused_occ[3] = {}, fused_n[3] = {};
+    int fused_occ[6] = {}, fused_n[6] = {};   // [CLS + 3 * mask_memo]
     bool fused = false;                  // last run used the fused kernel
     bool sharded = false;                // last run used the sharded (multi-GPU) path
     struct SubProblem {                  // MPDP_FLAG_RECORD_SUBPROBLEMS
@@ -352,10 +353,18 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     // ceil(C(n,k)/W) fit (in-place allgather of the sharded levels)
     unsigned long long dense_entries = 0;
     for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k) + (unsigned long long)W;
+    // MEMO_MASK: clique / general queries on one GPU through the whole-query
+    // kernel index the same arrays by bitmask (2^n entries)
+    const bool mask = c->cls != CLS_TREE && W == 1 && !c->wide && n >= 2 && n <= kMaskMaxN &&
+                      !(c->flags & (MPDP_FLAG_HASH_MEMO | MPDP_FLAG_RANK_MEMO | MPDP_FLAG_NO_FUSED |
+                                    MPDP_FLAG_PROFILE_KERNELS)) &&
+                      c->timeout_ms <= 0;
+    if (mask) dense_entries = std::max(dense_entries, 1ull << n);
     const size_t dense_bytes = 2 * align_up(8 * dense_entries, 256) + align_up(4 * dense_entries, 256);
     const bool dense_ok = !c->wide && !(c->flags & MPDP_FLAG_HASH_MEMO) &&
                           (size_t)nsh * dense_bytes + 1024 <= memo_bytes;
     L.memo_kind = dense_ok ? MEMO_DENSE : MEMO_HASH;
+    L.mask_memo = dense_ok && mask;
     if (W > 1 && !dense_ok)
         return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs the perfect-hash memo (n <= 32) and " +
                                               std::to_string(nsh * dense_bytes >> 20) + " MiB of memo space");
@@ -544,11 +553,11 @@ static mpdp_status enqueue_query(mpdp_ctx* c, const Params<M>& p, bool sync_leve
 // The whole-query kernel of a class: trees (no heavy sets) use the level-list
 // kernel with enumerate-ahead, the other classes the tile kernel.
 template <int CLS>
-static const void* level_loop_kernel() {
+static const void* level_loop_kernel(bool mask_memo = false) {
     if constexpr (CLS == CLS_TREE)
         return (const void*)k_dp_list<CLS>;
     else
-        return (const void*)k_dp_fused<CLS>;
+        return mask_memo ? (const void*)k_dp_fused<CLS, MEMO_MASK> : (const void*)k_dp_fused<CLS, MEMO_DENSE>;
 }
 template <int CLS>
 static size_t level_loop_smem(int n) {
@@ -561,12 +570,15 @@ static size_t level_loop_smem(int n) {
 template <int CLS>
 static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     const size_t smem = level_loop_smem<CLS>(c->n);
-    int& occ = c->fused_occ[CLS];
-    if (!occ || c->fused_n[CLS] != c->n) {
-        CUDA_TRY(c, cudaFuncSetAttribute(level_loop_kernel<CLS>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, level_loop_kernel<CLS>(), kBlock, smem));
+    const bool mask = c->lay.mask_memo;
+    const void* kern = level_loop_kernel<CLS>(mask);
+    const int slot = CLS + (mask ? 3 : 0);
+    int& occ = c->fused_occ[slot];
+    if (!occ || c->fused_n[slot] != c->n) {
+        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
-        c->fused_n[CLS] = c->n;
+        c->fused_n[slot] = c->n;
     }
     CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
     k_init<uint32_t><<<1, 64, 0, c->stream>>>(p);
@@ -583,7 +595,7 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
         std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ), (unsigned long long)kMaxGrid);
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
     CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));    // device time of the fused kernel itself
-    CUDA_TRY(c, cudaLaunchCooperativeKernel(level_loop_kernel<CLS>(), dim3(grid), dim3(kBlock), args, smem, c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kBlock), args, smem, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
@@ -1128,7 +1140,7 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     out->d2h_bytes = c->d2h_bytes;
     out->enum_launches = c->enum_launches;
     out->eval_launches = c->eval_launches;
-    out->memo_kind = (uint32_t)c->lay.memo_kind;
+    out->memo_kind = c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
     out->enum_ms = out->eval_ms = 0;
     if (c->fused && c->nkev == 2) {      // the fused kernel: enumeration and evaluation together
         float t = 0;

@@ -203,9 +203,27 @@ def test_hash_memo_ablation_parity(hash_ctx, topo, n, seed):
     check(hash_ctx.mpdp_optimize(g), O.optimize(g), g)
 
 
+@pytest.mark.parametrize("topo,n,seed", [("clique", 12, 1), ("cycle", 16, 2), ("random", 15, 3),
+                                         ("clique", 16, 7), ("random", 16, 8)])
+def test_memo_layouts_agree(ctx, topo, n, seed):
+    """Clique / general queries use the bitmask-indexed memo (memo_kind 2) by
+    default; the colex-rank layout (MPDP_FLAG_RANK_MEMO) gives the same results."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate(topo, n, seed)
+    o = O.optimize(g)
+    r = ctx.mpdp_optimize(g)
+    assert r.memo_kind == 2, r.memo_kind
+    check(r, o, g)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_RANK_MEMO) as c:
+        r2 = c.mpdp_optimize(g)
+        assert r2.memo_kind == 1
+        check(r2, o, g)
+    assert ctx.mpdp_optimize(W.star(12, seed)).memo_kind == 1     # trees keep the colex layout
+
+
 def test_alternating_memo_kinds(ctx, hash_ctx):
     # interleave both memo layouts and widths on one device
-    for g in [W.star(12, 1), W.clique(9, 2), W.random_connected(13, 3)]:
+    for g in [W.star(12, 1), W.clique(9, 2), W.random_connected(13, 3), W.star(11, 4), W.cycle(12, 5)]:
         o = O.optimize(g)
         check(ctx.mpdp_optimize(g), o, g)
         check(hash_ctx.mpdp_optimize(g), o, g)
