@@ -292,6 +292,199 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     }
 }
 
+// ------------------------------------------------------------ clique levels
+// Cliques with the bitmask memo: every k-subset is connected and is one
+// complete block (Lemma 8), so set h of level k IS the colex rank h and
+// its join pairs are j = 0 .. w-1 with w = 2^(k-1) - 1:
+//     A_j = lowbit(S) | deposit(j, S \ lowbit(S)),   B_j = S \ A_j
+// (Alg. mpdp_generalization P:545-568 with one block and no CCP checks).
+// The level's pair space [0, C(n,k) * w) is cut into one contiguous chunk per
+// warp (>= 1024 pairs), lanes interleaved over j so that a warp's probes fall
+// into few memo lines -- no enumeration, compaction, look-back or heavy list.
+// A set cut by chunk boundaries is merged through the slot of the first chunk
+// that touches it (128-bit CAS min + pair count; the last contributor
+// scatters); slots alternate between two buffers by level parity and each
+// warp clears its slot of the next level's buffer.  Sets with fewer than 32
+// pairs (k <= 5) take G = 2^(k-1) lanes each, one pair per lane.
+// Memo entries of level 1 (leaf cost, card) are written at k = 2, so probes
+// of levels >= 3 are branch-free loads.
+template <int G>
+__device__ __forceinline__ void clique_eval_span(const SQ<uint32_t>& q, const double* __restrict__ dcost, uint32_t S,
+                                                 uint32_t lo, uint32_t R, uint32_t DG, uint32_t sub,
+                                                 unsigned long long j, unsigned long long b, double cS, bool leaves,
+                                                 Key& best) {
+    // pairs j, j + G, j + 2G, ... of the set; 4 pairs (8 probes) in flight
+    for (; j < b; j += 4 * G) {
+        uint32_t A[4];
+        double ca[4], cb[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const bool ok = j + (unsigned long long)(G * u) < b;
+            A[u] = lo | sub;
+            const uint32_t B = S ^ A[u];
+            if (leaves) {
+                ca[u] = ok ? q.leaf[__ffs(A[u]) - 1] : 0.0;
+                cb[u] = ok ? q.leaf[__ffs(B) - 1] : 0.0;
+            } else {
+                ca[u] = ok ? dcost[A[u]] : 0.0;
+                cb[u] = ok ? dcost[B] : 0.0;
+            }
+            sub = ((sub | ~R) + DG) & R;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (j + (unsigned long long)(G * u) < b) {
+                const double c = __dadd_rn(__dadd_rn(ca[u], cb[u]), cS);
+                const uint32_t B = S ^ A[u];
+                const Key key{(unsigned long long)__double_as_longlong(c), (unsigned long long)(A[u] < B ? A[u] : B)};
+                if (key_less(key, best)) best = key;
+            }
+        }
+    }
+}
+
+// deposit(j, R) for j < 2^popc(R) without a bit loop over j: lowest five bits
+// of j through R's lowest five elements, the rest as a masked add
+__device__ __forceinline__ uint32_t deposit_small(unsigned int j, uint32_t R) {
+    uint32_t out = 0;
+    for (uint32_t T = R; j; T &= T - 1, j >>= 1)
+        if (j & 1u) out |= T & (0u - T);
+    return out;
+}
+
+__device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, const Key& best, double cS) {
+    P.dcost[S] = __longlong_as_double((long long)best.c);
+    __stcs(P.dleft + S, (unsigned int)best.l);
+    P.dcard[S] = cS;
+}
+
+// lanes per set of w pairs: the power of two nearest (w + 1) / 8, 1..32
+__host__ __device__ __forceinline__ unsigned int clique_group(unsigned long long w) {
+    unsigned int G = 1;
+    while (G < 32 && 8ull * G < w + 1) G <<= 1;
+    return G;
+}
+
+template <int G>
+__device__ void clique_groups(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                              const unsigned int* bin, unsigned int C, unsigned long long w,
+                              unsigned long long probes_per_set, bool leaves, unsigned long long& pairs,
+                              unsigned long long& nccp, unsigned long long& nprobe, unsigned long long& nsets) {
+    constexpr int MEMO = MEMO_MASK;
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long ngroups = nthreads / G, grp = gtid / G;
+    const unsigned int sub = threadIdx.x & (G - 1);
+    const unsigned long long h0 = C * grp / ngroups, h1 = C * (grp + 1) / ngroups;
+    const unsigned long long rounds = (C + ngroups - 1) / ngroups;       // >= h1 - h0 on every group
+    uint32_t S = h0 < h1 ? unrank_colex32(bin, q.n, k, (unsigned int)h0) : 0u;
+    for (unsigned long long it = 0; it < rounds; it++) {
+        const unsigned long long h = h0 + it;
+        const bool act = h < h1;
+        Key best = key_inf();
+        double cS = 0.0;
+        if (act) {
+            cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, (unsigned int)h);
+            const uint32_t lo = S & (0u - S), R = S ^ lo;
+            clique_eval_span<G>(q, p.memo.dcost, S, lo, R, deposit_small(G, R), deposit_small(sub, R), sub, w, cS,
+                                leaves, best);
+        }
+        best = group_min(best, G);
+        if (act && sub == 0) {
+            clique_write(p.memo, S, best, cS);
+            pairs += w;
+            nccp += w;
+            nprobe += probes_per_set;
+            nsets++;
+        }
+        if (act) S = gosper(S);
+    }
+}
+
+__device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                             const unsigned int* bin, unsigned long long& pairs, unsigned long long& nccp,
+                             unsigned long long& nprobe, unsigned long long& nsets) {
+    constexpr int MEMO = MEMO_MASK;
+    const int n = q.n;
+    const unsigned int C = bin[n * 33 + k];
+    const unsigned long long w = (1ull << (k - 1)) - 1;
+    const unsigned long long probes_per_set = k >= 3 ? 2 * w - (unsigned long long)k : 0ull;
+    const unsigned int lane = threadIdx.x & 31;
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long nwarps = nthreads >> 5, gw = gtid >> 5;
+    Key* slot_key = p.bkey + (k & 1) * nwarps;
+    unsigned long long* slot_done = p.bdone + (k & 1) * nwarps;
+    if (lane == 0) {                       // this warp's slot of level k+1
+        p.bkey[((k + 1) & 1) * nwarps + gw] = key_inf();
+        p.bdone[((k + 1) & 1) * nwarps + gw] = 0;
+    }
+    const bool leaves = k == 2;
+    if (leaves && gtid < (unsigned long long)n) {      // level-1 entries
+        p.memo.dcost[1u << gtid] = q.leaf[gtid];
+        p.memo.dcard[1u << gtid] = q.card[gtid];
+    }
+    // G lanes per set, about 8 pairs per lane: G = 1, 2, 4, 8, 16 up to
+    // w = 127; whole sets, contiguous runs per group (Gosper successor)
+    const unsigned int G = clique_group(w);
+    if (G < 32) {
+        switch (G) {
+            case 1: clique_groups<1>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 2: clique_groups<2>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 4: clique_groups<4>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 8: clique_groups<8>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            default: clique_groups<16>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+        }
+        return;
+    }
+    const unsigned long long P = (unsigned long long)C * w;
+    unsigned long long csize = (P + nwarps - 1) / nwarps;
+    if (csize < 1024) csize = 1024;
+    const unsigned long long c0 = gw * csize;
+    if (c0 >= P) return;
+    const unsigned long long c1 = c0 + csize < P ? c0 + csize : P;
+    unsigned long long h = c0 / w, a = c0 - h * w;
+    uint32_t S = unrank_colex32(bin, n, k, (unsigned int)h);
+    while (true) {
+        const unsigned long long hw = h * w;
+        const unsigned long long b = c1 - hw < w ? c1 - hw : w;
+        const double cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, (unsigned int)h);
+        const uint32_t lo = S & (0u - S), R = S ^ lo;
+        const uint32_t D32 = deposit_small(32, R);
+        // deposit(a + lane) = deposit(a) (+) deposit(lane) in R's domain
+        const uint32_t da = a ? deposit<uint32_t>(a, R) : 0u;
+        const uint32_t sub = ((da | ~R) + deposit_small(lane, R)) & R;
+        Key best = key_inf();
+        clique_eval_span<32>(q, p.memo.dcost, S, lo, R, D32, sub, a + lane, b, cS, false, best);
+        best = warp_min(best);
+        if (lane == 0) {
+            pairs += b - a;
+            nccp += b - a;
+            if (a == 0 && b == w) {
+                clique_write(p.memo, S, best, cS);
+                nprobe += probes_per_set;
+                nsets++;
+            } else {
+                const unsigned long long sl = hw / csize;     // first chunk touching set h
+                atomic_key_min(&slot_key[sl], best);
+                __threadfence();
+                const unsigned long long old = atomicAdd(&slot_done[sl], b - a);
+                if (old + (b - a) == w) {      // last contributor scatters the set
+                    __threadfence();
+                    const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&slot_key[sl]);
+                    clique_write(p.memo, S, Key{ld_relaxed(kp), ld_relaxed(kp + 1)}, cS);
+                    nprobe += probes_per_set;
+                    nsets++;
+                }
+            }
+        }
+        if (hw + b >= c1) break;
+        h++;
+        a = 0;
+        S = gosper(S);
+    }
+}
+
 #ifdef MPDP_TRACE
 // per-CTA arrival time at each level's barrier (debug builds only)
 constexpr int kCtaTraceMax = 1024;
@@ -338,6 +531,17 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 #endif
     for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+        if constexpr (CLS == CLS_CLIQUE && MEMO == MEMO_MASK) {    // one phase and one barrier per level
+            unsigned long long pairs = 0, nccp = 0, nprobe = 0, nsets = 0;
+            clique_level(p, k, q, v, bin, pairs, nccp, nprobe, nsets);
+            if ((p.count_levels >> k) & 1ull) {
+                flush_counters(&p.desc[k], pairs, nccp, nprobe);
+                nsets = warp_sum(nsets);
+                if ((threadIdx.x & 31) == 0 && nsets) atomicAdd(&p.desc[k].n_light, nsets);
+            }
+            grid_sync(p.gbar, nbar, &p.result->error);
+            continue;
+        }
         TRACE(0);
 #ifdef MPDP_TRACE
         CT_NOW(ct_lvl0);
@@ -572,7 +776,9 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride)
                 p.hcard[h] = card_of(q, p.heavy[h]);
             grid_sync(p.gbar, nbar, &p.result->error);
+            TRACE(7);
             heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, sp, sc, spr);
+            TRACE(7);
             if (counting) flush_counters(&p.desc[k], sp, sc, spr);
             grid_sync(p.gbar, nbar, &p.result->error);
         } else if (nsmall) {

@@ -793,12 +793,28 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
             const int kind = set_kind<M, CLS>(q, S, k, wk);
             PairSink<M, MEMO> sink;
             sink.init(&p.memo, gen, &v, rtab, &q, p.hcard[h]);
-            // lane-contiguous chunks of the segment [a, b)
-            const unsigned long long cnt = b - a, per = (cnt + 31) >> 5;
-            unsigned long long j0 = a + per * lane, j1 = j0 + per;
-            if (j0 > b) j0 = b;
-            if (j1 > b) j1 = b;
-            eval_range<M, CLS>(q, S, k, kind, j0, j1, sink, nccp);
+            const unsigned long long cnt = b - a;
+            if (kind == KIND_COMPLETE) {
+                // lane-interleaved pairs j = a + lane + 32 i: the lanes' left
+                // sides differ in the lowest elements of S, so one warp's probes
+                // fall into few memo lines; +32 in the deposited domain is a
+                // masked add (carries skip the bits outside R)
+                const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;   // (<= 32 pairs: one round)
+                unsigned long long j = a + lane;
+                M sub = j < b ? deposit<M>(j, R) : 0;
+                for (; j < b; j += 32) {
+                    const M A = lo | sub;
+                    sink.add(A, S ^ A);
+                    sub = ((sub | ~R) + D) & R;
+                    nccp++;
+                }
+            } else {                               // lane-contiguous chunks of [a, b)
+                const unsigned long long per = (cnt + 31) >> 5;
+                unsigned long long j0 = a + per * lane, j1 = j0 + per;
+                if (j0 > b) j0 = b;
+                if (j1 > b) j1 = b;
+                eval_range<M, CLS>(q, S, k, kind, j0, j1, sink, nccp);
+            }
             sink.flush();
             nprobe += sink.nprobe;
             const Key best = warp_min(sink.best);

@@ -402,8 +402,14 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     if (c->cls == CLS_TREE)
         for (int k = 2; k < n; k++)
             list_cap = std::max(list_cap, sat_mul(binom_u64(n, k) + 2ull * kMaxGrid, (unsigned long long)(n - k)));
+    // cliques with the bitmask memo merge split sets through two buffers of
+    // one (key, count) slot per warp of the grid (clique_level)
+    if (L.mask_memo && c->cls == CLS_CLIQUE)
+        heavy_cap = std::max<unsigned long long>(heavy_cap, 2ull * kMaxGrid * (kBlock / 32));
     list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / 16);   // fused: two lists of (rank << 32 | mask)
     heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 40));
+    if (L.mask_memo && c->cls == CLS_CLIQUE && heavy_cap < 2ull * kMaxGrid * (kBlock / 32))
+        return fail(c, MPDP_ERR_CAPACITY, "workspace too small for the clique merge slots");
     L.tiles = take(sizeof(TileRec) * tiles_cap);
     L.light = take(16 * list_cap);
     L.heavy = take(msz * heavy_cap);
