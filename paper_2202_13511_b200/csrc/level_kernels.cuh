@@ -890,8 +890,10 @@ __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView
         r->n_nodes = 0;
         return;
     }
-    // explicit-stack post-order walk
-    M st_set[2 * kMaxN];
+    // explicit-stack post-order walk; one memo read per internal node (its
+    // left, cost and, in the dense layouts, card are kept on the stack)
+    M st_set[2 * kMaxN], st_L[2 * kMaxN];
+    double st_c[2 * kMaxN], st_card[2 * kMaxN];
     int st_state[2 * kMaxN], st_left[2 * kMaxN];
     int sp = 0, nn = 0;
     const M all = (n == (int)(8 * sizeof(M))) ? ~(M)0 : (bitm<M>(n) - 1);
@@ -915,9 +917,10 @@ __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView
             --sp;
             continue;
         }
-        M L;
-        const double c = memo_get<M, MEMO>(p.memo, gen, v, rtab, S, L);
         if (st_state[top] == 0) {
+            M L;
+            st_c[top] = memo_get<M, MEMO>(p.memo, gen, v, rtab, S, L, &st_card[top]);
+            st_L[top] = L;
             st_state[top] = 1;
             st_set[sp] = L;
             st_state[sp] = 0;
@@ -925,7 +928,7 @@ __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView
         } else if (st_state[top] == 1) {
             st_left[top] = last;
             st_state[top] = 2;
-            st_set[sp] = S & ~L;
+            st_set[sp] = S & ~st_L[top];
             st_state[sp] = 0;
             sp++;
         } else {
@@ -935,8 +938,8 @@ __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView
             nd.relation = -1;
             nd.reserved = 0;
             nd.set = (unsigned long long)S;
-            nd.cardinality = card_of(q, S);
-            nd.cost = c;
+            nd.cardinality = MEMO != MEMO_HASH ? st_card[top] : card_of(q, S);   // (reading R5: bit-equal)
+            nd.cost = st_c[top];
             last = nn++;
             --sp;
         }

@@ -282,11 +282,12 @@ __device__ __forceinline__ void memo_insert(const MemoPtrs& P, unsigned int gen,
 // (cost, left) of a finished set (extraction)
 template <typename M, int MEMO>
 __device__ __forceinline__ double memo_get(const MemoPtrs& P, unsigned int gen, const MemoView& v,
-                                           const unsigned int* rtab, M S, M& left) {
+                                           const unsigned int* rtab, M S, M& left, double* card = nullptr) {
     const int j = popc(S);
     if (MEMO != MEMO_HASH) {
         const unsigned long long idx = memo_slot<MEMO>(v, P.rg, rtab, j, (uint32_t)S);
         left = (M)P.dleft[idx];
+        if (card) *card = P.dcard[idx];
         return P.dcost[idx];
     } else {
         unsigned long long slot = 0;

@@ -619,9 +619,9 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
 // [r*seg, (r+1)*seg) of the level (seg = ceil(C(n,k)/W)) with the fused kernel
 // restricted to that share; its memo entries are then one contiguous segment
 // of the level's perfect-hash array, so the exchange is an in-place
-// ncclAllGather of `seg` costs and `seg` left masks (plus `seg` cards on trees
-// and cliques, where card(S) is derived from card(S \ max)) per rank -- no packing and
-// no replica insert.  Levels below kShardMinRanks are computed redundantly by
+// ncclAllGather of `seg` costs, `seg` left masks and `seg` cards per rank (the
+// cards feed card(S) = card(S \ max) x ... and the plan extraction) -- no
+// packing and no replica insert.  Levels below kShardMinRanks are computed redundantly by
 // every rank (counted by rank 0 only).  Counters are summed with one
 // ncclAllReduce at the end; every rank extracts the identical plan from its
 // complete replica.  In simulated mode the ranks are shards of this context
@@ -717,7 +717,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
             if (st != MPDP_OK) return st;
         }
         if (sharded) {
-            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, CLS == CLS_TREE || CLS == CLS_CLIQUE);
+            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, true);   // cards: card_fast and the extraction read them
             if (st != MPDP_OK) return st;
         }
         CUDA_TRY(c, cudaGetLastError());
