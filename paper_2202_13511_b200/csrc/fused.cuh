@@ -190,6 +190,44 @@ __device__ __forceinline__ void emit_children(const unsigned int* bin, uint32_t 
 // One thread per set (G = 1): the CTA's run is walked in rounds of blockDim;
 // the next list entry is loaded before the current set is evaluated (the set
 // evaluation is a latency chain, the list load should not add to it).
+// One set, one thread: evaluate, min, memo scatter (and, on fused-grow tree
+// levels, the children of the set).
+template <int CLS, int MEMO>
+__device__ __forceinline__ void eval_set_thread(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q,
+                                                const MemoView& v, const unsigned int* rtab, const unsigned int* bin,
+                                                unsigned int gen, unsigned long long ent, unsigned long long& pairs,
+                                                unsigned long long& nccp, unsigned long long& nprobe,
+                                                const uint2* binp, const EmitCtx* emit) {
+    const uint32_t S = (uint32_t)ent;
+    const unsigned int R = (unsigned int)(ent >> 32);
+    unsigned long long w;
+    const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
+    pairs += w;
+    if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE) {
+        if (k > 2) {
+            if (emit) {
+                TreeSetInfo info;
+                eval_tree_dense<MEMO, true, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp, &info);
+                __syncwarp(__activemask());
+                emit_children(bin, S, R, k, children_of(q, S, info), *emit, &p.result->error);
+            } else {
+                eval_tree_dense<MEMO, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp);
+            }
+            nccp += w;
+            return;
+        }
+    }
+    PairSink<uint32_t, MEMO> sink;
+    sink.init(&p.memo, gen, &v, rtab, &q, card_fast<CLS, MEMO>(p.memo, v, bin, q, S, k, R));
+    eval_range<uint32_t, CLS>(q, S, k, kind, 0, w, sink, nccp);
+    sink.flush();
+    nprobe += sink.nprobe;
+    const unsigned long long idx = memo_slot_r<MEMO>(v, k, R, S);
+    p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
+    __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
+    p.memo.dcard[idx] = sink.cS;
+}
+
 template <int CLS, int MEMO, typename Locate>
 __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q,
                                                    const MemoView& v, const unsigned int* rtab, const unsigned int* bin,
@@ -205,34 +243,7 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
     for (; e < c_hi; e += blockDim.x) {
         const unsigned long long ent = nxt;
         if (e + blockDim.x < c_hi) nxt = __ldcs(list + loc.at(e + blockDim.x, cur));
-        const uint32_t S = (uint32_t)ent;
-        const unsigned int R = (unsigned int)(ent >> 32);
-        unsigned long long w;
-        const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
-        pairs += w;
-        if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE) {
-            if (k > 2) {
-                if (emit) {
-                    TreeSetInfo info;
-                    eval_tree_dense<MEMO, true, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp, &info);
-                    __syncwarp(__activemask());
-                    emit_children(bin, S, R, k, children_of(q, S, info), *emit, &p.result->error);
-                } else {
-                    eval_tree_dense<MEMO, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, binp);
-                }
-                nccp += w;
-                continue;
-            }
-        }
-        PairSink<uint32_t, MEMO> sink;
-        sink.init(&p.memo, gen, &v, rtab, &q, card_fast<CLS, MEMO>(p.memo, v, bin, q, S, k, R));
-        eval_range<uint32_t, CLS>(q, S, k, kind, 0, w, sink, nccp);
-        sink.flush();
-        nprobe += sink.nprobe;
-        const unsigned long long idx = memo_slot_r<MEMO>(v, k, R, S);
-        p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
-        __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
-        p.memo.dcard[idx] = sink.cS;
+        eval_set_thread<CLS, MEMO>(p, k, q, v, rtab, bin, gen, ent, pairs, nccp, nprobe, binp, emit);
     }
 }
 

@@ -213,7 +213,7 @@ __device__ __forceinline__ void seg_prefix(const unsigned int* cnt, unsigned int
 }
 
 template <int CLS>
-__global__ void __launch_bounds__(kBlock, 3) k_dp_list(const __grid_constant__ Params<uint32_t> p) {
+__global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ Params<uint32_t> p) {
     constexpr int MEMO = MEMO_DENSE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
