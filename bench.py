@@ -278,7 +278,7 @@ def run_ours(args):
     # 8 B cost + 4 B left insert; open-addressing memo = 16 B slot per probe,
     # per set list write + read + 16 B slot + left.
     msz = 4 if n <= 32 else 8
-    if memo_kind in (1, 2):                   # colex-rank or bitmask-indexed arrays: same bytes
+    if memo_kind in (1, 2, 3):                # colex-rank or bitmask-indexed arrays: same bytes
         alg_bytes = 8 * probes_total + sets_total * (16 + 8 + 4)
     else:
         alg_bytes = 16 * probes_total + sets_total * (2 * msz + 16 + msz)
@@ -297,7 +297,8 @@ def run_ours(args):
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
             "traffic_source": traffic.get("source") if traffic else None,
             "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-            "memo": {1: "perfect-hash (colex rank)", 2: "bitmask-indexed (MEMO_MASK)"}.get(
+            "memo": {1: "perfect-hash (colex rank)", 2: "bitmask-indexed (MEMO_MASK)",
+                     3: "shared-memory bitmask memo (single CTA)"}.get(
                 memo_kind, "murmur3 open addressing"),
             "algorithmic_bytes_per_launch": alg_bytes / max(1, kernel_launches),
             "avg_launch_ms": kernel_ms / max(1, kernel_launches),

@@ -104,7 +104,9 @@ typedef struct {
     uint32_t eval_launches;        /* out: k_eval launches                            */
     uint32_t memo_kind;            /* out: 1 = perfect-hash (colex rank) memo,
                                            0 = Murmur3 open-addressing memo,
-                                           2 = bitmask-indexed memo (MEMO_MASK)      */
+                                           2 = bitmask-indexed memo (MEMO_MASK),
+                                           3 = shared-memory bitmask memo of the
+                                               single-CTA small-query kernel         */
     uint32_t inner_calls;          /* out, IDP2/UnionDP: inner exact DP calls          */
     double* level_ms;              /* optional [n+1]: device time of each level (fused
                                       kernel: %globaltimer at the level barriers; 0 on
@@ -163,6 +165,9 @@ typedef struct {
  * the bitmask-indexed one (MEMO_MASK, used for n <= 24 on one GPU by the
  * whole-query kernel); for ablations                                           */
 #define MPDP_FLAG_RANK_MEMO 512u
+/* flags: do not use the single-CTA shared-memory kernel for small queries
+ * (n <= 13); run them through the multi-CTA whole-query kernels (ablation)    */
+#define MPDP_FLAG_NO_SMALL 1024u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

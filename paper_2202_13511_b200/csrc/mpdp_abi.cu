@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "list_kernel.cuh"
+#include "small_kernel.cuh"
 #include "heuristics.h"
 
 using namespace mpdp;
@@ -131,6 +132,8 @@ struct mpdp_ctx {
     bool ran = false;
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
     int fused_occ[6] = {}, fused_n[6] = {};   // [CLS + 3 * mask_memo]
+    bool small_attr[3] = {};              // k_dp_small<CLS>: dynamic smem attribute set
+    bool small = false;                   // last query ran the single-CTA kernel
     bool fused = false;                  // last run used the fused kernel
     bool sharded = false;                // last run used the sharded (multi-GPU) path
     struct SubProblem {                  // MPDP_FLAG_RECORD_SUBPROBLEMS
@@ -614,6 +617,47 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     return MPDP_OK;
 }
 
+// ------------------------------------------------------------ small queries
+// One CTA with the memo in shared memory (small_kernel.cuh) when the query is
+// small enough that the multi-CTA kernels' per-level grid barriers and global
+// round trips dominate: tree queries with n <= 13.
+static bool small_eligible(const mpdp_ctx* c) {
+    const int n = c->n;
+    if (c->wide || c->world > 1 || n < 2 || n > kSmallMaxN || c->timeout_ms > 0) return false;
+    if (c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
+        return false;
+    // measured (B200): star-10 115 -> 54 us, snowflake-12 -> 74 us; cliques and
+    // general graphs gain nothing or lose (clique-9 59 vs 62 us, cycle-12 and
+    // random-12 several times slower: Find-Blocks and the pair counts need the
+    // whole GPU), so only tree queries take this path
+    return c->cls == CLS_TREE;
+}
+
+template <int CLS>
+static mpdp_status run_small(mpdp_ctx* c, const Params<uint32_t>& p) {
+    const size_t smem = small_smem_bytes(c->n);
+    if (!c->small_attr[CLS]) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_small<CLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)small_smem_bytes(kSmallMaxN)));
+        c->small_attr[CLS] = true;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    k_dp_small<CLS><<<1, kSmallBlock, smem, c->stream>>>(p);
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = 1;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->small = true;
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
+}
+
 // ------------------------------------------------------------ sharded run
 // Multi-GPU: per level k, rank r evaluates the colex ranks
 // [r*seg, (r+1)*seg) of the level (seg = ceil(C(n,k)/W)) with the fused kernel
@@ -756,12 +800,15 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
 template <typename M, int CLS, int MEMO>
 static mpdp_status run_query(mpdp_ctx* c) {
     c->sharded = false;
+    c->small = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (c->world > 1) return run_sharded<CLS>(c);
     }
     if (c->world > 1) return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
     c->fused = false;
+    c->small = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
+        if (small_eligible(c)) return run_small<CLS>(c, make_params<M>(c));
         if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
             return run_fused<CLS>(c, make_params<M>(c));
     }
@@ -1146,7 +1193,7 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     out->d2h_bytes = c->d2h_bytes;
     out->enum_launches = c->enum_launches;
     out->eval_launches = c->eval_launches;
-    out->memo_kind = c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
+    out->memo_kind = c->small ? 3u : c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
     out->enum_ms = out->eval_ms = 0;
     if (c->fused && c->nkev == 2) {      // the fused kernel: enumeration and evaluation together
         float t = 0;

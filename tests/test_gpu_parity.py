@@ -52,7 +52,7 @@ def check(r, o, g, exact=True):
     for a, b in zip(r.nodes, o.nodes):
         assert (a.left, a.right, a.relation, a.set) == (b.left, b.right, b.relation, b.set)
         assert a.cardinality == b.card and a.cost == b.cost
-    assert r.gpu_launches >= 2
+    assert r.gpu_launches >= 1
 
 
 SMALL = [(t, n, s) for t in ["star", "snowflake", "chain", "clique", "cycle", "random"]
@@ -218,7 +218,39 @@ def test_memo_layouts_agree(ctx, topo, n, seed):
         r2 = c.mpdp_optimize(g)
         assert r2.memo_kind == 1
         check(r2, o, g)
-    assert ctx.mpdp_optimize(W.star(12, seed)).memo_kind == 1     # trees keep the colex layout
+    assert ctx.mpdp_optimize(W.star(16, seed)).memo_kind == 1     # (n > 13) trees keep the colex layout
+
+
+@pytest.mark.parametrize("topo,n,seed", [("star", 2, 0), ("chain", 3, 1), ("star", 10, 0), ("snowflake", 13, 2),
+                                         ("chain", 13, 3), ("snowflake", 9, 4), ("star", 13, 10), ("chain", 2, 5)])
+def test_small_kernel_parity(ctx, topo, n, seed):
+    """Tree queries with n <= 13 run on the single-CTA shared-memory kernel
+    (memo_kind 3); the multi-CTA path (MPDP_FLAG_NO_SMALL) and the oracle agree."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate(topo, n, seed)
+    o = O.optimize(g)
+    r = ctx.mpdp_optimize(g)
+    assert r.memo_kind == 3, (g.name, r.memo_kind)
+    assert r.gpu_launches == 1
+    check(r, o, g)
+    with mpdp.Context(device=0, workspace_bytes=256 << 20, flags=mpdp.FLAG_NO_SMALL) as c:
+        r2 = c.mpdp_optimize(g)
+        assert r2.memo_kind != 3
+        check(r2, o, g)
+
+
+def test_small_kernel_leaf_costs_and_dpsub():
+    """Composite leaves (non-zero leaf costs) on the small kernel; the
+    DPSUB-enumeration ablation (general-graph kernels) agrees on the cost."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate("snowflake", 12, 3)
+    g.leaf_cost = [float(10 * (i % 4)) + 0.5 for i in range(g.n)]
+    with mpdp.Context(device=0, workspace_bytes=256 << 20) as c:
+        check(c.mpdp_optimize(g), O.optimize(g), g)
+    with mpdp.Context(device=0, workspace_bytes=256 << 20, flags=mpdp.FLAG_DPSUB_ENUM) as c:
+        r = c.mpdp_optimize(g)
+        o = O.optimize(g)
+        assert r.cost == o.cost
 
 
 def test_alternating_memo_kinds(ctx, hash_ctx):
@@ -252,11 +284,11 @@ def test_fused_and_per_level_kernels_agree(topo, n, seed):
     from paper_2202_13511_b200 import mpdp
     g = W.generate(topo, n, seed)
     o = O.optimize(g)
-    for flags in (0, mpdp.FLAG_NO_FUSED):
+    for flags in (mpdp.FLAG_NO_SMALL, mpdp.FLAG_NO_FUSED):
         with mpdp.Context(device=0, workspace_bytes=512 << 20, flags=flags) as c:
             r = c.mpdp_optimize(g)
             check(r, o, g)
-            if flags == 0:
+            if flags == mpdp.FLAG_NO_SMALL:
                 assert r.gpu_launches == 2          # k_init + the fused level loop
 
 
