@@ -542,17 +542,6 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 #endif
     for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
-        if constexpr (CLS == CLS_CLIQUE && MEMO == MEMO_MASK) {    // one phase and one barrier per level
-            unsigned long long pairs = 0, nccp = 0, nprobe = 0, nsets = 0;
-            clique_level(p, k, q, v, bin, pairs, nccp, nprobe, nsets);
-            if ((p.count_levels >> k) & 1ull) {
-                flush_counters(&p.desc[k], pairs, nccp, nprobe);
-                nsets = warp_sum(nsets);
-                if ((threadIdx.x & 31) == 0 && nsets) atomicAdd(&p.desc[k].n_light, nsets);
-            }
-            grid_sync(p.gbar, nbar, &p.result->error);
-            continue;
-        }
         TRACE(0);
 #ifdef MPDP_TRACE
         CT_NOW(ct_lvl0);
@@ -800,6 +789,47 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
         p.result->t_level[n + 1] = globaltimer_ns();
         extract_phase<M, MEMO>(p, q, v, rtab, gen);
+    }
+}
+
+// Whole-query kernel for cliques with the bitmask memo: clique_level per level
+// (one phase, one grid barrier), then the extraction.  A kernel of its own so
+// its register budget (and so its occupancy: kCliqueMinBlocks CTAs per SM) is
+// not set by the tile machinery of k_dp_fused.
+constexpr int kCliqueMinBlocks = 3;
+__host__ __device__ constexpr size_t clique_smem_bytes() { return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33; }
+
+__global__ void __launch_bounds__(kBlock, kCliqueMinBlocks) k_dp_clique(const __grid_constant__ Params<uint32_t> p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
+    unsigned int* bin = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));   // 33 x 33
+    __shared__ MemoView v;
+    load_query(q, p.q);
+    for (int j = threadIdx.x; j <= kMaxN; j += blockDim.x) {
+        v.off[j] = 0;
+        v.nb[j] = 0;
+    }
+    constexpr int NB = MaxN<uint32_t>::value + 1;
+    for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
+        const int a = i / 33, b = i % 33;
+        bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
+    }
+    unsigned int nbar = 0;
+    __syncthreads();
+    for (int k = p.k_begin; k <= p.k_end; k++) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+        unsigned long long pairs = 0, nccp = 0, nprobe = 0, nsets = 0;
+        clique_level(p, k, q, v, bin, pairs, nccp, nprobe, nsets);
+        if ((p.count_levels >> k) & 1ull) {
+            flush_counters(&p.desc[k], pairs, nccp, nprobe);
+            nsets = warp_sum(nsets);
+            if ((threadIdx.x & 31) == 0 && nsets) atomicAdd(&p.desc[k].n_light, nsets);
+        }
+        grid_sync(p.gbar, nbar, &p.result->error);
+    }
+    if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
+        p.result->t_level[p.n + 1] = globaltimer_ns();
+        extract_phase<uint32_t, MEMO_MASK>(p, q, v, bin, p.q->gen);
     }
 }
 

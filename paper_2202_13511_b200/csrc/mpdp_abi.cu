@@ -565,6 +565,8 @@ template <int CLS>
 static const void* level_loop_kernel(bool mask_memo = false) {
     if constexpr (CLS == CLS_TREE)
         return (const void*)k_dp_list<CLS>;
+    else if constexpr (CLS == CLS_CLIQUE)
+        return mask_memo ? (const void*)k_dp_clique : (const void*)k_dp_fused<CLS, MEMO_DENSE>;
     else
         return mask_memo ? (const void*)k_dp_fused<CLS, MEMO_MASK> : (const void*)k_dp_fused<CLS, MEMO_DENSE>;
 }
@@ -578,8 +580,8 @@ static size_t level_loop_smem(int n) {
 // and the extraction, then the D2H copy of the result.
 template <int CLS>
 static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
-    const size_t smem = level_loop_smem<CLS>(c->n);
     const bool mask = c->lay.mask_memo;
+    const size_t smem = (CLS == CLS_CLIQUE && mask) ? clique_smem_bytes() : level_loop_smem<CLS>(c->n);
     const void* kern = level_loop_kernel<CLS>(mask);
     const int slot = CLS + (mask ? 3 : 0);
     int& occ = c->fused_occ[slot];
