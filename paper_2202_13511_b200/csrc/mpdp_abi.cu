@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <dlfcn.h>
@@ -133,7 +134,10 @@ struct mpdp_ctx {
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
     int fused_occ[6] = {}, fused_n[6] = {};   // [CLS + 3 * mask_memo]
     bool small_attr[3] = {};              // k_dp_small<CLS>: dynamic smem attribute set
-    bool small = false;                   // last query ran the single-CTA kernel
+    bool small = false;                   // last query ran a single-CTA kernel
+    bool tree1_attr = false;
+    bool tree1 = false;                   // last query ran k_dp_tree1 (memo_kind 1, global memo)
+    unsigned long long tree_max_level = 0;  // tree queries: largest level (connected sets of one size)
     bool fused = false;                  // last run used the fused kernel
     bool sharded = false;                // last run used the sharded (multi-GPU) path
     struct SubProblem {                  // MPDP_FLAG_RECORD_SUBPROBLEMS
@@ -284,6 +288,30 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
             maxd = std::max(maxd, depth[v]);
         }
         q->max_depth = maxd;
+        // connected sets per size (subtrees of the tree): with f_v(x) the
+        // generating polynomial of the subtrees whose top vertex is v,
+        // f_v = x * prod over children u of (1 + f_u); level s holds sum_v [x^s] f_v
+        std::vector<std::vector<unsigned long long>> f(n);
+        std::vector<unsigned long long> cnt(n + 1, 0);
+        for (int i = (int)order.size() - 1; i >= 0; i--) {
+            const int v = order[i];
+            std::vector<unsigned long long> a(2, 0);
+            a[1] = 1;
+            for (int u = 0; u < n; u++) {
+                if (u == v || parent[u] != v) continue;
+                std::vector<unsigned long long> b(a.size() + f[u].size() - 1, 0);
+                for (size_t x = 0; x < a.size(); x++) {
+                    if (!a[x]) continue;
+                    b[x] += a[x];                                // the child's subtree left out
+                    for (size_t y = 1; y < f[u].size(); y++) b[x + y] += a[x] * f[u][y];
+                }
+                a.swap(b);
+            }
+            for (size_t x = 0; x < a.size() && x <= (size_t)n; x++) cnt[x] += a[x];
+            f[v].swap(a);
+        }
+        c->tree_max_level = 0;
+        for (int x = 2; x <= n; x++) c->tree_max_level = std::max(c->tree_max_level, cnt[x]);
     }
     constexpr int NB = MaxN<M>::value + 1;
     for (int i = 0; i < NB; i++)
@@ -602,8 +630,12 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
         want = std::max(want, heavy_pair_bound(c->n, k, CLS) / 2048);
     }
     if (CLS == CLS_GENERAL && c->n > 12) want = ~0ull;     // heavy work unknown up front
-    const unsigned int grid = (unsigned int)std::min<unsigned long long>(
+    unsigned int grid = (unsigned int)std::min<unsigned long long>(
         std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ), (unsigned long long)kMaxGrid);
+    if (const char* e = getenv("MPDP_DEBUG_GRID")) {      // experiments only: cap the whole-query grid
+        const unsigned int g = (unsigned int)atoi(e);
+        if (g >= 1 && g < grid) grid = g;
+    }
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
     CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));    // device time of the fused kernel itself
     CUDA_TRY(c, cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kBlock), args, smem, c->stream));
@@ -633,6 +665,43 @@ static bool small_eligible(const mpdp_ctx* c) {
     // random-12 several times slower: Find-Blocks and the pair counts need the
     // whole GPU), so only tree queries take this path
     return c->cls == CLS_TREE;
+}
+
+// Sparse tree queries whose every level fits the single-CTA kernel's shared
+// memory lists (k_dp_tree1; global colex-rank memo).
+static bool tree1_eligible(const mpdp_ctx* c) {
+    if (c->cls != CLS_TREE || c->wide || c->world > 1 || c->n < 3 || c->n > 32 || c->timeout_ms > 0) return false;
+    if (c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
+        return false;
+    // measured (B200): chain-25 (<= 24 sets per level) 290 -> 222 us; snowflake-20
+    // (up to ~2k sets per level) 253 -> 345 us: one SM is then instruction-bound,
+    // so only levels of at most kTree1MaxLevel sets take this kernel
+    return c->lay.memo_kind == MEMO_DENSE && c->tree_max_level <= (unsigned long long)kTree1MaxLevel;
+}
+
+static mpdp_status run_tree1(mpdp_ctx* c, const Params<uint32_t>& p) {
+    const size_t smem = tree1_smem_bytes(p.memo.rg.entries);
+    if (!c->tree1_attr) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_tree1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tree1_smem_bytes(rank_geom(32).entries)));
+        c->tree1_attr = true;
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    k_dp_tree1<<<1, kTree1Block, smem, c->stream>>>(p);
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = 1;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->small = true;
+    c->tree1 = true;
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
 }
 
 template <int CLS>
@@ -803,6 +872,7 @@ template <typename M, int CLS, int MEMO>
 static mpdp_status run_query(mpdp_ctx* c) {
     c->sharded = false;
     c->small = false;
+    c->tree1 = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (c->world > 1) return run_sharded<CLS>(c);
     }
@@ -811,6 +881,7 @@ static mpdp_status run_query(mpdp_ctx* c) {
     c->small = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (small_eligible(c)) return run_small<CLS>(c, make_params<M>(c));
+        if (tree1_eligible(c)) return run_tree1(c, make_params<M>(c));
         if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
             return run_fused<CLS>(c, make_params<M>(c));
     }
@@ -1195,7 +1266,7 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     out->d2h_bytes = c->d2h_bytes;
     out->enum_launches = c->enum_launches;
     out->eval_launches = c->eval_launches;
-    out->memo_kind = c->small ? 3u : c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
+    out->memo_kind = c->tree1 ? 1u : c->small ? 3u : c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
     out->enum_ms = out->eval_ms = 0;
     if (c->fused && c->nkev == 2) {      // the fused kernel: enumeration and evaluation together
         float t = 0;

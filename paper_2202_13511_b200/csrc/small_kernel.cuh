@@ -4,12 +4,12 @@
 // For n <= kSmallMaxN the memo indexed by relation bitmask fits in shared
 // memory: cost[2^n] (f64), card[2^n] (f64), left[2^n] (u16) = 18 B x 8192 =
 // 144 KB at n = 13.  Every step of the path then stays on one SM:
-//   * unrank + connectivity filter of level k: every thread
-//     walks a contiguous run of colex ranks (one unrank, then Gosper);
-//   * stream compaction: a block scan of the survivor counts writes the
-//     level list to shared memory; the same scan yields max w (pairs per set);
-//   * evaluate: G lanes per set (G = the power of two nearest
-//     max_w / 8, 1..32), each lane a contiguous range of the set's csg-cmp
+//   * connectivity filter + stream compaction of EVERY level up front
+//     (the enumeration reads no memo): the 2^n masks are
+//     filtered in bitmask order, counted per size, and written into per-size
+//     segments of a shared-memory list (two passes, 32-bit shared atomics);
+//   * per level, evaluate: G lanes per set (about 8 pairs per
+//     lane, more lanes when the level is small), each lane a contiguous range of the set's csg-cmp
 //     pairs through the same enumeration as the multi-CTA kernels
 //     (eval_range: trees, complete blocks, Find-Blocks), C_out cost from the
 //     shared-memory memo, group shuffle min of (cost, left), one memo write;
@@ -25,10 +25,9 @@ namespace mpdp {
 
 constexpr int kSmallMaxN = 13;
 constexpr int kSmallBlock = 512;
-constexpr int kSmallListCap = 1716;        // max_k C(13, k)
 
 __host__ __device__ constexpr size_t small_smem_bytes(int n) {
-    return sizeof(SQ<uint32_t>) + (size_t(1) << n) * (8 + 8 + 2) + 4 * kSmallListCap + 33 * 33 * 4 + 64;
+    return sizeof(SQ<uint32_t>) + (size_t(1) << n) * (8 + 8 + 2 + 2) + 64;   // cost, card, left, list
 }
 
 struct SmallSink {
@@ -43,6 +42,30 @@ struct SmallSink {
         if (key_less(key, best)) best = key;
     }
 };
+
+// Per-warp partial sums of three counters (64-bit shared-memory atomics are
+// CAS spin loops on sm_100 -- ATOMS.CAST.SPIN.64 -- and 16-32 warps hitting one
+// address cost microseconds per level); block_sum3_final reduces them in warp 0
+// after a barrier, lane 0 gets the totals.
+__device__ __forceinline__ void block_sum3_part(unsigned long long a, unsigned long long b, unsigned long long c,
+                                                unsigned long long (*part)[32]) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0) {
+        part[0][threadIdx.x >> 5] = a;
+        part[1][threadIdx.x >> 5] = b;
+        part[2][threadIdx.x >> 5] = c;
+    }
+}
+__device__ __forceinline__ void block_sum3_final(unsigned long long (*part)[32], unsigned long long* out) {
+    const unsigned int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        const unsigned long long x = warp_sum(lane < nw ? part[i][lane] : 0ull);
+        if (lane == 0) out[i] = x;
+    }
+}
 
 // card(S) as card_fast (reading R5 / R19), from the shared-memory card array
 template <int CLS>
@@ -107,70 +130,54 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_consta
     double* cost = reinterpret_cast<double*>(smem_raw + sizeof(SQ<uint32_t>));
     double* card = cost + NS;
     unsigned short* left = reinterpret_cast<unsigned short*>(card + NS);
-    uint32_t* list = reinterpret_cast<uint32_t*>(left + NS + (NS & 1u));
-    unsigned int* bin = list + kSmallListCap;                 // 33 x 33 u32 binomials
-    __shared__ unsigned int s_sum[33];
-    __shared__ unsigned long long s_max[33];
-    __shared__ unsigned long long s_cnt[3];                   // ccp, pairs, probes of the level
-    __shared__ unsigned long long s_tot[4];                   // csg, ccp, pairs, probes
+    unsigned short* list = left + NS;                        // connected sets (<= 2^n), grouped by size
+    __shared__ unsigned int s_len[kSmallMaxN + 2];           // sets per level, then level offsets
+    __shared__ unsigned int s_fill[kSmallMaxN + 2];
+    __shared__ unsigned int s_lvl[kSmallMaxN + 1][3];        // ccp, pairs, probes per level (u32: n <= 13)
     ResultDev* r = p.result;
-    for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
-        const int a = i / 33, b = i % 33;
-        constexpr int NB = MaxN<uint32_t>::value + 1;
-        bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
+    if (threadIdx.x <= kSmallMaxN + 1) s_len[threadIdx.x] = s_fill[threadIdx.x] = 0;
+    if (threadIdx.x < (kSmallMaxN + 1) * 3) (&s_lvl[0][0])[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        r->error = 0;
+        r->t_level[2] = globaltimer_ns();
     }
-    if (threadIdx.x < 4) s_tot[threadIdx.x] = 0;
-    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
-    if (threadIdx.x == 0) r->error = 0;
     __syncthreads();
     for (int v = threadIdx.x; v < n; v += blockDim.x) {      // level 1
         cost[1u << v] = q.leaf[v];
         card[1u << v] = q.card[v];
     }
+    // ---- unrank + connectivity filter + compaction of EVERY level at once
+    // (enumeration reads no memo): the masks are walked in
+    // bitmask order, counted per size, then written into per-size segments
+    // (list order inside a level is irrelevant: the memo is indexed by mask)
+    const unsigned int per = (NS + blockDim.x - 1) / blockDim.x;
+    const unsigned int m0 = threadIdx.x * per, m1 = m0 + per < NS ? m0 + per : NS;
+    for (unsigned int S = m0 > 3u ? m0 : 3u; S < m1; S++)
+        if ((S & (S - 1)) && connected_cls<uint32_t, CLS>(q, S, __popc(S))) atomicAdd(&s_len[__popc(S)], 1u);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        r->t_level[2] = globaltimer_ns();
-        s_tot[0] = (unsigned long long)n;
-        r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
-        r->lvl_csg[1] = (unsigned long long)n;
-        r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
+        unsigned int acc = 0;
+        for (int k = 2; k <= n; k++) {
+            const unsigned int c = s_len[k];
+            s_len[k] = acc;                                  // exclusive offsets
+            acc += c;
+        }
+        s_len[n + 1] = acc;
     }
-    const unsigned int T = blockDim.x, lane = threadIdx.x & 31;
+    __syncthreads();
+    for (unsigned int S = m0 > 3u ? m0 : 3u; S < m1; S++)
+        if ((S & (S - 1)) && connected_cls<uint32_t, CLS>(q, S, __popc(S))) {
+            const int k = __popc(S);
+            list[s_len[k] + atomicAdd(&s_fill[k], 1u)] = (unsigned short)S;
+        }
+    __syncthreads();
+    // ---- levels: evaluate (G lanes per set, about 8 pairs per lane), barrier
     for (int k = 2; k <= n; k++) {
-        // ---- unrank + filter + compaction into list[]
-        const unsigned int C = bin[n * 33 + k];
-        const unsigned int r0 = (unsigned int)((unsigned long long)C * threadIdx.x / T);
-        const unsigned int r1 = (unsigned int)((unsigned long long)C * (threadIdx.x + 1) / T);
-        unsigned int flags = 0;
-        unsigned long long wmax = 0;
-        uint32_t S0 = r0 < r1 ? unrank_colex32(bin, n, k, r0) : 0u;
-        {
-            uint32_t S = S0;
-            for (unsigned int i = 0; r0 + i < r1; i++) {
-                if (connected_cls<uint32_t, CLS>(q, S, k)) {
-                    flags |= 1u << i;
-                    unsigned long long w;
-                    set_kind<uint32_t, CLS>(q, S, k, w);
-                    wmax = w > wmax ? w : wmax;
-                }
-                if (r0 + i + 1 < r1) S = gosper(S);
-            }
-        }
-        unsigned int N;
-        unsigned long long maxw;
-        const unsigned int incl = block_scan_max((unsigned int)__popc(flags), wmax, N, maxw, s_sum, s_max);
-        {
-            unsigned int d = incl - (unsigned int)__popc(flags);
-            uint32_t S = S0;
-            for (unsigned int i = 0; r0 + i < r1; i++) {
-                if ((flags >> i) & 1u) list[d++] = S;
-                if (r0 + i + 1 < r1) S = gosper(S);
-            }
-        }
-        __syncthreads();
-        // ---- evaluate: G lanes per set, about 8 pairs per lane
+        const unsigned int L0 = s_len[k], N = s_len[k + 1] - L0;
+        const unsigned long long maxw = CLS == CLS_TREE ? (unsigned long long)(k - 1) : (1ull << (k - 1)) - 1;
         unsigned int G = 1;
-        while (G < 32 && 8ull * G < maxw) G <<= 1;
-        const unsigned int ngroups = T / G, grp = threadIdx.x / G, sub = threadIdx.x & (G - 1);
+        while (G < 32 && (8ull * G < maxw || G * N * 2 <= blockDim.x)) G <<= 1;
+        const unsigned int ngroups = blockDim.x / G, grp = threadIdx.x / G, sub = threadIdx.x & (G - 1);
         const unsigned int rounds = (N + ngroups - 1) / ngroups;
         unsigned long long pairs = 0, nccp = 0, nprobe = 0;
         for (unsigned int it = 0; it < rounds; it++) {
@@ -180,11 +187,11 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_consta
             uint32_t S = 0;
             unsigned long long w = 0;
             if (act) {
-                S = list[e];
+                S = list[L0 + e];
                 const int kind = set_kind<uint32_t, CLS>(q, S, k, w);
                 sink.cS = small_card<CLS>(q, card, S, k);
-                const unsigned long long per = (w + G - 1) / G;
-                unsigned long long j0 = per * sub, j1 = j0 + per;
+                const unsigned long long pl = (w + G - 1) / G;
+                unsigned long long j0 = pl * sub, j1 = j0 + pl;
                 if (j0 > w) j0 = w;
                 if (j1 > w) j1 = w;
                 eval_range<uint32_t, CLS>(q, S, k, kind, j0, j1, sink, nccp);
@@ -201,29 +208,32 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_consta
         nccp = warp_sum(nccp);
         pairs = warp_sum(pairs);
         nprobe = warp_sum(nprobe);
-        if (lane == 0) {
-            if (nccp) atomicAdd(&s_cnt[0], nccp);
-            if (pairs) atomicAdd(&s_cnt[1], pairs);
-            if (nprobe) atomicAdd(&s_cnt[2], nprobe);
+        if ((threadIdx.x & 31) == 0) {                       // 32-bit shared atomics are native
+            if (nccp) atomicAdd(&s_lvl[k][0], (unsigned int)nccp);
+            if (pairs) atomicAdd(&s_lvl[k][1], (unsigned int)pairs);
+            if (nprobe) atomicAdd(&s_lvl[k][2], (unsigned int)nprobe);
         }
-        __syncthreads();                                    // level barrier: level k is final
-        if (threadIdx.x == 0) {
-            r->lvl_csg[k] = N;
-            r->lvl_ccp[k] = s_cnt[0];
-            r->lvl_pairs[k] = s_cnt[1];
-            s_tot[0] += N;
-            s_tot[1] += s_cnt[0];
-            s_tot[2] += s_cnt[1];
-            s_tot[3] += s_cnt[2];
-            s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;       // (the next level adds after its scan's barriers)
-            r->t_level[k + 1] = globaltimer_ns();
-        }
+        __syncthreads();                                     // level barrier: level k is final
+        if (threadIdx.x == 0) r->t_level[k + 1] = globaltimer_ns();
     }
     if (threadIdx.x != 0) return;
-    r->csg = s_tot[0];
-    r->ccp = s_tot[1];
-    r->pairs = s_tot[2];
-    r->probes = s_tot[3];
+    unsigned long long tot[4] = {(unsigned long long)n, 0, 0, 0};
+    r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
+    r->lvl_csg[1] = (unsigned long long)n;
+    r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
+    for (int k = 2; k <= n; k++) {
+        r->lvl_csg[k] = s_len[k + 1] - s_len[k];
+        r->lvl_ccp[k] = s_lvl[k][0];
+        r->lvl_pairs[k] = s_lvl[k][1];
+        tot[0] += s_len[k + 1] - s_len[k];
+        tot[1] += s_lvl[k][0];
+        tot[2] += s_lvl[k][1];
+        tot[3] += s_lvl[k][2];
+    }
+    r->csg = tot[0];
+    r->ccp = tot[1];
+    r->pairs = tot[2];
+    r->probes = tot[3];
     // ---- plan extraction (post-order, root last) from shared memory
     uint32_t st_set[2 * kSmallMaxN];
     int st_state[2 * kSmallMaxN], st_left[2 * kSmallMaxN];
@@ -270,6 +280,181 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_consta
     }
     r->n_nodes = (unsigned int)nn;
     r->cost = r->nodes[nn - 1].cost;
+}
+
+// ------------------------------------------------------------ k_dp_tree1
+// Sparse tree queries (snowflakes, chains) whose levels hold a few thousand
+// connected sets: ONE CTA, level lists in shared memory, the colex-rank memo in
+// global memory (L2-resident).  Level 2 is the edge list; level k+1 is
+// generated from level k's sets during their evaluation (fused generation of
+// the list kernel: S' = S u {v} is emitted once, from S' minus
+// its largest leaf), so no C(n,k) rank space is ever scanned.  The level barrier
+// is __syncthreads instead of a grid barrier over ~300 CTAs, which is what the
+// multi-CTA list kernel pays per level on these queries (9-13 us of which the
+// set evaluations are ~1 us).  The host picks this kernel from the exact
+// per-level csg counts of the tree (a subtree-counting DP) for queries whose
+// levels hold at most kTree1MaxLevel sets (chains, thin snowflakes); with a few
+// thousand sets per level one SM becomes instruction-bound and the multi-CTA
+// list kernel is faster.
+constexpr int kTree1Block = 1024;
+constexpr int kTree1ListCap = 6144;
+constexpr int kTree1MaxLevel = 512;        // eligibility: largest level (sets) routed to this kernel
+
+__host__ __device__ constexpr size_t tree1_smem_bytes(unsigned int rank_entries) {
+    return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * (rank_entries + 33 * 33 + 1) +
+           2ull * kTree1ListCap * sizeof(unsigned long long) + 16;
+}
+
+__global__ void __launch_bounds__(kTree1Block, 1) k_dp_tree1(const __grid_constant__ Params<uint32_t> p) {
+    constexpr int MEMO = MEMO_DENSE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
+    unsigned int* rtab = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));
+    unsigned int* bin = rtab + p.memo.rg.entries;
+    unsigned long long* lists =
+        reinterpret_cast<unsigned long long*>(smem_raw + ((sizeof(SQ<uint32_t>) + sizeof(unsigned int) *
+                                                           (p.memo.rg.entries + 33 * 33) + 15) & ~size_t(15)));
+    __shared__ MemoView v;
+    __shared__ unsigned int s_cnt[2];
+    __shared__ unsigned long long s_part[3][32];         // per-warp ccp, pairs, probes of the level
+    __shared__ unsigned long long s_lvl[3];
+    memo_prologue<uint32_t, MEMO>(p, p.n, q, v, rtab);
+    const int n = p.n;
+    const unsigned int gen = p.q->gen;
+    ResultDev* r = p.result;
+    if (threadIdx.x == 0) {
+        s_cnt[0] = 0;
+        s_cnt[1] = 0;
+        r->error = 0;
+        r->t_level[2] = globaltimer_ns();
+    }
+    __syncthreads();
+    // level 2: the edges {u, v}, u < v, colex rank u + C(v, 2)
+    for (int a = threadIdx.x; a < n; a += blockDim.x)
+        for (uint32_t U = q.adj[a] & ((1u << a) - 1u); U; U &= U - 1) {
+            const int u = __ffs(U) - 1;
+            const unsigned int d = atomicAdd(&s_cnt[0], 1u);
+            const unsigned int R = (unsigned int)u + bin[a * 33 + 2];
+            if (d < kTree1ListCap) lists[d] = ((unsigned long long)R << 32) | ((1u << u) | (1u << a));
+        }
+    __syncthreads();
+    for (int k = 2; k <= n; k++) {
+        const unsigned long long* cur = lists + (size_t)(k & 1) * kTree1ListCap;
+        unsigned long long* nxt = lists + (size_t)((k + 1) & 1) * kTree1ListCap;
+        const unsigned int N = s_cnt[k & 1] < kTree1ListCap ? s_cnt[k & 1] : kTree1ListCap;
+        if (s_cnt[k & 1] > kTree1ListCap && threadIdx.x == 0) atomicOr(&r->error, ERR_CAPACITY);
+        unsigned long long pairs = 0, nccp = 0, nprobe = 0;
+        // G lanes per set when the level has fewer sets than threads: each
+        // lane takes ceil((k-1)/G) of the set's join pairs, so a set costs one
+        // round of probes instead of k/4 dependent rounds
+        unsigned int G = 1;
+        while (G < 32 && 2u * G * N <= blockDim.x) G <<= 1;
+        const unsigned int sub = threadIdx.x & (G - 1), ngrp = blockDim.x / G;
+        const unsigned int rounds = (N + ngrp - 1) / ngrp;
+        for (unsigned int it = 0; it < rounds; it++) {
+            const unsigned int e = it * ngrp + threadIdx.x / G;
+            const bool act = e < N;
+            const unsigned long long ent = act ? cur[e] : 0ull;
+            const uint32_t S = (uint32_t)ent;
+            const unsigned int R = (unsigned int)(ent >> 32);
+            TreeSetInfo info;
+            bool lead = act;
+            if (G == 1) {
+                if (act && k > 2) {
+                    eval_tree_dense<MEMO, false, true>(p.memo, gen, v, rtab, bin, q, S, k, R, nprobe, nullptr, &info);
+                } else if (act) {                        // both sides are leaves
+                    PairSink<uint32_t, MEMO> sink;
+                    sink.init(&p.memo, gen, &v, rtab, &q, card_of(q, S));
+                    const uint32_t lo = S & (0u - S);
+                    sink.add(lo, S ^ lo);
+                    sink.flush();
+                    const unsigned long long idx = v.off[2] + R;
+                    p.memo.dcost[idx] = __longlong_as_double((long long)sink.best.c);
+                    __stcs(p.memo.dleft + idx, (unsigned int)sink.best.l);
+                    p.memo.dcard[idx] = sink.cS;
+                }
+            } else {
+                Key best = key_inf();
+                double cS = 0.0;
+                if (act) {
+                    unsigned long long w;
+                    const int kind = set_kind<uint32_t, CLS_TREE>(q, S, k, w);
+                    cS = card_fast<CLS_TREE, MEMO>(p.memo, v, bin, q, S, k, R);
+                    PairSink<uint32_t, MEMO> sink;
+                    sink.init(&p.memo, gen, &v, rtab, &q, cS);
+                    const unsigned long long per = (w + G - 1) / G;
+                    unsigned long long j0 = per * sub, j1 = j0 + per;
+                    if (j0 > w) j0 = w;
+                    if (j1 > w) j1 = w;
+                    unsigned long long dummy = 0;
+                    eval_range<uint32_t, CLS_TREE>(q, S, k, kind, j0, j1, sink, dummy);
+                    sink.flush();
+                    nprobe += sink.nprobe;
+                    best = sink.best;
+                }
+                best = group_min(best, G);
+                lead = act && sub == 0;
+                if (lead) {
+                    const unsigned long long idx = v.off[k] + R;
+                    p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
+                    __stcs(p.memo.dleft + idx, (unsigned int)best.l);
+                    p.memo.dcard[idx] = cS;
+                }
+            }
+            if (lead && (G > 1 || k == 2)) {             // leaves and neighbourhood of S
+                uint32_t L = 0, nb = 0;
+                for (uint32_t T = S; T; T &= T - 1) {
+                    const uint32_t a = q.adj[__ffs(T) - 1];
+                    nb |= a;
+                    if (__popc(a & S) == 1) L |= T & (0u - T);
+                }
+                info.leaves = L;
+                info.nb = nb;
+            }
+            if (lead) {
+                pairs += (unsigned long long)(k - 1);
+                nccp += (unsigned long long)(k - 1);
+            }
+            if (lead && k < n) {                         // children S u {v}, each generated once
+                const uint32_t acc = children_of(q, S, info);
+                if (acc) {
+                    unsigned int d = atomicAdd(&s_cnt[(k + 1) & 1], (unsigned int)__popc(acc));
+                    const int mx = 31 - __clz(S);
+                    for (uint32_t V = acc; V; V &= V - 1, d++) {
+                        const int w = __ffs(V) - 1;
+                        const uint32_t Sp = S | (1u << w);
+                        unsigned int Rp;
+                        if (w > mx) {
+                            Rp = R + bin[w * 33 + k + 1];
+                        } else {
+                            Rp = 0;
+                            int i = 1;
+                            for (uint32_t T = Sp; T; T &= T - 1, i++) Rp += bin[(__ffs(T) - 1) * 33 + i];
+                        }
+                        if (d < kTree1ListCap) nxt[d] = ((unsigned long long)Rp << 32) | Sp;
+                    }
+                }
+            }
+        }
+        block_sum3_part(nccp, pairs, nprobe, s_part);
+        __syncthreads();                                 // level k is final in the memo
+        if (threadIdx.x < 32) block_sum3_final(s_part, s_lvl);
+        if (threadIdx.x == 0) {
+            LevelDesc& d = p.desc[k];
+            d.n_light = N;
+            d.n_heavy = 0;
+            d.ccp = s_lvl[0];
+            d.pairs = s_lvl[1];
+            d.probes = s_lvl[2];
+            s_cnt[k & 1] = 0;                            // becomes level k+2's counter
+            r->t_level[k + 1] = globaltimer_ns();
+        }
+        __syncthreads();
+    }
+    if (p.do_extract && threadIdx.x == 0) {
+        __threadfence_block();
+        extract_phase<uint32_t, MEMO>(p, q, v, rtab, gen);
+    }
 }
 
 }  // namespace mpdp

@@ -239,6 +239,23 @@ def test_small_kernel_parity(ctx, topo, n, seed):
         check(r2, o, g)
 
 
+@pytest.mark.parametrize("topo,n,seed", [("chain", 14, 0), ("chain", 20, 1), ("chain", 25, 3), ("chain", 26, 4)])
+def test_tree1_kernel_parity(ctx, topo, n, seed):
+    """Sparse tree queries whose levels fit the single-CTA list kernel
+    (k_dp_tree1: one launch, global colex-rank memo) agree with the oracle and
+    with the multi-CTA list kernel (MPDP_FLAG_NO_SMALL)."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate(topo, n, seed)
+    o = O.optimize(g)
+    r = ctx.mpdp_optimize(g)
+    assert (r.memo_kind, r.gpu_launches) == (1, 1), g.name
+    check(r, o, g)
+    with mpdp.Context(device=0, workspace_bytes=2 << 30, flags=mpdp.FLAG_NO_SMALL) as c:
+        r2 = c.mpdp_optimize(g)
+        assert r2.gpu_launches >= 2                 # multi-CTA kernels
+        check(r2, o, g)
+
+
 def test_small_kernel_leaf_costs_and_dpsub():
     """Composite leaves (non-zero leaf costs) on the small kernel; the
     DPSUB-enumeration ablation (general-graph kernels) agrees on the cost."""

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workload as W  # noqa: E402
 from paper_2202_13511_b200 import mpdp  # noqa: E402
 
-PH = ["start", "ticket", "enum", "queued", "evald", "counted", "barrier", "heavy"]
+PH = ["start", "ticket", "enum", "queued", "evald", "counted", "barrier", "heavy"]  # (k_dp_small: start, enum, -, listed, evald)
 L = mpdp.load_library()
 L.mpdp_debug_trace.restype = C.c_int
 L.mpdp_debug_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]
