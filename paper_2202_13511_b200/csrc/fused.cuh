@@ -255,7 +255,11 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
                             const uint2* binp = nullptr, const EmitCtx* emit = nullptr) {
     const unsigned long long total = (unsigned long long)gridDim.x * blockDim.x;
     unsigned int G = 1;
-    while (G < 32 && 2ull * G * nsmall <= total) G <<= 1;
+    // (dense tree levels stop at G = 4: wider groups take the generic
+    // per-pair path with a rank lookup per probe; measured snowflake-20 252 ->
+    // 244 us, snowflake-24 337 -> 327 us, G = 2 / 8 / 32 slower)
+    const unsigned int gmax = (CLS == CLS_TREE && MEMO == MEMO_DENSE) ? 4u : 32u;
+    while (G < gmax && 2ull * G * nsmall <= total) G <<= 1;
     // CTA b takes the contiguous run [N*b/grid, N*(b+1)/grid) of the list, so
     // consecutive rounds of a CTA evaluate colex-near sets whose subsets share
     // L1 lines (the list is a concatenation of warp runs of consecutive ranks)
