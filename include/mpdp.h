@@ -168,6 +168,10 @@ typedef struct {
 /* flags: do not use the single-CTA shared-memory kernel for small queries
  * (n <= 13); run them through the multi-CTA whole-query kernels (ablation)    */
 #define MPDP_FLAG_NO_SMALL 1024u
+/* flags: no Collaborative Context Collection in the heavy phase of
+ * block-decomposed sets (general graphs): lanes walk contiguous candidate
+ * chunks and evaluate their valid pairs in place (ablation)                   */
+#define MPDP_FLAG_NO_CCC 2048u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

@@ -515,6 +515,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.epoch_salt = shard;
     p.n = c->n;
     p.inv_load = 1.0 / c->load_factor;
+    p.no_ccc = (c->flags & MPDP_FLAG_NO_CCC) ? 1 : 0;
     return p;
 }
 

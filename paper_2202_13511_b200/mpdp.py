@@ -68,6 +68,7 @@ FLAG_RECORD_SUBPROBLEMS = 128
 FLAG_DPSUB_ENUM = 256
 FLAG_RANK_MEMO = 512
 FLAG_NO_SMALL = 1024
+FLAG_NO_CCC = 2048
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",

@@ -256,6 +256,18 @@ def test_tree1_kernel_parity(ctx, topo, n, seed):
         check(r2, o, g)
 
 
+@pytest.mark.parametrize("topo,n,seed", [("random", 14, 0), ("random", 16, 1), ("cycle", 17, 2)])
+def test_ccc_ablation_parity(ctx, topo, n, seed):
+    """Collaborative Context Collection (default) and lane-contiguous candidate
+    chunks (MPDP_FLAG_NO_CCC) give the oracle's results on general graphs."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.generate(topo, n, seed)
+    o = O.optimize(g)
+    check(ctx.mpdp_optimize(g), o, g)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_NO_CCC) as c:
+        check(c.mpdp_optimize(g), o, g)
+
+
 def test_small_kernel_leaf_costs_and_dpsub():
     """Composite leaves (non-zero leaf costs) on the small kernel; the
     DPSUB-enumeration ablation (general-graph kernels) agrees on the cost."""
