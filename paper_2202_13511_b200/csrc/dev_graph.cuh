@@ -177,7 +177,20 @@ __device__ int find_blocks(const SQ<M>& q, M S, M* blk) {
     return nb;
 }
 
-enum SetKind : int { KIND_TREE = 0, KIND_COMPLETE = 1, KIND_BLOCKS = 2 };
+enum SetKind : int { KIND_TREE = 0, KIND_COMPLETE = 1, KIND_BLOCKS = 2, KIND_ONEBLOCK = 3 };
+
+// G[S] (connected, |S| >= 3) is biconnected -- Find-Blocks would return the one
+// block S -- iff no vertex has induced degree < 2 and no S \ {v} is
+// disconnected (register BFS per vertex; cheaper than the Hopcroft-Tarjan DFS
+// with its local-memory stacks, and the common case on dense random graphs)
+template <typename M>
+__device__ __forceinline__ bool biconnected(const SQ<M>& q, M S) {
+    for (M T = S; T; T &= T - 1)
+        if (popc(q.adj[ctz(T)] & S) < 2) return false;
+    for (M T = S; T; T &= T - 1)
+        if (!connected(q, S & ~lowbit(T))) return false;
+    return true;
+}
 
 // Kind and MPDP join-pair count (reading R3) of one connected set of size k:
 // tree-induced sets have one pair per edge (Alg. mpdp_trees);
@@ -205,6 +218,10 @@ __device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned lon
     if (e2 == k * (k - 1)) {
         w = (1ull << (k - 1)) - 1;
         return KIND_COMPLETE;
+    }
+    if (biconnected(q, S)) {               // one (non-complete) block: S
+        w = (1ull << (k - 1)) - 1;
+        return KIND_ONEBLOCK;
     }
     M blk[MaxN<M>::value];
     const int nb = find_blocks(q, S, blk);

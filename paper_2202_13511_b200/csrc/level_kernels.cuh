@@ -483,10 +483,10 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
         return;
     }
     if (CLS != CLS_GENERAL) return;        // cliques are one complete block
-    // KIND_BLOCKS
+    // KIND_BLOCKS / KIND_ONEBLOCK
     M blk[MaxN<M>::value];
     int nb;
-    if (q.dpsub) {                         // ablation: the whole set is the only "block"
+    if (q.dpsub || kind == KIND_ONEBLOCK) {   // the whole set is the only block (dpsub: ablation)
         blk[0] = S;
         nb = 1;
     } else {
@@ -775,12 +775,12 @@ __global__ void __launch_bounds__(kLightBlock, kLightMinBlocks) k_eval_light(con
 // full warp instead of with the lanes whose candidate passed (35% on random-20).
 constexpr int kCccStash = 64;
 template <typename M, typename Sink>
-__device__ __forceinline__ void eval_blocks_ccc(const SQ<M>& q, M S, unsigned long long a, unsigned long long b,
-                                                Sink& sink, unsigned long long& nccp, M* stash) {
+__device__ __forceinline__ void eval_blocks_ccc(const SQ<M>& q, M S, int kind, unsigned long long a,
+                                                unsigned long long b, Sink& sink, unsigned long long& nccp, M* stash) {
     const unsigned int lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
     M blk[MaxN<M>::value];
     int nb;
-    if (q.dpsub) {
+    if (q.dpsub || kind == KIND_ONEBLOCK) {
         blk[0] = S;
         nb = 1;
     } else {
@@ -878,8 +878,8 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                     sub = ((sub | ~R) + D) & R;
                     nccp++;
                 }
-            } else if (CLS == CLS_GENERAL && kind == KIND_BLOCKS && !p.no_ccc) {
-                eval_blocks_ccc<M>(q, S, a, b, sink, nccp, s_ccc[threadIdx.x >> 5]);
+            } else if (CLS == CLS_GENERAL && kind >= KIND_BLOCKS && !p.no_ccc) {
+                eval_blocks_ccc<M>(q, S, kind, a, b, sink, nccp, s_ccc[threadIdx.x >> 5]);
             } else {                               // lane-contiguous chunks of [a, b)
                 const unsigned long long per = (cnt + 31) >> 5;
                 unsigned long long j0 = a + per * lane, j1 = j0 + per;
