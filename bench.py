@@ -278,12 +278,16 @@ def run_ours(args):
     # 8 B cost + 4 B left insert; open-addressing memo = 16 B slot per probe,
     # per set list write + read + 16 B slot + left.
     msz = 4 if n <= 32 else 8
-    if memo_kind in (1, 2, 3):                # colex-rank or bitmask-indexed arrays: same bytes
+    if memo_kind == 4:                        # star: no level lists; card(S \ max) read + cost/card/left write
+        alg_bytes = 8 * probes_total + sets_total * (8 + 8 + 8 + 4)
+    elif memo_kind in (1, 2, 3):              # colex-rank or bitmask-indexed arrays: same bytes
         alg_bytes = 8 * probes_total + sets_total * (16 + 8 + 4)
     else:
         alg_bytes = 16 * probes_total + sets_total * (2 * msz + 16 + msz)
-    kernel_name = ("k_dp_list (tree queries: whole level loop, one launch per query)" if topo_is_tree
-                   else "k_dp_fused (whole level loop, one launch per query)")
+    kernel_name = {4: "k_dp_star (star queries: closed-form level indexing, one launch per query)",
+                   3: "k_dp_small (single CTA, shared-memory memo)"}.get(memo_kind) or (
+        "k_dp_list (tree queries: whole level loop, one launch per query)" if topo_is_tree
+        else "k_dp_fused / k_dp_clique (whole level loop, one launch per query)")
     peak, peak_kind = measured_peaks()
     kern_s = kernel_ms / 1e3
     achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
@@ -298,7 +302,8 @@ def run_ours(args):
             "traffic_source": traffic.get("source") if traffic else None,
             "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
             "memo": {1: "perfect-hash (colex rank)", 2: "bitmask-indexed (MEMO_MASK)",
-                     3: "shared-memory bitmask memo (single CTA)"}.get(
+                     3: "shared-memory bitmask memo (single CTA)",
+                     4: "star memo (leaf-set colex rank, C(n-1,k-1) per level)"}.get(
                 memo_kind, "murmur3 open addressing"),
             "algorithmic_bytes_per_launch": alg_bytes / max(1, kernel_launches),
             "avg_launch_ms": kernel_ms / max(1, kernel_launches),

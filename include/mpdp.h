@@ -106,7 +106,9 @@ typedef struct {
                                            0 = Murmur3 open-addressing memo,
                                            2 = bitmask-indexed memo (MEMO_MASK),
                                            3 = shared-memory bitmask memo of the
-                                               single-CTA small-query kernel         */
+                                               single-CTA small-query kernel,
+                                           4 = star memo (k_dp_star: C(n-1,k-1)
+                                               entries per level, leaf-set rank) */
     uint32_t inner_calls;          /* out, IDP2/UnionDP: inner exact DP calls          */
     double* level_ms;              /* optional [n+1]: device time of each level (fused
                                       kernel: %globaltimer at the level barriers; 0 on
@@ -172,6 +174,9 @@ typedef struct {
  * block-decomposed sets (general graphs): lanes walk contiguous candidate
  * chunks and evaluate their valid pairs in place (ablation)                   */
 #define MPDP_FLAG_NO_CCC 2048u
+/* flags: run star queries (one relation adjacent to all others, n >= 14)
+ * through the general tree kernel instead of k_dp_star (ablation)              */
+#define MPDP_FLAG_NO_STAR 4096u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

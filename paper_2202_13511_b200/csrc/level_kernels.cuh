@@ -80,6 +80,8 @@ template <typename M> struct Params {
     int memo_kind;                         // MEMO_HASH / MEMO_DENSE / MEMO_MASK
     double inv_load;                       // HASH: buckets = ceil(count * inv_load / 2)
     int no_ccc;                            // MPDP_FLAG_NO_CCC: lane-contiguous candidates (ablation)
+    int star_hub;                          // k_dp_star: the hub relation
+    unsigned long long star_off[kMaxN + 1];   // k_dp_star: first memo entry of level k (C(n-1, k-1) per level)
 };
 
 // ------------------------------------------------------------- mem helpers

@@ -21,6 +21,7 @@
 
 #include "list_kernel.cuh"
 #include "small_kernel.cuh"
+#include "star_kernel.cuh"
 #include "heuristics.h"
 
 using namespace mpdp;
@@ -137,6 +138,9 @@ struct mpdp_ctx {
     bool small = false;                   // last query ran a single-CTA kernel
     bool tree1_attr = false;
     bool tree1 = false;                   // last query ran k_dp_tree1 (memo_kind 1, global memo)
+    int star_hub = -1;                    // star queries: the relation adjacent to all others
+    int star_occ = 0;                     // k_dp_star CTAs per SM
+    bool star = false;                    // last query ran k_dp_star (memo_kind 4)
     unsigned long long tree_max_level = 0;  // tree queries: largest level (connected sets of one size)
     bool fused = false;                  // last run used the fused kernel
     bool sharded = false;                // last run used the sharded (multi-GPU) path
@@ -312,6 +316,9 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
         }
         c->tree_max_level = 0;
         for (int x = 2; x <= n; x++) c->tree_max_level = std::max(c->tree_max_level, cnt[x]);
+        c->star_hub = -1;
+        for (int v = 0; v < n && n >= 3; v++)
+            if (__builtin_popcountll(adj[v]) == n - 1) c->star_hub = v;
     }
     constexpr int NB = MaxN<M>::value + 1;
     for (int i = 0; i < NB; i++)
@@ -516,6 +523,14 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.n = c->n;
     p.inv_load = 1.0 / c->load_factor;
     p.no_ccc = (c->flags & MPDP_FLAG_NO_CCC) ? 1 : 0;
+    p.star_hub = c->star_hub;
+    {
+        unsigned long long so = 0;
+        for (int k = 0; k <= kMaxN; k++) {
+            p.star_off[k] = so;
+            if (k >= 2 && k <= c->n) so += binom_u64(c->n - 1, k - 1);
+        }
+    }
     return p;
 }
 
@@ -705,6 +720,46 @@ static mpdp_status run_tree1(mpdp_ctx* c, const Params<uint32_t>& p) {
     return MPDP_OK;
 }
 
+// Star queries on one GPU (k_dp_star): closed-form set indexing, memo of
+// C(n-1, k-1) entries per level inside the dense region.
+static bool star_eligible(const mpdp_ctx* c) {
+    if (c->cls != CLS_TREE || c->star_hub < 0 || c->wide || c->world > 1 || c->n < 3 || c->n > 32 ||
+        c->timeout_ms > 0)
+        return false;
+    if (c->flags & (MPDP_FLAG_NO_STAR | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
+        return false;
+    return c->lay.memo_kind == MEMO_DENSE;
+}
+
+static mpdp_status run_star(mpdp_ctx* c, const Params<uint32_t>& p) {
+    const size_t smem = star_smem_bytes();
+    if (!c->star_occ) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_star, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->star_occ, k_dp_star, kBlock, smem));
+        if (c->star_occ < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
+    }
+    unsigned long long want = 1;
+    for (int k = 2; k <= c->n; k++) want = std::max(want, (binom_u64(c->n - 1, k - 1) + 255) / 256);
+    const unsigned int grid = (unsigned int)std::min<unsigned long long>(
+        std::min<unsigned long long>(want, (unsigned long long)c->num_sms * c->star_occ), (unsigned long long)kMaxGrid);
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    k_init<uint32_t><<<1, 64, 0, c->stream>>>(p);
+    void* args[] = {const_cast<Params<uint32_t>*>(&p)};
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_star, dim3(grid), dim3(kBlock), args, smem, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = 2;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->star = true;
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
+}
+
 template <int CLS>
 static mpdp_status run_small(mpdp_ctx* c, const Params<uint32_t>& p) {
     const size_t smem = small_smem_bytes(c->n);
@@ -874,6 +929,7 @@ static mpdp_status run_query(mpdp_ctx* c) {
     c->sharded = false;
     c->small = false;
     c->tree1 = false;
+    c->star = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (c->world > 1) return run_sharded<CLS>(c);
     }
@@ -883,6 +939,7 @@ static mpdp_status run_query(mpdp_ctx* c) {
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (small_eligible(c)) return run_small<CLS>(c, make_params<M>(c));
         if (tree1_eligible(c)) return run_tree1(c, make_params<M>(c));
+        if (star_eligible(c)) return run_star(c, make_params<M>(c));
         if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
             return run_fused<CLS>(c, make_params<M>(c));
     }
@@ -1267,7 +1324,7 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     out->d2h_bytes = c->d2h_bytes;
     out->enum_launches = c->enum_launches;
     out->eval_launches = c->eval_launches;
-    out->memo_kind = c->tree1 ? 1u : c->small ? 3u : c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
+    out->memo_kind = c->star ? 4u : c->tree1 ? 1u : c->small ? 3u : c->lay.mask_memo && c->fused ? 2u : (uint32_t)c->lay.memo_kind;
     out->enum_ms = out->eval_ms = 0;
     if (c->fused && c->nkev == 2) {      // the fused kernel: enumeration and evaluation together
         float t = 0;

@@ -69,6 +69,7 @@ FLAG_DPSUB_ENUM = 256
 FLAG_RANK_MEMO = 512
 FLAG_NO_SMALL = 1024
 FLAG_NO_CCC = 2048
+FLAG_NO_STAR = 4096
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",

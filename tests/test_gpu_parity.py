@@ -218,7 +218,7 @@ def test_memo_layouts_agree(ctx, topo, n, seed):
         r2 = c.mpdp_optimize(g)
         assert r2.memo_kind == 1
         check(r2, o, g)
-    assert ctx.mpdp_optimize(W.star(16, seed)).memo_kind == 1     # (n > 13) trees keep the colex layout
+    assert ctx.mpdp_optimize(W.snowflake(20, seed)).memo_kind == 1     # (n > 13) trees keep the colex layout
 
 
 @pytest.mark.parametrize("topo,n,seed", [("star", 2, 0), ("chain", 3, 1), ("star", 10, 0), ("snowflake", 13, 2),
@@ -266,6 +266,33 @@ def test_ccc_ablation_parity(ctx, topo, n, seed):
     check(ctx.mpdp_optimize(g), o, g)
     with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_NO_CCC) as c:
         check(c.mpdp_optimize(g), o, g)
+
+
+@pytest.mark.parametrize("n,seed,hub", [(14, 0, 0), (17, 1, 0), (20, 2, 0), (16, 3, 15), (18, 4, 7)])
+def test_star_kernel_parity(ctx, n, seed, hub):
+    """Star queries (n >= 14) run on k_dp_star (memo_kind 4), also with the hub
+    not at vertex 0 (relabelled stars) and with composite leaf costs; the general
+    tree kernel (MPDP_FLAG_NO_STAR) and the oracle agree."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.star(n, seed)
+    if hub:
+        perm = list(range(n))
+        perm[0], perm[hub] = perm[hub], perm[0]          # swap vertex 0 and `hub`
+        card = [0.0] * n
+        for v in range(n):
+            card[perm[v]] = g.card[v]
+        edges = [(min(perm[a], perm[b]), max(perm[a], perm[b])) for a, b in g.edges]
+        g = W.QueryGraph(n, card, edges, list(g.sel), name=f"star-{n}-hub{hub}")
+    if seed % 2:
+        g.leaf_cost = [float((7 * i) % 5) for i in range(n)]
+    o = O.optimize(g)
+    r = ctx.mpdp_optimize(g)
+    assert r.memo_kind == 4, r.memo_kind
+    check(r, o, g)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_NO_STAR) as c:
+        r2 = c.mpdp_optimize(g)
+        assert r2.memo_kind == 1
+        check(r2, o, g)
 
 
 def test_small_kernel_leaf_costs_and_dpsub():
