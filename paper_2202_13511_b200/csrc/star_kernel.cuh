@@ -14,7 +14,7 @@
 //     (the incremental colex rank of the tree fast path, reading R10);
 //   * card(S) = card(S \ {max}) * card[max] * sel(hub, max) bit for bit
 //     (reading R19) when max(S) is a leaf.
-// Each thread walks a contiguous run of ranks (one unrank, then Gosper); small
+// Sets are spread lane-consecutively over the grid (each one unranked); small
 // levels give G = 2 or 4 lanes to a set.  One grid barrier per level.
 #pragma once
 #include "fused.cuh"
@@ -72,13 +72,17 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         while (G < 4 && 2ull * G * C <= T) G <<= 1;
         const unsigned long long ng = T / G, grp = gtid / G;
         const unsigned int sub = threadIdx.x & (G - 1);
-        const unsigned long long h0 = C * grp / ng, h1 = C * (grp + 1) / ng;
+        // lane-consecutive sets (h = it * ng + grp), each one unranked: colex
+        // neighbours share their high elements, so a warp's probes of those
+        // coalesce (per-thread Gosper runs put lanes ~24 sets apart: 27
+        // sectors per request instead of ~14, star-25 1.19 vs 1.01 ms)
         const unsigned long long rounds = (C + ng - 1) / ng;
-        uint32_t L = h0 < h1 ? unrank_colex32(bin, nl, kl, (unsigned int)h0) : 0u;
+        uint32_t L = 0;
         unsigned long long pairs = 0, nprobe = 0, nsets = 0;
         for (unsigned long long it = 0; it < rounds; it++) {
-            const unsigned long long h = h0 + it;
-            const bool act = h < h1;
+            const unsigned long long h = it * ng + grp;
+            const bool act = h < C;
+            if (act) L = unrank_colex32(bin, nl, kl, (unsigned int)h);
             Key best = key_inf();
             double cS = 0.0;
             uint32_t S = 0;
@@ -144,7 +148,6 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                 nprobe += k >= 3 ? (unsigned long long)kl : 0ull;
                 nsets++;
             }
-            if (act) L = gosper(L);
         }
         if ((p.count_levels >> k) & 1ull) {
             flush_counters(&p.desc[k], pairs, pairs, nprobe);
