@@ -390,12 +390,15 @@ __device__ void clique_groups(const Params<uint32_t>& p, int k, const SQ<uint32_
     const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long ngroups = nthreads / G, grp = gtid / G;
     const unsigned int sub = threadIdx.x & (G - 1);
-    const unsigned long long h0 = C * grp / ngroups, h1 = C * (grp + 1) / ngroups;
-    const unsigned long long rounds = (C + ngroups - 1) / ngroups;       // >= h1 - h0 on every group
-    uint32_t S = h0 < h1 ? unrank_colex32(bin, q.n, k, (unsigned int)h0) : 0u;
+    // group-consecutive sets (h = it * ngroups + grp), each one unranked: the
+    // warp's groups work on colex neighbours, whose probes share lines
+    // (per-group Gosper runs: clique-16 316 vs 291 us)
+    const unsigned long long rounds = (C + ngroups - 1) / ngroups;
+    uint32_t S = 0;
     for (unsigned long long it = 0; it < rounds; it++) {
-        const unsigned long long h = h0 + it;
-        const bool act = h < h1;
+        const unsigned long long h = it * ngroups + grp;
+        const bool act = h < C;
+        if (act) S = unrank_colex32(bin, q.n, k, (unsigned int)h);
         Key best = key_inf();
         double cS = 0.0;
         if (act) {
@@ -412,7 +415,6 @@ __device__ void clique_groups(const Params<uint32_t>& p, int k, const SQ<uint32_
             nprobe += probes_per_set;
             nsets++;
         }
-        if (act) S = gosper(S);
     }
 }
 
