@@ -72,17 +72,22 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         while (G < 4 && 2ull * G * C <= T) G <<= 1;
         const unsigned long long ng = T / G, grp = gtid / G;
         const unsigned int sub = threadIdx.x & (G - 1);
-        // lane-consecutive sets (h = it * ng + grp), each one unranked: colex
-        // neighbours share their high elements, so a warp's probes of those
-        // coalesce (per-thread Gosper runs put lanes ~24 sets apart: 27
-        // sectors per request instead of ~14, star-25 1.19 vs 1.01 ms)
-        const unsigned long long rounds = (C + ng - 1) / ng;
+        // lane-consecutive sets, each (run) unranked: colex neighbours share
+        // their high elements, so a warp's probes of those coalesce (per-thread
+        // Gosper runs over a whole share put lanes ~24 sets apart: 27 sectors
+        // per request instead of 8.4, star-25 1.19 vs 1.01 ms)
+        // runs of RUN consecutive sets per group (one unrank, then Gosper) on
+        // levels with several sets per thread: half the unranks for slightly
+        // less coalescing (star-25 1.006 -> 0.945 ms; RUN = 4 no gain, and RUN > 1
+        // on small levels costs parallelism)
+        const unsigned int RUN = C >= 4ull * T ? 2u : 1u;
+        const unsigned long long rounds = (C + ng * RUN - 1) / (ng * RUN) * RUN;
         uint32_t L = 0;
         unsigned long long pairs = 0, nprobe = 0, nsets = 0;
         for (unsigned long long it = 0; it < rounds; it++) {
-            const unsigned long long h = it * ng + grp;
+            const unsigned long long h = (it / RUN * ng + grp) * RUN + it % RUN;
             const bool act = h < C;
-            if (act) L = unrank_colex32(bin, nl, kl, (unsigned int)h);
+            if (act) L = (it % RUN == 0) ? unrank_colex32(bin, nl, kl, (unsigned int)h) : gosper(L);
             Key best = key_inf();
             double cS = 0.0;
             uint32_t S = 0;
