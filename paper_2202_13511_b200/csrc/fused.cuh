@@ -827,9 +827,7 @@ __global__ void __launch_bounds__(kBlock, kCliqueMinBlocks) k_dp_clique(const __
         unsigned long long pairs = 0, nccp = 0, nprobe = 0, nsets = 0;
         clique_level(p, k, q, v, bin, pairs, nccp, nprobe, nsets);
         if ((p.count_levels >> k) & 1ull) {
-            flush_counters(&p.desc[k], pairs, nccp, nprobe);
-            nsets = warp_sum(nsets);
-            if ((threadIdx.x & 31) == 0 && nsets) atomicAdd(&p.desc[k].n_light, nsets);
+            flush_counters(&p.desc[k], pairs, nccp, nprobe, nsets);
         }
         grid_sync(p.gbar, nbar, &p.result->error);
     }

@@ -697,15 +697,31 @@ __device__ __forceinline__ void memo_prologue(const Params<M>& p, int kmax, SQ<M
     }
 }
 
+// Level counters of a CTA into the level descriptor: warp sums, then one
+// reduction per counter per CTA (every warp reducing into the same four
+// addresses serialised ~10k same-address atomics per level at one L2 slice,
+// and the level barrier's release waits for them: 25 us of star-25).  Every
+// thread of the CTA must call it (it contains a __syncthreads).
 __device__ __forceinline__ void flush_counters(LevelDesc* dk, unsigned long long pairs, unsigned long long nccp,
-                                               unsigned long long nprobe) {
+                                               unsigned long long nprobe, unsigned long long nsets = 0) {
+    __shared__ unsigned long long s_fc[32][4];
     pairs = warp_sum(pairs);
     nccp = warp_sum(nccp);
     nprobe = warp_sum(nprobe);
+    nsets = warp_sum(nsets);
+    const unsigned int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        if (pairs) atomicAdd(&dk->pairs, pairs);
-        if (nccp) atomicAdd(&dk->ccp, nccp);
-        if (nprobe) atomicAdd(&dk->probes, nprobe);
+        s_fc[w][0] = pairs;
+        s_fc[w][1] = nccp;
+        s_fc[w][2] = nprobe;
+        s_fc[w][3] = nsets;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        unsigned long long x = 0;
+        for (unsigned int i = 0; i < (blockDim.x >> 5); i++) x += s_fc[i][threadIdx.x];
+        unsigned long long* dst[4] = {&dk->pairs, &dk->ccp, &dk->probes, &dk->n_light};
+        if (x) atomicAdd(dst[threadIdx.x], x);
     }
 }
 

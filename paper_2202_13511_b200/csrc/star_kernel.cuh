@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         const unsigned int RUN = C >= 4ull * T ? 2u : 1u;
         const unsigned long long rounds = (C + ng * RUN - 1) / (ng * RUN) * RUN;
         uint32_t L = 0;
-        unsigned long long pairs = 0, nprobe = 0, nsets = 0;
+        unsigned long long nsets = 0;
         for (unsigned long long it = 0; it < rounds; it++) {
             const unsigned long long h = (it / RUN * ng + grp) * RUN + it % RUN;
             const bool act = h < C;
@@ -149,15 +149,14 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                 p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
                 __stcs(p.memo.dleft + idx, (unsigned int)best.l);
                 p.memo.dcard[idx] = cS;
-                pairs += (unsigned long long)kl;
-                nprobe += k >= 3 ? (unsigned long long)kl : 0ull;
                 nsets++;
             }
         }
         if ((p.count_levels >> k) & 1ull) {
-            flush_counters(&p.desc[k], pairs, pairs, nprobe);
-            nsets = warp_sum(nsets);
-            if ((threadIdx.x & 31) == 0 && nsets) atomicAdd(&p.desc[k].n_light, nsets);
+            // every written set evaluated its kl join pairs (kl non-singleton
+            // probes when k >= 3)
+            const unsigned long long pairs = nsets * (unsigned long long)kl, nprobe = k >= 3 ? pairs : 0ull;
+            flush_counters(&p.desc[k], pairs, pairs, nprobe, nsets);
         }
         grid_sync(p.gbar, nbar, &p.result->error);
     }
