@@ -524,11 +524,11 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.inv_load = 1.0 / c->load_factor;
     p.no_ccc = (c->flags & MPDP_FLAG_NO_CCC) ? 1 : 0;
     p.star_hub = c->star_hub;
-    {
+    {   // star levels: C(n-1, k-1) entries + `world` padding (equal rank segments, as dense_off)
         unsigned long long so = 0;
         for (int k = 0; k <= kMaxN; k++) {
             p.star_off[k] = so;
-            if (k >= 2 && k <= c->n) so += binom_u64(c->n - 1, k - 1);
+            if (k >= 2 && k <= c->n) so += binom_u64(c->n - 1, k - 1) + (unsigned long long)c->world;
         }
     }
     return p;
@@ -731,7 +731,11 @@ static bool star_eligible(const mpdp_ctx* c) {
     return c->lay.memo_kind == MEMO_DENSE;
 }
 
-static mpdp_status run_star(mpdp_ctx* c, const Params<uint32_t>& p) {
+static mpdp_status run_star(mpdp_ctx* c, Params<uint32_t> p) {
+    for (int k = 2; k <= c->n; k++) {                      // every level: all C(n-1, k-1) sets
+        p.share_lo[k] = 0;
+        p.share_hi[k] = (unsigned int)binom_u64(c->n - 1, k - 1);
+    }
     const size_t smem = star_smem_bytes();
     if (!c->star_occ) {
         CUDA_TRY(c, cudaFuncSetAttribute(k_dp_star, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -800,8 +804,7 @@ static mpdp_status run_small(mpdp_ctx* c, const Params<uint32_t>& p) {
 constexpr unsigned long long kShardMinRanks = 1ull << 14;
 
 static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k, unsigned long long C,
-                                  unsigned long long seg, bool with_card) {
-    const unsigned long long off = P[0].dense_off[k];
+                                  unsigned long long seg, bool with_card, unsigned long long off) {
     const int W = c->world;
     if (c->simulate) {
         for (int s = 0; s < W; s++) {
@@ -837,11 +840,21 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     if (c->wide || c->lay.memo_kind != MEMO_DENSE)
         return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
     const int n = c->n, W = c->world, nsh = c->lay.nshards;
-    const size_t smem = level_loop_smem<CLS>(n);
-    int& occ = c->fused_occ[CLS];
-    if (!occ || c->fused_n[CLS] != n) {
-        CUDA_TRY(c, cudaFuncSetAttribute(level_loop_kernel<CLS>(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, level_loop_kernel<CLS>(), kBlock, smem));
+    // star queries shard k_dp_star's leaf-set ranks; everything else the
+    // whole-query kernel's colex ranks
+    const bool star = CLS == CLS_TREE && c->star_hub >= 0 && n >= 3 &&
+                      !(c->flags & (MPDP_FLAG_NO_STAR | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS));
+    const void* kern = star ? (const void*)k_dp_star : level_loop_kernel<CLS>();
+    const size_t smem = star ? star_smem_bytes() : level_loop_smem<CLS>(n);
+    int occ_star = 0;
+    int& occ = star ? occ_star : c->fused_occ[CLS];
+    if (star) {
+        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
+        if (occ < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
+    } else if (!occ || c->fused_n[CLS] != n) {
+        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
         c->fused_n[CLS] = n;
     }
@@ -858,14 +871,13 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     auto launch = [&](Params<uint32_t>& p, unsigned long long grid) -> mpdp_status {
         void* args[] = {&p};
         CUDA_TRY(c, cudaMemsetAsync(p.gbar, 0, sizeof(unsigned int), c->stream));   // barrier counter per launch
-        CUDA_TRY(c, cudaLaunchCooperativeKernel(level_loop_kernel<CLS>(), dim3((unsigned int)grid), dim3(kBlock),
-                                                args, smem, c->stream));
+        CUDA_TRY(c, cudaLaunchCooperativeKernel(kern, dim3((unsigned int)grid), dim3(kBlock), args, smem, c->stream));
         c->launches++;
         return MPDP_OK;
     };
     const unsigned long long min_shard = (c->flags & MPDP_FLAG_SHARD_ALL_LEVELS) ? 0ull : kShardMinRanks;
     for (int k = 2; k <= n; k++) {
-        const unsigned long long C = binom_u64(n, k);
+        const unsigned long long C = star ? binom_u64(n - 1, k - 1) : binom_u64(n, k);
         const bool sharded = W > 1 && C >= min_shard;
         const unsigned long long seg = (C + W - 1) / W;
         for (int sh = 0; sh < nsh; sh++) {
@@ -881,14 +893,15 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
             p.count_levels = counts ? (1ull << k) : 0ull;
             if (counts) counted[sh] |= 1ull << k;
             if (hi <= lo) continue;
-            unsigned long long grid = std::max<unsigned long long>(1, (hi - lo + 511) / 512);
+            unsigned long long grid = std::max<unsigned long long>(1, (hi - lo + (star ? 255 : 511)) / (star ? 256 : 512));
             grid = std::max(grid, heavy_pair_bound(n, k, CLS) / ((unsigned long long)W * 16384));
             if (CLS == CLS_GENERAL) grid = full;
             const mpdp_status st = launch(p, std::min(grid, full));
             if (st != MPDP_OK) return st;
         }
         if (sharded) {
-            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, true);   // cards: card_fast and the extraction read them
+            // cards: card(S \ max) of the next level and the extraction read them
+            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, true, star ? P[0].star_off[k] : P[0].dense_off[k]);
             if (st != MPDP_OK) return st;
         }
         CUDA_TRY(c, cudaGetLastError());
@@ -921,6 +934,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     c->nkev = 0;
     c->d2h_bytes = sizeof(ResultDev) * nsh;
     c->sharded = true;
+    c->star = star;
     return MPDP_OK;
 }
 

@@ -61,10 +61,12 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
     const bool leaf_costs = q.pad != 0;
     const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int k = 2; k <= n; k++) {
+    for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
         const int kl = k - 1;                                 // leaves per set
-        const unsigned int C = bin[nl * 33 + kl];
+        // this launch's share [lo, lo + C) of the level's C(n-1, k-1) sets
+        // (all of them on one GPU; a rank's segment when sharded)
+        const unsigned int lo = p.share_lo[k], C = p.share_hi[k] - lo;
         const double* lvl = p.memo.dcost + p.star_off[k - 1];
         const double* lcard = p.memo.dcard + p.star_off[k - 1];
         const unsigned long long out = p.star_off[k];
@@ -85,8 +87,8 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         uint32_t L = 0;
         unsigned long long nsets = 0;
         for (unsigned long long it = 0; it < rounds; it++) {
-            const unsigned long long h = (it / RUN * ng + grp) * RUN + it % RUN;
-            const bool act = h < C;
+            const unsigned long long h = lo + (it / RUN * ng + grp) * RUN + it % RUN;
+            const bool act = h < lo + (unsigned long long)C;
             if (act) L = (it % RUN == 0) ? unrank_colex32(bin, nl, kl, (unsigned int)h) : gosper(L);
             Key best = key_inf();
             double cS = 0.0;
@@ -164,12 +166,14 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
     // ---- counters and plan extraction
     ResultDev* r = p.result;
     r->t_level[n + 1] = globaltimer_ns();
-    unsigned long long csg = (unsigned long long)n, ccp = 0, pr = 0, probes = 0;
+    // bit 1 of count_levels: this rank counts the n singletons (level 1)
+    const unsigned long long n1 = ((p.count_levels >> 1) & 1ull) ? (unsigned long long)n : 0ull;
+    unsigned long long csg = n1, ccp = 0, pr = 0, probes = 0;
     r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
-    r->lvl_csg[1] = (unsigned long long)n;
+    r->lvl_csg[1] = n1;
     r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
     for (int j = 2; j <= n; j++) {
-        const LevelDesc& d = p.desc[j];
+        const LevelDesc& d = p.desc[j];                       // (zero for levels another rank counts)
         r->lvl_csg[j] = d.n_light;
         r->lvl_ccp[j] = d.ccp;
         r->lvl_pairs[j] = d.pairs;

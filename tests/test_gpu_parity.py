@@ -350,7 +350,7 @@ def test_fused_and_per_level_kernels_agree(topo, n, seed):
 
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("topo,n,seed", [("star", 12, 0), ("clique", 13, 1), ("cycle", 13, 2),
-                                         ("random", 14, 3), ("snowflake", 16, 4)])
+                                         ("random", 14, 3), ("snowflake", 16, 4), ("star", 17, 5)])
 def test_sharded_world_all_levels(world, topo, n, seed):
     """The multi-GPU sharded level loop (per-level colex-rank shares + in-place
     segment exchange + counter reduction), with `world` ranks simulated as memo
