@@ -124,6 +124,14 @@ struct DenseLocate {
 // The children are counted, reserved with one shared-memory atomic and written
 // to this CTA's segment of the next list; rank(S u {v}) = R + C(v, k+1) when v
 // is above max(S), else it is recomputed.
+// A team of whole warps of the CTA that shares a phase's work: the whole CTA,
+// or (sparse levels of the list kernel) half of it, so that the next level's
+// expansion and this level's evaluation run on different warps at once.
+struct Team {
+    unsigned int tid, size;
+};
+__device__ __forceinline__ Team whole_cta() { return Team{threadIdx.x, blockDim.x}; }
+
 struct EmitCtx {
     unsigned long long* seg;               // this CTA's segment of the next level list
     unsigned long long cap;                // its capacity
@@ -235,14 +243,14 @@ __device__ __forceinline__ void small_phase_thread(const Params<uint32_t>& p, in
                                                    unsigned long long c_lo, unsigned long long c_hi,
                                                    unsigned long long& pairs, unsigned long long& nccp,
                                                    unsigned long long& nprobe, const uint2* binp,
-                                                   const EmitCtx* emit) {
-    unsigned long long e = c_lo + threadIdx.x;
+                                                   const EmitCtx* emit, Team tm) {
+    unsigned long long e = c_lo + tm.tid;
     if (e >= c_hi) return;
     unsigned int cur = loc.seek(e);
     unsigned long long nxt = __ldcs(list + loc.at(e, cur));
-    for (; e < c_hi; e += blockDim.x) {
+    for (; e < c_hi; e += tm.size) {
         const unsigned long long ent = nxt;
-        if (e + blockDim.x < c_hi) nxt = __ldcs(list + loc.at(e + blockDim.x, cur));
+        if (e + tm.size < c_hi) nxt = __ldcs(list + loc.at(e + tm.size, cur));
         eval_set_thread<CLS, MEMO>(p, k, q, v, rtab, bin, gen, ent, pairs, nccp, nprobe, binp, emit);
     }
 }
@@ -252,8 +260,8 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
                             const unsigned int* rtab, const unsigned int* bin, unsigned int gen,
                             const unsigned long long* list, const Locate& loc, unsigned long long nsmall,
                             unsigned long long& pairs, unsigned long long& nccp, unsigned long long& nprobe,
-                            const uint2* binp = nullptr, const EmitCtx* emit = nullptr) {
-    const unsigned long long total = (unsigned long long)gridDim.x * blockDim.x;
+                            const uint2* binp = nullptr, const EmitCtx* emit = nullptr, Team tm = whole_cta()) {
+    const unsigned long long total = (unsigned long long)gridDim.x * tm.size;
     unsigned int G = 1;
     // (dense tree levels stop at G = 4: wider groups take the generic
     // per-pair path with a rank lookup per probe; measured snowflake-20 252 ->
@@ -265,14 +273,15 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
     // L1 lines (the list is a concatenation of warp runs of consecutive ranks)
     const unsigned long long c_lo = nsmall * blockIdx.x / gridDim.x, c_hi = nsmall * (blockIdx.x + 1) / gridDim.x;
     if (G == 1) {
-        small_phase_thread<CLS, MEMO>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp, emit);
+        small_phase_thread<CLS, MEMO>(p, k, q, v, rtab, bin, gen, list, loc, c_lo, c_hi, pairs, nccp, nprobe, binp, emit,
+                                      tm);
         return;
     }
-    const unsigned int sub = threadIdx.x & (G - 1);
-    const unsigned int gpc = blockDim.x / G;                 // groups per CTA
+    const unsigned int sub = tm.tid & (G - 1);
+    const unsigned int gpc = tm.size / G;                    // groups per CTA (team)
     // groups in reverse thread order: with only a few sets per CTA the set and
     // the level-ahead expansion (forward order) land on different warps
-    const unsigned int grp = gpc - 1 - threadIdx.x / G;
+    const unsigned int grp = gpc - 1 - tm.tid / G;
     for (unsigned long long base = c_lo; base < c_hi; base += gpc) {      // same trip count on every lane
         const unsigned long long e = base + grp;
         const bool act = e < c_hi;

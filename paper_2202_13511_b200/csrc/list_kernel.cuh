@@ -93,18 +93,19 @@ __device__ void enum_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t
 template <typename Locate>
 __device__ void expand_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const unsigned int* bin,
                                const unsigned long long* src, const Locate& loc, unsigned long long N,
-                               unsigned long long* out, unsigned int* cnt, unsigned long long seg) {
+                               unsigned long long* out, unsigned int* cnt, unsigned long long seg,
+                               Team tm = whole_cta()) {
     // G lanes per input set (largest power of two <= 32 that keeps every set a
     // group); lane `sub` tests the candidates v with index = sub (mod G)
-    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * tm.size;
     unsigned int G = 1;
     while (G < 32 && 2ull * G * N <= nthreads) G <<= 1;
-    const unsigned int sub = threadIdx.x & (G - 1), gpc = blockDim.x / G;
+    const unsigned int sub = tm.tid & (G - 1), gpc = tm.size / G;
     const unsigned long long c_lo = N * blockIdx.x / gridDim.x, c_hi = N * (blockIdx.x + 1) / gridDim.x;
     unsigned long long* segp = out + (unsigned long long)blockIdx.x * seg;
     const unsigned int lane = threadIdx.x & 31;
     for (unsigned long long base = c_lo; base < c_hi; base += gpc) {   // same trip count on every lane
-        const unsigned long long e = base + threadIdx.x / G;
+        const unsigned long long e = base + tm.tid / G;
         uint32_t S = 0, em = 0;
         if (e < c_hi) {
             S = (uint32_t)src[loc(e)];
@@ -285,8 +286,16 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
         const unsigned long long ct_a = globaltimer_ns();
 #endif
         // even warps enumerate level k+1 first, odd warps evaluate level k
-        // first: ALU-bound enumeration overlaps latency-bound evaluation
-        const bool enum_first = ((threadIdx.x >> 5) & 1) == 0;
+        // first: ALU-bound enumeration overlaps latency-bound evaluation.  On
+        // sparse levels (few sets per thread, next level by expansion) the
+        // two halves of the CTA split the work instead: warps 0..3 expand,
+        // warps 4..7 evaluate, so the level costs max(expand, evaluate) of
+        // latency instead of their sum.
+        const bool split = expand && 8ull * N <= (unsigned long long)gridDim.x * blockDim.x && blockDim.x >= 64;
+        const unsigned int half = blockDim.x / 2;
+        const bool enum_first = split ? threadIdx.x < half : ((threadIdx.x >> 5) & 1) == 0;
+        const Team tm_enum = split ? Team{threadIdx.x, half} : whole_cta();
+        const Team tm_eval = split ? Team{threadIdx.x - half, half} : whole_cta();
         unsigned long long pairs = 0, nccp = 0, nprobe = 0;
         __shared__ unsigned int s_emit;
         if (threadIdx.x == 0) s_emit = 0;
@@ -295,7 +304,8 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
         auto next_level = [&]() {
             if (k >= p.k_end || fused_grow) return;
             if (expand)
-                expand_to_list(p, k, q, bin, lists[k & 1], loc, N, lists[(k + 1) & 1], cnts[(k + 1) & 1], seg_next);
+                expand_to_list(p, k, q, bin, lists[k & 1], loc, N, lists[(k + 1) & 1], cnts[(k + 1) & 1], seg_next,
+                               tm_enum);
             else
                 enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
         };
@@ -303,9 +313,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
 #ifdef MPDP_TRACE
         const unsigned long long ct_b = globaltimer_ns();
 #endif
-        if (N) small_phase<CLS, MEMO>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp,
-                                fused_grow ? &ectx : nullptr);
-        if (!enum_first) next_level();
+        if (N && (!split || !enum_first))
+            small_phase<CLS, MEMO>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp,
+                                   fused_grow ? &ectx : nullptr, tm_eval);
+        if (!enum_first && !split) next_level();
         if (fused_grow) {
             __syncthreads();
             if (threadIdx.x == 0) cnts[(k + 1) & 1][blockIdx.x] = s_emit;
