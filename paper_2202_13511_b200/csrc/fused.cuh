@@ -325,10 +325,11 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
 // The level's pair space [0, C(n,k) * w) is cut into one contiguous chunk per
 // warp (>= 1024 pairs), lanes interleaved over j so that a warp's probes fall
 // into few memo lines -- no enumeration, compaction, look-back or heavy list.
-// A set cut by chunk boundaries is merged through the slot of the first chunk
-// that touches it (128-bit CAS min + pair count; the last contributor
-// scatters); slots alternate between two buffers by level parity and each
-// warp clears its slot of the next level's buffer.  Sets with fewer than 32
+// A set cut by chunk boundaries is merged from per-chunk partial keys: a pair
+// count on the slot of the first chunk that touches it elects the last
+// contributor, which reduces the partials and scatters; the count slots
+// alternate between two buffers by level parity and each warp clears its slot
+// of the next level's buffer.  Sets with fewer than 32
 // pairs (k <= 5) take G = 2^(k-1) lanes each, one pair per lane.
 // Memo entries of level 1 (leaf cost, card) are written at k = 2, so probes
 // of levels >= 3 are branch-free loads.
@@ -374,6 +375,11 @@ __device__ __forceinline__ uint32_t deposit_small(unsigned int j, uint32_t R) {
     for (uint32_t T = R; j; T &= T - 1, j >>= 1)
         if (j & 1u) out |= T & (0u - T);
     return out;
+}
+
+__device__ __forceinline__ Key ld_key(const Key* k) {   // written by other SMs in this level: L2
+    const unsigned long long* x = reinterpret_cast<const unsigned long long*>(k);
+    return Key{__ldcg(x), __ldcg(x + 1)};
 }
 
 __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, const Key& best, double cS) {
@@ -439,12 +445,10 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
     const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
     const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long nwarps = nthreads >> 5, gw = gtid >> 5;
-    Key* slot_key = p.bkey + (k & 1) * nwarps;
+    Key* key_first = p.bkey;               // per chunk: key of its first / last set segment
+    Key* key_last = p.bkey + nwarps;
     unsigned long long* slot_done = p.bdone + (k & 1) * nwarps;
-    if (lane == 0) {                       // this warp's slot of level k+1
-        p.bkey[((k + 1) & 1) * nwarps + gw] = key_inf();
-        p.bdone[((k + 1) & 1) * nwarps + gw] = 0;
-    }
+    if (lane == 0) p.bdone[((k + 1) & 1) * nwarps + gw] = 0;   // this warp's counter slot of level k+1
     const bool leaves = k == 2;
     if (leaves && gtid < (unsigned long long)n) {      // level-1 entries
         p.memo.dcost[1u << gtid] = q.leaf[gtid];
@@ -486,19 +490,40 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         if (lane == 0) {
             pairs += b - a;
             nccp += b - a;
-            if (a == 0 && b == w) {
+        }
+        if (a == 0 && b == w) {
+            if (lane == 0) {
                 clique_write(p.memo, S, best, cS);
                 nprobe += probes_per_set;
                 nsets++;
-            } else {
-                const unsigned long long sl = hw / csize;     // first chunk touching set h
-                atomic_key_min(&slot_key[sl], best);
+            }
+        } else {
+            // split set: this chunk's partial key goes to its first / last
+            // segment slot (plain stores); the pair count on the slot of the
+            // first chunk touching the set elects the last contributor, which
+            // reduces the partial keys of all chunks of the set with its warp
+            // (no contended 128-bit CAS: 128 chunks meet at clique-18 k = 18)
+            const bool is_first = h == c0 / w, is_last = hw + b >= c1;
+            unsigned int last = 0;
+            if (lane == 0) {
+                if (is_first) key_first[gw] = best;
+                if (is_last) key_last[gw] = best;
                 __threadfence();
-                const unsigned long long old = atomicAdd(&slot_done[sl], b - a);
-                if (old + (b - a) == w) {      // last contributor scatters the set
-                    __threadfence();
-                    const unsigned long long* kp = reinterpret_cast<const unsigned long long*>(&slot_key[sl]);
-                    clique_write(p.memo, S, Key{ld_relaxed(kp), ld_relaxed(kp + 1)}, cS);
+                const unsigned long long old = atomicAdd(&slot_done[hw / csize], b - a);
+                last = old + (b - a) == w;
+            }
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+                __threadfence();
+                const unsigned long long cf = hw / csize, cl = (hw + w - 1) / csize;
+                Key m = key_inf();
+                if (lane == 0) m = ld_key(&key_last[cf]);
+                for (unsigned long long c = cf + 1 + lane; c <= cl; c += 32) {
+                    const Key t = ld_key(&key_first[c]);
+                    if (key_less(t, m)) m = t;
+                }
+                m = warp_min(m);
+                if (lane == 0) {
+                    clique_write(p.memo, S, m, cS);
                     nprobe += probes_per_set;
                     nsets++;
                 }
