@@ -22,6 +22,8 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <queue>
+#include <tuple>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -193,25 +195,39 @@ static int goo(Driver& D) {
         }
     }
     std::vector<char> alive(n, 1);
+    // The cheapest join among all current component pairs, in the order of a
+    // full scan (card, cost, lowest relation, then pair (a < b) ascending):
+    // a min-heap of candidate joins stamped with the versions of both sides;
+    // a merge re-pushes the merged component's pairs, stale entries are
+    // skipped.  O(E log E) instead of a scan of every pair per step.
+    struct Cand {
+        double c, cost;
+        int key, a, b;
+        unsigned va, vb;
+        bool operator>(const Cand& o) const {
+            return std::tie(c, cost, key, a, b) > std::tie(o.c, o.cost, o.key, o.a, o.b);
+        }
+    };
+    std::vector<unsigned> ver(n, 0);
+    std::priority_queue<Cand, std::vector<Cand>, std::greater<Cand>> pq;
+    auto push = [&](int a, int b, double s) {
+        if (a > b) std::swap(a, b);
+        const double c = D.pool[root[a]].card * D.pool[root[b]].card * s;
+        const double cost = (D.pool[root[a]].cost + D.pool[root[b]].cost) + c;
+        pq.push(Cand{c, cost, std::min(minrel[a], minrel[b]), a, b, ver[a], ver[b]});
+    };
+    for (int a = 0; a < n; a++)
+        for (auto& [b, s] : nb[a])
+            if (b > a) push(a, b, s);
     for (int step = 0; step < n - 1; step++) {
         int ba = -1, bb = -1;
-        double bcard = 0, bcost = 0;
-        for (int a = 0; a < n; a++) {
-            if (!alive[a]) continue;
-            for (auto& [b, s] : nb[a]) {
-                if (b <= a) continue;
-                const double c = D.pool[root[a]].card * D.pool[root[b]].card * s;
-                const double cost = (D.pool[root[a]].cost + D.pool[root[b]].cost) + c;
-                const int key = std::min(minrel[a], minrel[b]);
-                const bool better = ba < 0 || c < bcard || (c == bcard && cost < bcost) ||
-                                    (c == bcard && cost == bcost && key < std::min(minrel[ba], minrel[bb]));
-                if (better) {
-                    ba = a;
-                    bb = b;
-                    bcard = c;
-                    bcost = cost;
-                }
-            }
+        while (!pq.empty()) {
+            const Cand t = pq.top();
+            pq.pop();
+            if (!alive[t.a] || !alive[t.b] || ver[t.a] != t.va || ver[t.b] != t.vb) continue;   // stale
+            ba = t.a;
+            bb = t.b;
+            break;
         }
         if (ba < 0) return -1;   // disconnected (validated before)
         HNode h;
@@ -236,6 +252,8 @@ static int goo(Driver& D) {
         }
         nb[ba].erase(bb);
         nb[bb].clear();
+        ver[ba]++;
+        for (auto& [c, s] : nb[ba]) push(ba, c, s);
     }
     for (int a = 0; a < n; a++)
         if (alive[a]) return root[a];
@@ -396,23 +414,26 @@ static int uniondp(Driver& D, int k) {
             while (uf[x] != x) x = uf[x] = uf[uf[x]];
             return x;
         };
+        // repeatedly the edge of minimal (combined size, weight, edge id) among
+        // edges joining different sets with combined size <= k: a min-heap with
+        // lazy re-keying -- set sizes only grow, so a stored key never exceeds
+        // the edge's current key, and an entry whose key is still current is
+        // the minimum (O(E log E) per level instead of a scan per union)
+        using UKey = std::tuple<int, double, int, int>;   // (combined size, weight, edge id, ce index)
+        std::priority_queue<UKey, std::vector<UKey>, std::greater<UKey>> pq;
+        for (size_t i = 0; i < ce.size(); i++) pq.emplace(2, ce[i].w, ce[i].id, (int)i);
         int unions = 0;
-        while (true) {
-            int best = -1;
-            int bsize = 0;
-            for (size_t i = 0; i < ce.size(); i++) {
-                const int ra = find(ce[i].a), rb = find(ce[i].b);
-                if (ra == rb) continue;
-                const int s = sz[ra] + sz[rb];
-                if (s > k) continue;
-                if (best < 0 || s < bsize || (s == bsize && ce[i].w < ce[best].w) ||
-                    (s == bsize && ce[i].w == ce[best].w && ce[i].id < ce[best].id)) {
-                    best = (int)i;
-                    bsize = s;
-                }
+        while (!pq.empty()) {
+            const auto [s0, w0, id0, i] = pq.top();
+            pq.pop();
+            const int ra = find(ce[i].a), rb = find(ce[i].b);
+            if (ra == rb) continue;                    // joined already
+            const int s = sz[ra] + sz[rb];
+            if (s > k) continue;                       // can only grow: never valid again
+            if (s != s0) {                             // stale size: re-key
+                pq.emplace(s, w0, id0, i);
+                continue;
             }
-            if (best < 0) break;
-            const int ra = find(ce[best].a), rb = find(ce[best].b);
             uf[rb] = ra;
             sz[ra] += sz[rb];
             unions++;
