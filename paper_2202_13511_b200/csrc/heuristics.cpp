@@ -195,39 +195,25 @@ static int goo(Driver& D) {
         }
     }
     std::vector<char> alive(n, 1);
-    // The cheapest join among all current component pairs, in the order of a
-    // full scan (card, cost, lowest relation, then pair (a < b) ascending):
-    // a min-heap of candidate joins stamped with the versions of both sides;
-    // a merge re-pushes the merged component's pairs, stale entries are
-    // skipped.  O(E log E) instead of a scan of every pair per step.
-    struct Cand {
-        double c, cost;
-        int key, a, b;
-        unsigned va, vb;
-        bool operator>(const Cand& o) const {
-            return std::tie(c, cost, key, a, b) > std::tie(o.c, o.cost, o.key, o.a, o.b);
-        }
-    };
-    std::vector<unsigned> ver(n, 0);
-    std::priority_queue<Cand, std::vector<Cand>, std::greater<Cand>> pq;
-    auto push = [&](int a, int b, double s) {
-        if (a > b) std::swap(a, b);
-        const double c = D.pool[root[a]].card * D.pool[root[b]].card * s;
-        const double cost = (D.pool[root[a]].cost + D.pool[root[b]].cost) + c;
-        pq.push(Cand{c, cost, std::min(minrel[a], minrel[b]), a, b, ver[a], ver[b]});
-    };
-    for (int a = 0; a < n; a++)
-        for (auto& [b, s] : nb[a])
-            if (b > a) push(a, b, s);
     for (int step = 0; step < n - 1; step++) {
         int ba = -1, bb = -1;
-        while (!pq.empty()) {
-            const Cand t = pq.top();
-            pq.pop();
-            if (!alive[t.a] || !alive[t.b] || ver[t.a] != t.va || ver[t.b] != t.vb) continue;   // stale
-            ba = t.a;
-            bb = t.b;
-            break;
+        double bcard = 0, bcost = 0;
+        for (int a = 0; a < n; a++) {
+            if (!alive[a]) continue;
+            for (auto& [b, s] : nb[a]) {
+                if (b <= a) continue;
+                const double c = D.pool[root[a]].card * D.pool[root[b]].card * s;
+                const double cost = (D.pool[root[a]].cost + D.pool[root[b]].cost) + c;
+                const int key = std::min(minrel[a], minrel[b]);
+                const bool better = ba < 0 || c < bcard || (c == bcard && cost < bcost) ||
+                                    (c == bcard && cost == bcost && key < std::min(minrel[ba], minrel[bb]));
+                if (better) {
+                    ba = a;
+                    bb = b;
+                    bcard = c;
+                    bcost = cost;
+                }
+            }
         }
         if (ba < 0) return -1;   // disconnected (validated before)
         HNode h;
@@ -252,8 +238,6 @@ static int goo(Driver& D) {
         }
         nb[ba].erase(bb);
         nb[bb].clear();
-        ver[ba]++;
-        for (auto& [c, s] : nb[ba]) push(ba, c, s);
     }
     for (int a = 0; a < n; a++)
         if (alive[a]) return root[a];

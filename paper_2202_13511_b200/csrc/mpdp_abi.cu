@@ -134,6 +134,11 @@ struct mpdp_ctx {
     bool ran = false;
     int occ[2][3][2][3] = {};            // [wide][class][memo][enum, light, heavy]
     int fused_occ[6] = {}, fused_n[6] = {};   // [CLS + 3 * mask_memo]
+    // occupancy of the whole-query kernels per (slot, n) -- the dynamic shared
+    // memory (rank tables) depends on n; the heuristics' inner DPs change n on
+    // almost every call, and re-querying cost ~0.1 ms of host time per call
+    int occ_by_n[6][kMaxN + 1] = {};
+    bool attr_set[6] = {};
     bool small_attr[3] = {};              // k_dp_small<CLS>: dynamic smem attribute set
     bool small = false;                   // last query ran a single-CTA kernel
     bool tree1_attr = false;
@@ -162,7 +167,8 @@ struct mpdp_ctx {
     };
     std::map<unsigned long long, GraphEntry> graphs;   // level loop per (n, class, memo, width, flags)
     int rank_n = -1;                      // n the uploaded rank tables were built for
-    std::vector<unsigned int> h_rank;
+    std::vector<unsigned int> rank_cache[33];   // host rank tables per n
+    unsigned int* h_rank_pinned = nullptr;  // staging of the async rank-table upload
     cudaEvent_t kev[2 * kMaxN + 2] = {};  // MPDP_FLAG_PROFILE_KERNELS: around every level kernel
     int nkev = 0;
     unsigned int enum_launches = 0, eval_launches = 0;
@@ -628,12 +634,15 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
     const size_t smem = (CLS == CLS_CLIQUE && mask) ? clique_smem_bytes() : level_loop_smem<CLS>(c->n);
     const void* kern = level_loop_kernel<CLS>(mask);
     const int slot = CLS + (mask ? 3 : 0);
-    int& occ = c->fused_occ[slot];
-    if (!occ || c->fused_n[slot] != c->n) {
-        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int& occ = c->occ_by_n[slot][c->n];
+    if (!c->attr_set[slot]) {              // once, for the largest n (32) this kernel can see
+        const size_t smax = (CLS == CLS_CLIQUE && mask) ? clique_smem_bytes() : level_loop_smem<CLS>(32);
+        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        c->attr_set[slot] = true;
+    }
+    if (!occ) {
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
-        c->fused_n[slot] = c->n;
     }
     CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
     k_init<uint32_t><<<1, 64, 0, c->stream>>>(p);
@@ -1167,7 +1176,8 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
         return bail(fail(nullptr, MPDP_ERR_CUDA, "workspace clear failed"));
     const int nsh = simulate ? cfg->world : 1;
     if (cudaMallocHost(&c->h_query, sizeof(QueryDev<uint64_t>)) != cudaSuccess ||
-        cudaMallocHost(&c->h_results, sizeof(ResultDev) * nsh) != cudaSuccess)
+        cudaMallocHost(&c->h_results, sizeof(ResultDev) * nsh) != cudaSuccess ||
+        cudaMallocHost(&c->h_rank_pinned, sizeof(unsigned int) * rank_geom(32).entries) != cudaSuccess)
         return bail(fail(nullptr, MPDP_ERR_OOM, "pinned host allocation failed"));
     c->h_result = c->h_results;
     if (cfg->world > 1 && !simulate) {     // one NCCL communicator per context
@@ -1194,6 +1204,7 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->own_ws && c->ws) cudaFree(c->ws);
     if (c->h_query) cudaFreeHost(c->h_query);
+    if (c->h_rank_pinned) cudaFreeHost(c->h_rank_pinned);
     if (c->comm && c->nccl && c->nccl->CommDestroy) c->nccl->CommDestroy(c->comm);
     if (c->h_results) cudaFreeHost(c->h_results);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1244,20 +1255,26 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
     c->last_memo = c->lay.memo_kind;
     if (c->lay.memo_kind == MEMO_DENSE && c->rank_n != n) {       // chunked colex-rank tables
         const RankGeom rg = rank_geom(n);
-        c->h_rank.assign(rg.entries, 0);
-        for (int ch = 0; ch < rg.nch; ch++) {
-            const int bits = std::min(8, n - 8 * ch);
-            for (int o = 0; o <= 8 * ch; o++)
-                for (unsigned int bv = 0; bv < (1u << bits); bv++) {
-                    unsigned long long val = 0;
-                    int seen = 0;
-                    for (int i = 0; i < bits; i++)
-                        if (bv >> i & 1) val += binom_u64(8 * ch + i, o + (seen++) + 1);
-                    c->h_rank[rg.base[ch] + o * rg.len[ch] + bv] = (unsigned int)val;
-                }
+        std::vector<unsigned int>& tab = c->rank_cache[n];       // built once per n
+        if (tab.empty()) {
+            tab.assign(rg.entries, 0);
+            for (int ch = 0; ch < rg.nch; ch++) {
+                const int bits = std::min(8, n - 8 * ch);
+                for (int o = 0; o <= 8 * ch; o++)
+                    for (unsigned int bv = 0; bv < (1u << bits); bv++) {
+                        unsigned long long val = 0;
+                        int seen = 0;
+                        for (int i = 0; i < bits; i++)
+                            if (bv >> i & 1) val += binom_u64(8 * ch + i, o + (seen++) + 1);
+                        tab[rg.base[ch] + o * rg.len[ch] + bv] = (unsigned int)val;
+                    }
+            }
         }
-        CUDA_TRY(c, cudaMemcpy(c->ws + c->lay.rank, c->h_rank.data(), sizeof(unsigned int) * rg.entries,
-                               cudaMemcpyHostToDevice));
+        // async from pinned memory: the stream is idle here (synchronised above),
+        // so the staging buffer is free, and the kernels follow in stream order
+        memcpy(c->h_rank_pinned, tab.data(), sizeof(unsigned int) * rg.entries);
+        CUDA_TRY(c, cudaMemcpyAsync(c->ws + c->lay.rank, c->h_rank_pinned, sizeof(unsigned int) * rg.entries,
+                                    cudaMemcpyHostToDevice, c->stream));
         c->rank_n = n;
     }
     c->query_counter++;
