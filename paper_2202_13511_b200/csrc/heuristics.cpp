@@ -195,25 +195,52 @@ static int goo(Driver& D) {
         }
     }
     std::vector<char> alive(n, 1);
+    // Candidate joins ordered as a full scan of the component pairs would
+    // order them: (card, cost, lowest relation, a, b) with a < b.  Each
+    // component caches its best pair; a merge recomputes the merged
+    // component's pairs and the cache of a neighbour only when its cached pair
+    // touched the merged components or the new pair beats it.  The step's join
+    // is the minimum over the caches (O(n) per step instead of O(E) map walks).
+    struct Cand {
+        double c = 0, cost = 0;
+        int key = 0, a = -1, b = -1;
+        bool less(const Cand& o) const {
+            if (o.a < 0) return a >= 0;
+            if (a < 0) return false;
+            if (c != o.c) return c < o.c;
+            if (cost != o.cost) return cost < o.cost;
+            if (key != o.key) return key < o.key;
+            if (a != o.a) return a < o.a;
+            return b < o.b;
+        }
+    };
+    auto pair_cand = [&](int x, int y, double s) {
+        Cand t;
+        t.a = std::min(x, y);
+        t.b = std::max(x, y);
+        t.c = D.pool[root[t.a]].card * D.pool[root[t.b]].card * s;
+        t.cost = (D.pool[root[t.a]].cost + D.pool[root[t.b]].cost) + t.c;
+        t.key = std::min(minrel[t.a], minrel[t.b]);
+        return t;
+    };
+    std::vector<Cand> best(n);
+    auto recompute = [&](int x) {
+        Cand m;
+        for (auto& [y, s] : nb[x]) {
+            const Cand t = pair_cand(x, y, s);
+            if (t.less(m)) m = t;
+        }
+        best[x] = m;
+    };
+    for (int a = 0; a < n; a++) recompute(a);
     for (int step = 0; step < n - 1; step++) {
         int ba = -1, bb = -1;
-        double bcard = 0, bcost = 0;
-        for (int a = 0; a < n; a++) {
-            if (!alive[a]) continue;
-            for (auto& [b, s] : nb[a]) {
-                if (b <= a) continue;
-                const double c = D.pool[root[a]].card * D.pool[root[b]].card * s;
-                const double cost = (D.pool[root[a]].cost + D.pool[root[b]].cost) + c;
-                const int key = std::min(minrel[a], minrel[b]);
-                const bool better = ba < 0 || c < bcard || (c == bcard && cost < bcost) ||
-                                    (c == bcard && cost == bcost && key < std::min(minrel[ba], minrel[bb]));
-                if (better) {
-                    ba = a;
-                    bb = b;
-                    bcard = c;
-                    bcost = cost;
-                }
-            }
+        {
+            Cand m;
+            for (int a = 0; a < n; a++)
+                if (alive[a] && best[a].less(m)) m = best[a];
+            ba = m.a;
+            bb = m.b;
         }
         if (ba < 0) return -1;   // disconnected (validated before)
         HNode h;
@@ -238,6 +265,12 @@ static int goo(Driver& D) {
         }
         nb[ba].erase(bb);
         nb[bb].clear();
+        recompute(ba);
+        for (auto& [c, sv] : nb[ba]) {         // neighbours: their pair with ba changed
+            const Cand t = pair_cand(c, ba, sv);
+            if (best[c].a == ba || best[c].b == ba || best[c].a == bb || best[c].b == bb) recompute(c);
+            else if (t.less(best[c])) best[c] = t;
+        }
     }
     for (int a = 0; a < n; a++)
         if (alive[a]) return root[a];
