@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                         cS = card_of(q, S);
                     }
                     // descending walk over L, 4 probes in flight
+                    double bc = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+                    uint32_t bl = 0xffffffffu;
                     unsigned int SD = 0;
                     uint32_t W = L;
                     int m = kl - 1;
@@ -135,14 +137,17 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                         for (int u = 0; u < 4; u++) dv[u] = ok[u] ? lvl[rk[u]] : 0.0;
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
+                            // min of (cost, left) in f64 / u32 (costs are >= 0: the
+                            // f64 order is the bit order of the Key)
                             const double a = leaf_costs ? __dadd_rn(q.leaf[vv[u]], dv[u]) : dv[u];
                             const double c = __dadd_rn(a, cS);
-                            const uint32_t lb = 1u << vv[u], rb = S ^ lb;
-                            const Key key{(unsigned long long)__double_as_longlong(c),
-                                          (unsigned long long)(lb < rb ? lb : rb)};
-                            if (ok[u] && key_less(key, best)) best = key;
+                            const uint32_t lb = 1u << vv[u], rb = S ^ lb, l = lb < rb ? lb : rb;
+                            const bool better = ok[u] && (c < bc || (c == bc && l < bl));
+                            bc = better ? c : bc;
+                            bl = better ? l : bl;
                         }
                     }
+                    best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
                 }
             }
             best = group_min(best, G);
