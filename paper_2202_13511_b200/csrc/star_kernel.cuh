@@ -19,6 +19,8 @@
 #pragma once
 #include "fused.cuh"
 
+#include <type_traits>
+
 namespace mpdp {
 
 constexpr int kStarMinBlocks = 3;
@@ -34,7 +36,9 @@ __device__ __forceinline__ uint32_t star_expand(uint32_t L, int hub) {
 }
 __device__ __forceinline__ int star_vertex(int li, int hub) { return li < hub ? li : li + 1; }
 
-__host__ __device__ constexpr size_t star_smem_bytes() { return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33; }
+__host__ __device__ constexpr size_t star_smem_bytes() {
+    return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33 + 8 + sizeof(uint2) * 33 * 33;
+}
 
 // (cost, left, card) of a star set of the memo (extraction)
 __device__ __forceinline__ unsigned long long star_slot(const Params<uint32_t>& p, const unsigned int* bin, uint32_t S) {
@@ -54,6 +58,13 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
     for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
         const int a = i / 33, b = i % 33;
         bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
+    }
+    // (C(v, m+1), C(v, m+1) - C(v, m)) pairs of the descending walk, 8-byte aligned
+    uint2* binp = reinterpret_cast<uint2*>(smem_raw + ((sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33 + 7) & ~size_t(7)));
+    __syncthreads();
+    for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x) {
+        const int a = i / 32, b = i % 32;
+        binp[a * 33 + b] = make_uint2(bin[a * 33 + b + 1], bin[a * 33 + b + 1] - bin[a * 33 + b]);
     }
     unsigned int nbar = 0;
     __syncthreads();
@@ -116,18 +127,21 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                     unsigned int SD = 0;
                     uint32_t W = L;
                     int m = kl - 1;
-                    while (W) {
+                    // batches of 4 elements: kl / 4 full ones without guards, then
+                    // the remainder
+                    auto batch = [&](auto guard) {
+                        constexpr bool GUARD = decltype(guard)::value;
                         unsigned int rk[4];
                         int vv[4];
                         bool ok[4];
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
-                            const bool has = W != 0;
+                            const bool has = !GUARD || W != 0;
                             const int l = has ? 31 - __clz(W) : 0;
-                            W &= has ? ~(1u << l) : ~0u;
-                            const unsigned int c1 = bin[l * 33 + (has ? m + 1 : 0)], c0 = bin[l * 33 + (has ? m : 0)];
-                            rk[u] = (unsigned int)h - c1 - SD;
-                            SD += has ? c1 - c0 : 0u;
+                            W ^= has ? 1u << l : 0u;
+                            const uint2 cc = binp[l * 33 + (has ? m : 0)];
+                            rk[u] = (unsigned int)h - cc.x - SD;
+                            SD += has ? cc.y : 0u;
                             ok[u] = has && ((unsigned int)m & (G - 1)) == sub;
                             vv[u] = star_vertex(l, hub);
                             m -= has ? 1 : 0;
@@ -146,7 +160,9 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                             bc = better ? c : bc;
                             bl = better ? l : bl;
                         }
-                    }
+                    };
+                    for (int bt = kl >> 2; bt > 0; bt--) batch(std::false_type{});
+                    if (kl & 3) batch(std::true_type{});
                     best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
                 }
             }
