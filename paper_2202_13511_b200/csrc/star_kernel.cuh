@@ -90,10 +90,10 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         // Gosper runs over a whole share put lanes ~24 sets apart: 27 sectors
         // per request instead of 8.4, star-25 1.19 vs 1.01 ms)
         // runs of RUN consecutive sets per group (one unrank, then Gosper) on
-        // levels with several sets per thread: half the unranks for slightly
-        // less coalescing (star-25 1.006 -> 0.945 ms; RUN = 4 no gain, and RUN > 1
-        // on small levels costs parallelism)
-        const unsigned int RUN = C >= 4ull * T ? 2u : 1u;
+        // levels with several sets per thread: fewer unranks for slightly less
+        // coalescing (star-25: RUN 1 -> 2 1.006 -> 0.945 ms; 4 on the largest
+        // levels 0.83 -> 0.81 ms; RUN > 1 on small levels costs parallelism)
+        const unsigned int RUN = C >= 8ull * T ? 4u : (C >= 4ull * T ? 2u : 1u);
         const unsigned long long rounds = (C + ng * RUN - 1) / (ng * RUN) * RUN;
         uint32_t L = 0;
         unsigned long long nsets = 0;
