@@ -336,15 +336,18 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
 template <int G>
 __device__ __forceinline__ void clique_eval_span(const SQ<uint32_t>& q, const double* __restrict__ dcost, uint32_t S,
                                                  uint32_t lo, uint32_t R, uint32_t DG, uint32_t sub,
-                                                 unsigned long long j, unsigned long long b, double cS, bool leaves,
-                                                 Key& best) {
-    // pairs j, j + G, j + 2G, ... of the set; 4 pairs (8 probes) in flight
+                                                 unsigned int j, unsigned int b, double cS, bool leaves, Key& best) {
+    // pairs j, j + G, j + 2G, ... of the set (w < 2^31 pairs); 4 pairs (8
+    // probes) in flight; the min in f64 / u32 registers (costs are >= 0, so
+    // the f64 order is the bit order of the Key)
+    double bc = __longlong_as_double((long long)best.c);
+    uint32_t bl = (uint32_t)best.l;
     for (; j < b; j += 4 * G) {
         uint32_t A[4];
         double ca[4], cb[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            const bool ok = j + (unsigned long long)(G * u) < b;
+            const bool ok = j + G * u < b;
             A[u] = lo | sub;
             const uint32_t B = S ^ A[u];
             if (leaves) {
@@ -358,14 +361,14 @@ __device__ __forceinline__ void clique_eval_span(const SQ<uint32_t>& q, const do
         }
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            if (j + (unsigned long long)(G * u) < b) {
-                const double c = __dadd_rn(__dadd_rn(ca[u], cb[u]), cS);
-                const uint32_t B = S ^ A[u];
-                const Key key{(unsigned long long)__double_as_longlong(c), (unsigned long long)(A[u] < B ? A[u] : B)};
-                if (key_less(key, best)) best = key;
-            }
+            const double c = __dadd_rn(__dadd_rn(ca[u], cb[u]), cS);
+            const uint32_t B = S ^ A[u], l = A[u] < B ? A[u] : B;
+            const bool better = j + G * u < b && (c < bc || (c == bc && l < bl));
+            bc = better ? c : bc;
+            bl = better ? l : bl;
         }
     }
+    if (bl != 0xffffffffu) best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
 }
 
 // deposit(j, R) for j < 2^popc(R) without a bit loop over j: lowest five bits
@@ -419,8 +422,8 @@ __device__ void clique_groups(const Params<uint32_t>& p, int k, const SQ<uint32_
         if (act) {
             cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, (unsigned int)h);
             const uint32_t lo = S & (0u - S), R = S ^ lo;
-            clique_eval_span<G>(q, p.memo.dcost, S, lo, R, deposit_small(G, R), deposit_small(sub, R), sub, w, cS,
-                                leaves, best);
+            clique_eval_span<G>(q, p.memo.dcost, S, lo, R, deposit_small(G, R), deposit_small(sub, R), sub,
+                                (unsigned int)w, cS, leaves, best);
         }
         best = group_min(best, G);
         if (act && sub == 0) {
@@ -485,7 +488,8 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         const uint32_t da = a ? deposit<uint32_t>(a, R) : 0u;
         const uint32_t sub = ((da | ~R) + deposit_small(lane, R)) & R;
         Key best = key_inf();
-        clique_eval_span<32>(q, p.memo.dcost, S, lo, R, D32, sub, a + lane, b, cS, false, best);
+        clique_eval_span<32>(q, p.memo.dcost, S, lo, R, D32, sub, (unsigned int)(a + lane), (unsigned int)b, cS, false,
+                             best);
         best = warp_min(best);
         if (lane == 0) {
             pairs += b - a;
