@@ -947,6 +947,47 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(const __grid_constant_
 // ------------------------------------------------------------ k_extract
 // One thread walks the memo from the full set: left(S) from the
 // memo, right = S \ left; nodes in post-order, root last.  Also sums counters.
+// Level counters into the result, one warp: lane j reads the descriptor of
+// level j (a single thread walking the levels waited one load round trip per
+// level, ~15 us at n = 25).  Bit 1 of count_levels: this rank counts the n
+// singletons (level 1).
+template <typename M>
+__device__ void level_counters_warp(const Params<M>& p, ResultDev* r) {
+    const int n = p.n;
+    const unsigned int lane = threadIdx.x & 31;
+    unsigned long long csg = 0, ccp = 0, pairs = 0, probes = 0;
+    for (int j = (int)lane; j <= n; j += 32) {
+        unsigned long long a = 0, b = 0, c = 0, d = 0;
+        if (j == 1) {
+            a = ((p.count_levels >> 1) & 1ull) ? (unsigned long long)n : 0ull;
+        } else if (j >= 2 && ((p.count_levels >> j) & 1ull)) {
+            const LevelDesc& ds = p.desc[j];
+            a = ds.n_light + ds.n_heavy;
+            b = ds.ccp;
+            c = ds.pairs;
+            d = ds.probes;
+        }
+        r->lvl_csg[j] = a;
+        r->lvl_ccp[j] = b;
+        r->lvl_pairs[j] = c;
+        csg += a;
+        ccp += b;
+        pairs += c;
+        probes += d;
+    }
+    csg = warp_sum(csg);
+    ccp = warp_sum(ccp);
+    pairs = warp_sum(pairs);
+    probes = warp_sum(probes);
+    if (lane == 0) {
+        r->csg = csg;
+        r->ccp = ccp;
+        r->pairs = pairs;
+        r->probes = probes;
+    }
+    __syncwarp();
+}
+
 template <typename M, int MEMO>
 __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView& v, const unsigned int* rtab,
                               unsigned int gen) {

@@ -183,81 +183,96 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         }
         grid_sync(p.gbar, nbar, &p.result->error);
     }
-    if (!(p.do_extract && blockIdx.x == 0 && threadIdx.x == 0)) return;
-    // ---- counters and plan extraction
+    if (!(p.do_extract && blockIdx.x == 0 && threadIdx.x < 32)) return;
+    // ---- counters and plan extraction, warp 0 of CTA 0
     ResultDev* r = p.result;
-    r->t_level[n + 1] = globaltimer_ns();
-    // bit 1 of count_levels: this rank counts the n singletons (level 1)
-    const unsigned long long n1 = ((p.count_levels >> 1) & 1ull) ? (unsigned long long)n : 0ull;
-    unsigned long long csg = n1, ccp = 0, pr = 0, probes = 0;
-    r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
-    r->lvl_csg[1] = n1;
-    r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
-    for (int j = 2; j <= n; j++) {
-        const LevelDesc& d = p.desc[j];                       // (zero for levels another rank counts)
-        r->lvl_csg[j] = d.n_light;
-        r->lvl_ccp[j] = d.ccp;
-        r->lvl_pairs[j] = d.pairs;
-        csg += d.n_light;
-        ccp += d.ccp;
-        pr += d.pairs;
-        probes += d.probes;
-    }
-    r->csg = csg;
-    r->ccp = ccp;
-    r->pairs = pr;
-    r->probes = probes;
-    if (r->error) {
-        r->n_nodes = 0;
+    const unsigned int lane = threadIdx.x;
+    if (lane == 0) r->t_level[n + 1] = globaltimer_ns();
+    level_counters_warp(p, r);
+    if (ld_relaxed_u32(&r->error)) {
+        if (lane == 0) r->n_nodes = 0;
         return;
     }
-    uint32_t st_set[2 * 32], st_L[2 * 32];
-    double st_c[2 * 32], st_card[2 * 32];
-    int st_state[2 * 32], st_left[2 * 32];
-    int sp = 1, nn = 0, last = -1;
-    st_set[0] = n == 32 ? ~0u : (1u << n) - 1u;
-    st_state[0] = 0;
-    while (sp) {
-        const int top = sp - 1;
-        const uint32_t S = st_set[top];
-        if ((S & (S - 1)) == 0) {
-            const int vtx = __ffs(S) - 1;
-            mpdp_plan_node& nd = r->nodes[nn];
-            nd.left = nd.right = -1;
-            nd.relation = vtx;
-            nd.reserved = 0;
-            nd.set = S;
-            nd.cardinality = q.card[vtx];
-            nd.cost = q.leaf[vtx];
-            last = nn++;
-            --sp;
-            continue;
+    // The optimal plan of a star set is a caterpillar: every join splits one
+    // leaf v off, ({v}, S \ {v}).  Walk the chain from V (one memo read per
+    // step; the colex rank of each set's leaf set is a warp sum of one binomial
+    // per element), then emit the post-order nodes from the recorded chain.
+    __shared__ uint32_t c_set[32], c_left[32];
+    __shared__ double c_cost[32], c_card[32];
+    uint32_t S = n == 32 ? ~0u : (1u << n) - 1u;
+    int len = 0;
+    while (__popc(S) >= 2) {
+        const uint32_t L = star_compress(S, hub);
+        const int kl = __popc(L);
+        unsigned int term = 0;
+        if ((int)lane < kl) term = bin[(__fns(L, 0, lane + 1)) * 33 + lane + 1];
+        for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+        const unsigned long long idx = p.star_off[kl + 1] + term;
+        uint32_t left = 0;
+        if (lane == 0) {
+            left = __ldcg(p.memo.dleft + idx);
+            c_set[len] = S;
+            c_left[len] = left;
+            c_cost[len] = __ldcg(p.memo.dcost + idx);
+            c_card[len] = __ldcg(p.memo.dcard + idx);
         }
-        if (st_state[top] == 0) {
-            const unsigned long long idx = star_slot(p, bin, S);
-            st_L[top] = p.memo.dleft[idx];
-            st_c[top] = p.memo.dcost[idx];
-            st_card[top] = p.memo.dcard[idx];
-            st_state[top] = 1;
-            st_set[sp] = st_L[top];
-            st_state[sp++] = 0;
-        } else if (st_state[top] == 1) {
-            st_left[top] = last;
-            st_state[top] = 2;
-            st_set[sp] = S & ~st_L[top];
-            st_state[sp++] = 0;
-        } else {
-            mpdp_plan_node& nd = r->nodes[nn];
-            nd.left = st_left[top];
-            nd.right = last;
-            nd.relation = -1;
-            nd.reserved = 0;
-            nd.set = S;
-            nd.cardinality = st_card[top];
-            nd.cost = st_c[top];
-            last = nn++;
-            --sp;
+        left = __shfl_sync(0xffffffffu, left, 0);
+        const uint32_t right = S ^ left;
+        S = (left & (left - 1)) ? left : right;           // the multi-relation side (a singleton at the end)
+        len++;
+        if ((S & (S - 1)) == 0) break;
+    }
+    if (lane != 0) return;
+    // post-order (left subtree, right subtree, node): with prefix_i = [v_i] when
+    // the leaf is the left child and suffix_i = [v_i if it is the right child,
+    // S_i], the sequence is prefix_0 .. prefix_{len-2}, the bottom pair (two
+    // leaves, then S_{len-1}), suffix_{len-2} .. suffix_0
+    auto leaf_node = [&](uint32_t X, int at) {
+        const int vtx = __ffs(X) - 1;
+        mpdp_plan_node& nd = r->nodes[at];
+        nd.left = nd.right = -1;
+        nd.relation = vtx;
+        nd.reserved = 0;
+        nd.set = X;
+        nd.cardinality = q.card[vtx];
+        nd.cost = q.leaf[vtx];
+    };
+    auto join_node = [&](int i, int a, int b, int at) {
+        mpdp_plan_node& nd = r->nodes[at];
+        nd.left = a;
+        nd.right = b;
+        nd.relation = -1;
+        nd.reserved = 0;
+        nd.set = c_set[i];
+        nd.cardinality = c_card[i];
+        nd.cost = c_cost[i];
+    };
+    int pos_leaf[32];
+    int nn = 0;
+    for (int i = 0; i + 1 < len; i++)
+        if ((c_left[i] & (c_left[i] - 1)) == 0) {     // leaf is the left child
+            leaf_node(c_left[i], nn);
+            pos_leaf[i] = nn++;
         }
+    {
+        const int b = len - 1;
+        const uint32_t A = c_left[b], B = c_set[b] ^ A;
+        leaf_node(A, nn);
+        leaf_node(B, nn + 1);
+        join_node(b, nn, nn + 1, nn + 2);
+        nn += 3;
+    }
+    int inner = nn - 1;
+    for (int i = len - 2; i >= 0; i--) {
+        const uint32_t A = c_left[i];
+        if ((A & (A - 1)) == 0) {
+            join_node(i, pos_leaf[i], inner, nn);
+        } else {                                          // leaf is the right child
+            leaf_node(c_set[i] ^ A, nn);
+            join_node(i, inner, nn, nn + 1);
+            nn++;
+        }
+        inner = nn++;
     }
     r->n_nodes = (unsigned int)nn;
     r->cost = r->nodes[nn - 1].cost;
