@@ -830,9 +830,10 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             grid_sync(p.gbar, nbar, &p.result->error);
         }
     }
-    if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
-        p.result->t_level[n + 1] = globaltimer_ns();
-        extract_phase<M, MEMO>(p, q, v, rtab, gen);
+    if (p.do_extract && blockIdx.x == 0 && threadIdx.x < 32) {
+        if (threadIdx.x == 0) p.result->t_level[n + 1] = globaltimer_ns();
+        level_counters_warp(p, p.result);
+        if (threadIdx.x == 0) extract_phase<M, MEMO>(p, q, v, rtab, gen);
     }
 }
 
@@ -869,9 +870,10 @@ __global__ void __launch_bounds__(kBlock, kCliqueMinBlocks) k_dp_clique(const __
         }
         grid_sync(p.gbar, nbar, &p.result->error);
     }
-    if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
-        p.result->t_level[p.n + 1] = globaltimer_ns();
-        extract_phase<uint32_t, MEMO_MASK>(p, q, v, bin, p.q->gen);
+    if (p.do_extract && blockIdx.x == 0 && threadIdx.x < 32) {
+        if (threadIdx.x == 0) p.result->t_level[p.n + 1] = globaltimer_ns();
+        level_counters_warp(p, p.result);
+        if (threadIdx.x == 0) extract_phase<uint32_t, MEMO_MASK>(p, q, v, bin, p.q->gen);
     }
 }
 

@@ -991,32 +991,9 @@ __device__ void level_counters_warp(const Params<M>& p, ResultDev* r) {
 template <typename M, int MEMO>
 __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView& v, const unsigned int* rtab,
                               unsigned int gen) {
+    // (the level counters are written by level_counters_warp before)
     ResultDev* r = p.result;
     const int n = p.n;
-    // bit 1 of count_levels: this rank counts the n singletons (level 1)
-    const unsigned long long n1 = ((p.count_levels >> 1) & 1ull) ? (unsigned long long)n : 0ull;
-    unsigned long long csg = n1, ccp = 0, pairs = 0, probes = 0;
-    r->lvl_csg[0] = r->lvl_ccp[0] = r->lvl_pairs[0] = 0;
-    r->lvl_csg[1] = n1;
-    r->lvl_ccp[1] = r->lvl_pairs[1] = 0;
-    for (int j = 2; j <= n; j++) {
-        const LevelDesc& d = p.desc[j];
-        if (!((p.count_levels >> j) & 1ull)) {   // sharded run: another rank counts level j
-            r->lvl_csg[j] = r->lvl_ccp[j] = r->lvl_pairs[j] = 0;
-            continue;
-        }
-        r->lvl_csg[j] = d.n_light + d.n_heavy;
-        r->lvl_ccp[j] = d.ccp;
-        r->lvl_pairs[j] = d.pairs;
-        csg += d.n_light + d.n_heavy;
-        ccp += d.ccp;
-        pairs += d.pairs;
-        probes += d.probes;
-    }
-    r->csg = csg;
-    r->ccp = ccp;
-    r->pairs = pairs;
-    r->probes = probes;
     if (r->error) {
         r->n_nodes = 0;
         return;
@@ -1088,7 +1065,10 @@ __global__ void k_extract(const __grid_constant__ Params<M> p) {
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
     const unsigned int gen = p.q->gen;
     __syncthreads();
-    if (threadIdx.x == 0) extract_phase<M, MEMO>(p, q, v, rtab, gen);
+    if (threadIdx.x < 32) {
+        level_counters_warp(p, p.result);
+        if (threadIdx.x == 0) extract_phase<M, MEMO>(p, q, v, rtab, gen);
+    }
 }
 
 }  // namespace mpdp

@@ -348,9 +348,10 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
 #endif
         grid_sync(p.gbar, nbar, &p.result->error);
     }
-    if (p.do_extract && blockIdx.x == 0 && threadIdx.x == 0) {
-        p.result->t_level[p.n + 1] = globaltimer_ns();
-        extract_phase<uint32_t, MEMO>(p, q, v, rtab, gen);
+    if (p.do_extract && blockIdx.x == 0 && threadIdx.x < 32) {
+        if (threadIdx.x == 0) p.result->t_level[p.n + 1] = globaltimer_ns();
+        level_counters_warp(p, p.result);
+        if (threadIdx.x == 0) extract_phase<uint32_t, MEMO>(p, q, v, rtab, gen);
     }
 }
 

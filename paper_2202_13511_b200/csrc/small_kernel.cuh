@@ -451,9 +451,9 @@ __global__ void __launch_bounds__(kTree1Block, 1) k_dp_tree1(const __grid_consta
         }
         __syncthreads();
     }
-    if (p.do_extract && threadIdx.x == 0) {
-        __threadfence_block();
-        extract_phase<uint32_t, MEMO>(p, q, v, rtab, gen);
+    if (p.do_extract && threadIdx.x < 32) {
+        level_counters_warp(p, p.result);
+        if (threadIdx.x == 0) extract_phase<uint32_t, MEMO>(p, q, v, rtab, gen);
     }
 }
 
