@@ -24,8 +24,8 @@ constexpr int kListChunk = 32;             // ranks per thread per reservation p
 
 // Level k's share [share_lo, share_hi) -> segmented list `out` (entries
 // rank << 32 | mask): CTA b owns the segment [b * seg, (b + 1) * seg) with
-// seg = blockDim * rpt (its ranks); cnt[b] (zeroed beforehand) counts its
-// survivors.  Every thread walks a contiguous run of rpt ranks (one unrank,
+// seg = blockDim * rpt (its ranks); *cnt (this CTA's counter, zeroed
+// beforehand; shared memory inside the level loop) counts its survivors.  Every thread walks a contiguous run of rpt ranks (one unrank,
 // then Gosper); per pass of kListChunk ranks a warp reserves its survivors with
 // one atomic on its CTA's counter.  No CTA-wide synchronisation, so warps can
 // interleave enumeration and evaluation.  (One grid-wide counter serialised
@@ -67,7 +67,7 @@ __device__ void enum_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t
         }
         const unsigned int total = __shfl_sync(0xffffffffu, inc, 31);
         unsigned int base = 0;
-        if (lane == 31 && total) base = atomicAdd(cnt + blockIdx.x, total);   // only this CTA's warps contend
+        if (lane == 31 && total) base = atomicAdd(cnt, total);   // this CTA's counter: only its warps contend
         base = __shfl_sync(0xffffffffu, base, 31);
         if (c) {
             unsigned long long d = base + inc - c;
@@ -134,7 +134,7 @@ __device__ void expand_to_list(const Params<uint32_t>& p, int k, const SQ<uint32
         }
         const unsigned int total = __shfl_sync(0xffffffffu, inc, 31);
         unsigned int wbase = 0;
-        if (lane == 31 && total) wbase = atomicAdd(cnt + blockIdx.x, total);
+        if (lane == 31 && total) wbase = atomicAdd(cnt, total);
         wbase = __shfl_sync(0xffffffffu, wbase, 31);
         unsigned long long d = wbase + inc - c;
         for (uint32_t E = em; E; E &= E - 1) {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
     if (blockIdx.x == 0 && threadIdx.x == 0)
         p.desc[p.k_begin].seg = (unsigned int)(blockDim.x * list_rpt(p.share_hi[p.k_begin] - p.share_lo[p.k_begin]));
     __syncthreads();
-    enum_to_list<CLS>(p, p.k_begin, q, bin, lists[p.k_begin & 1], cnts[p.k_begin & 1]);
+    enum_to_list<CLS>(p, p.k_begin, q, bin, lists[p.k_begin & 1], cnts[p.k_begin & 1] + blockIdx.x);
     grid_sync(p.gbar, nbar, &p.result->error);
     for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0 && k > p.k_begin) p.result->t_level[k] = globaltimer_ns();
@@ -304,10 +304,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
         auto next_level = [&]() {
             if (k >= p.k_end || fused_grow) return;
             if (expand)
-                expand_to_list(p, k, q, bin, lists[k & 1], loc, N, lists[(k + 1) & 1], cnts[(k + 1) & 1], seg_next,
-                               tm_enum);
+                expand_to_list(p, k, q, bin, lists[k & 1], loc, N, lists[(k + 1) & 1], &s_emit, seg_next, tm_enum);
             else
-                enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], cnts[(k + 1) & 1]);
+                enum_to_list<CLS>(p, k + 1, q, bin, lists[(k + 1) & 1], &s_emit);
         };
         if (enum_first) next_level();
 #ifdef MPDP_TRACE
@@ -317,7 +316,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
             small_phase<CLS, MEMO>(p, k, q, v, rtab, bin, gen, lists[k & 1], loc, N, pairs, nccp, nprobe, binp,
                                    fused_grow ? &ectx : nullptr, tm_eval);
         if (!enum_first && !split) next_level();
-        if (fused_grow) {
+        if (k < p.k_end) {                     // this CTA's count of level k+1 (reserved in shared memory)
             __syncthreads();
             if (threadIdx.x == 0) cnts[(k + 1) & 1][blockIdx.x] = s_emit;
         }
