@@ -149,17 +149,27 @@ struct Driver {
         collect(pool[x].left, rels);
         collect(pool[x].right, rels);
     }
+    // scratch of join_card_cost: relation stamps instead of a fresh n-byte
+    // vector per join
+    std::vector<unsigned> stamp;
+    unsigned cur_stamp = 0;
+    std::vector<int> scratch_l, scratch_r;
     void join_card_cost(int id) {
         HNode& h = pool[id];
-        std::vector<int> L, R;
-        collect(h.left, L);
-        collect(h.right, R);
-        std::vector<char> inR(Q.n, 0);
-        for (int r : R) inR[r] = 1;
+        scratch_l.clear();
+        scratch_r.clear();
+        collect(h.left, scratch_l);
+        collect(h.right, scratch_r);
+        if (stamp.size() != (size_t)Q.n) stamp.assign(Q.n, 0);
+        if (++cur_stamp == 0) {                // wrapped: clear once
+            std::fill(stamp.begin(), stamp.end(), 0u);
+            cur_stamp = 1;
+        }
+        for (int r : scratch_r) stamp[r] = cur_stamp;
         std::vector<int> cross;
-        for (int r : L)
+        for (int r : scratch_l)
             for (auto [u, e] : Q.adj[r])
-                if (inR[u]) cross.push_back(e);
+                if (stamp[u] == cur_stamp) cross.push_back(e);
         std::sort(cross.begin(), cross.end());
         double c = pool[h.left].card * pool[h.right].card;
         for (int e : cross) c = c * Q.sel[e];
@@ -301,7 +311,7 @@ static int idp2(Driver& D, int k) {
             }
         }
         std::reverse(post.begin(), post.end());
-        std::unordered_map<int, int> minrel;
+        std::vector<int> minrel(D.pool.size(), 0);   // per pool node (was a hash map: ~8 ms at n = 1000)
         int best = -1;
         for (int x : post) {
             HNode& h = D.pool[x];
