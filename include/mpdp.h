@@ -200,6 +200,18 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* ctx);
 mpdp_status mpdp_optimize(mpdp_ctx* ctx, const mpdp_query_graph* graph, mpdp_algo algo,
                           uint32_t k, mpdp_result* out);
 
+/* mpdp_optimize(MPDP) of `count` independent queries (e.g. the partitions of
+ * one UnionDP level).  Small tree queries (n <= 13) are solved together by ONE
+ * launch with one CTA per query (the single-CTA shared-memory kernel); the
+ * others run one by one as mpdp_optimize.  graphs[i] / results[i] have the
+ * meaning, layout and ownership of mpdp_optimize's graph / out (results[i].nodes
+ * caller-owned, capacity >= 2n-1); batched results report the launch's device
+ * time.  Errors: as mpdp_optimize (the first one is returned; results of the
+ * queries before it are valid).  Not for world > 1 contexts' sharded queries
+ * (those run one by one).                                                       */
+mpdp_status mpdp_optimize_batch(mpdp_ctx* ctx, const mpdp_query_graph* graphs, uint32_t count,
+                                mpdp_result* results);
+
 /* Split form of mpdp_optimize(MPDP) for device-resident timing:
  *   mpdp_stage : validate + stage the graph (async H2D on the context stream)
  *   mpdp_run   : enqueue every level + plan extraction; returns without a host

@@ -143,6 +143,14 @@ struct mpdp_ctx {
     bool small = false;                   // last query ran a single-CTA kernel
     bool tree1_attr = false;
     bool tree1 = false;                   // last query ran k_dp_tree1 (memo_kind 1, global memo)
+    // mpdp_optimize_batch: per-query device / pinned staging of the batched
+    // single-CTA launch
+    QueryDev<uint32_t>* d_bq = nullptr;
+    ResultDev* d_br = nullptr;
+    QueryDev<uint32_t>* h_bq = nullptr;
+    ResultDev* h_br = nullptr;
+    uint32_t batch_cap = 0;
+    bool batch_attr = false;
     int star_hub = -1;                    // star queries: the relation adjacent to all others
     int star_occ = 0;                     // k_dp_star CTAs per SM
     bool star = false;                    // last query ran k_dp_star (memo_kind 4)
@@ -1215,6 +1223,10 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (c->h_rank_pinned) cudaFreeHost(c->h_rank_pinned);
     if (c->comm && c->nccl && c->nccl->CommDestroy) c->nccl->CommDestroy(c->comm);
     if (c->h_results) cudaFreeHost(c->h_results);
+    if (c->h_bq) cudaFreeHost(c->h_bq);
+    if (c->h_br) cudaFreeHost(c->h_br);
+    if (c->d_bq) cudaFree(c->d_bq);
+    if (c->d_br) cudaFree(c->d_br);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto& e : c->kev)
@@ -1414,6 +1426,121 @@ mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo
     st = mpdp_run(c);
     if (st != MPDP_OK) return st;
     return mpdp_fetch(c, out);
+}
+
+mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uint32_t count, mpdp_result* results) {
+    if (!c) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (count && (!graphs || !results)) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "graphs/results is NULL");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));     // pinned staging is reused
+    const bool batchable = c->world == 1 && c->timeout_ms <= 0 &&
+                           !(c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS |
+                                         MPDP_FLAG_HASH_MEMO | MPDP_FLAG_FORCE_WIDE_MASKS | MPDP_FLAG_DPSUB_ENUM));
+    std::vector<uint32_t> small;               // queries of the batched launch
+    std::vector<std::vector<unsigned long long>> adjs;
+    for (uint32_t i = 0; i < count; i++) {
+        std::vector<unsigned long long> adj;
+        const mpdp_status st = validate(c, &graphs[i], adj);
+        if (st != MPDP_OK) return st;
+        const int n = (int)graphs[i].n;
+        if (results[i].nodes && results[i].capacity < (uint32_t)(2 * n - 1))
+            return fail(c, MPDP_ERR_INVALID_ARGUMENT, "result capacity < 2n-1");
+        const bool tree = n >= 2 && graphs[i].n_edges == (uint32_t)(n - 1);
+        if (batchable && tree && n <= kSmallMaxN) {
+            small.push_back(i);
+            adjs.push_back(std::move(adj));
+        }
+    }
+    if (!small.empty()) {
+        const uint32_t nb = (uint32_t)small.size();
+        if (nb > c->batch_cap) {                // grow the staging
+            if (c->h_bq) cudaFreeHost(c->h_bq);
+            if (c->h_br) cudaFreeHost(c->h_br);
+            if (c->d_bq) cudaFree(c->d_bq);
+            if (c->d_br) cudaFree(c->d_br);
+            c->h_bq = nullptr;
+            c->h_br = nullptr;
+            c->d_bq = nullptr;
+            c->d_br = nullptr;
+            c->batch_cap = 0;
+            const uint32_t cap = std::max<uint32_t>(nb, 64);
+            if (cudaMallocHost(&c->h_bq, sizeof(QueryDev<uint32_t>) * cap) != cudaSuccess ||
+                cudaMallocHost(&c->h_br, sizeof(ResultDev) * cap) != cudaSuccess ||
+                cudaMalloc(&c->d_bq, sizeof(QueryDev<uint32_t>) * cap) != cudaSuccess ||
+                cudaMalloc(&c->d_br, sizeof(ResultDev) * cap) != cudaSuccess)
+                return fail(c, MPDP_ERR_OOM, "batch staging allocation failed");
+            c->batch_cap = cap;
+        }
+        const int saved_n = c->n, saved_cls = c->cls;
+        const bool saved_wide = c->wide;
+        int maxn = 2;
+        for (uint32_t b = 0; b < nb; b++) {
+            const mpdp_query_graph& g = graphs[small[b]];
+            c->n = (int)g.n;
+            c->cls = CLS_TREE;
+            c->wide = false;
+            fill_query<uint32_t>(c, &g, adjs[b], c->h_bq + b);
+            maxn = std::max(maxn, (int)g.n);
+        }
+        c->n = saved_n;
+        c->cls = saved_cls;
+        c->wide = saved_wide;
+        if (!c->batch_attr) {
+            CUDA_TRY(c, cudaFuncSetAttribute(k_dp_small_batch<CLS_TREE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)small_smem_bytes(kSmallMaxN)));
+            c->batch_attr = true;
+        }
+        CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+        CUDA_TRY(c, cudaMemcpyAsync(c->d_bq, c->h_bq, sizeof(QueryDev<uint32_t>) * nb, cudaMemcpyHostToDevice, c->stream));
+        k_dp_small_batch<CLS_TREE><<<nb, kSmallBlock, small_smem_bytes(maxn), c->stream>>>(c->d_bq, c->d_br);
+        CUDA_TRY(c, cudaGetLastError());
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_br, c->d_br, sizeof(ResultDev) * nb, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+        CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+        for (uint32_t b = 0; b < nb; b++) {
+            const ResultDev* r = c->h_br + b;
+            mpdp_result* out = &results[small[b]];
+            const int n = (int)graphs[small[b]].n;
+            if (r->error) return fail(c, MPDP_ERR_INTERNAL, "device consistency check failed in a batched query");
+            out->time_ms = ms;                  // the whole batched launch
+            out->n_nodes = r->n_nodes;
+            out->root = r->n_nodes ? r->n_nodes - 1 : 0;
+            out->cost = r->cost;
+            out->csg_count = r->csg;
+            out->ccp_pairs = r->ccp;
+            out->pairs_evaluated = r->pairs;
+            out->gpu_launches = 1;
+            out->probes = r->probes;
+            out->h2d_bytes = sizeof(QueryDev<uint32_t>);
+            out->d2h_bytes = sizeof(ResultDev);
+            out->enum_launches = 0;
+            out->eval_launches = 1;
+            out->memo_kind = 3u;
+            out->inner_calls = 0;
+            out->enum_ms = 0;
+            out->eval_ms = ms;
+            if (out->nodes) memcpy(out->nodes, r->nodes, sizeof(mpdp_plan_node) * r->n_nodes);
+            for (int k = 0; k <= n; k++) {
+                if (out->level_ms) out->level_ms[k] = (k >= 2 && r->t_level[k] && r->t_level[k + 1]) ? 1e-6 * (double)(r->t_level[k + 1] - r->t_level[k]) : 0.0;
+                if (out->level_csg) out->level_csg[k] = r->lvl_csg[k];
+                if (out->level_ccp) out->level_ccp[k] = r->lvl_ccp[k];
+                if (out->level_pairs) out->level_pairs[k] = r->lvl_pairs[k];
+            }
+        }
+    }
+    // the rest one by one
+    size_t j = 0;
+    for (uint32_t i = 0; i < count; i++) {
+        if (j < small.size() && small[j] == i) {
+            j++;
+            continue;
+        }
+        const mpdp_status st = mpdp_optimize(c, &graphs[i], MPDP_ALGO_MPDP, 0, &results[i]);
+        if (st != MPDP_OK) return st;
+    }
+    return MPDP_OK;
 }
 
 #ifdef MPDP_TRACE

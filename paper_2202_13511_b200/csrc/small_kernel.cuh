@@ -121,11 +121,11 @@ __device__ __forceinline__ unsigned int block_scan_max(unsigned int x, unsigned 
 }
 
 template <int CLS>
-__global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_constant__ Params<uint32_t> p) {
+__device__ __forceinline__ void small_body(const QueryDev<uint32_t>* qd, ResultDev* r) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
-    load_query(q, p.q);
-    const int n = p.n;
+    load_query(q, qd);
+    const int n = qd->n;
     const unsigned int NS = 1u << n;
     double* cost = reinterpret_cast<double*>(smem_raw + sizeof(SQ<uint32_t>));
     double* card = cost + NS;
@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_consta
     __shared__ unsigned int s_len[kSmallMaxN + 2];           // sets per level, then level offsets
     __shared__ unsigned int s_fill[kSmallMaxN + 2];
     __shared__ unsigned int s_lvl[kSmallMaxN + 1][3];        // ccp, pairs, probes per level (u32: n <= 13)
-    ResultDev* r = p.result;
     if (threadIdx.x <= kSmallMaxN + 1) s_len[threadIdx.x] = s_fill[threadIdx.x] = 0;
     if (threadIdx.x < (kSmallMaxN + 1) * 3) (&s_lvl[0][0])[threadIdx.x] = 0;
     if (threadIdx.x == 0) {
@@ -280,6 +279,20 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_consta
     }
     r->n_nodes = (unsigned int)nn;
     r->cost = r->nodes[nn - 1].cost;
+}
+
+template <int CLS>
+__global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small(const __grid_constant__ Params<uint32_t> p) {
+    small_body<CLS>(p.q, p.result);
+}
+
+// Batched small queries (mpdp_optimize_batch): CTA b solves query b -- the
+// independent sub-problems of a heuristic level (UnionDP partitions) or any
+// set of small tree queries run side by side, one SM each.
+template <int CLS>
+__global__ void __launch_bounds__(kSmallBlock, 1) k_dp_small_batch(const QueryDev<uint32_t>* __restrict__ qs,
+                                                                   ResultDev* __restrict__ rs) {
+    small_body<CLS>(qs + blockIdx.x, rs + blockIdx.x);
 }
 
 // ------------------------------------------------------------ k_dp_tree1

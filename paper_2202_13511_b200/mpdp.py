@@ -72,8 +72,8 @@ FLAG_NO_CCC = 2048
 FLAG_NO_STAR = 4096
 
 
-EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_stage", "mpdp_run",
-           "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
+EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_optimize_batch", "mpdp_stage",
+           "mpdp_run", "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
            "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace", "mpdp_subproblem_count",
            "mpdp_subproblem_get", "mpdp_heuristic_optimize"]
 
@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
         "mpdp_ctx_destroy": (C.c_int, [P]),
         "mpdp_optimize": (C.c_int, [P, C.POINTER(mpdp_query_graph), C.c_int, C.c_uint32,
                                     C.POINTER(mpdp_result)]),
+        "mpdp_optimize_batch": (C.c_int, [P, C.POINTER(mpdp_query_graph), C.c_uint32, C.POINTER(mpdp_result)]),
         "mpdp_stage": (C.c_int, [P, C.POINTER(mpdp_query_graph)]),
         "mpdp_run": (C.c_int, [P]),
         "mpdp_fetch": (C.c_int, [P, C.POINTER(mpdp_result)]),
@@ -248,6 +249,20 @@ class Context:
         return rb.to_result()
 
     optimize = mpdp_optimize
+
+    def mpdp_optimize_batch(self, graphs) -> List[Result]:
+        """mpdp_optimize(MPDP) of independent queries; small tree queries share
+        one launch (one CTA each)."""
+        gas = [GraphArgs(g) for g in graphs]
+        rbs = [ResultBuf(g.n) for g in graphs]
+        ga_arr = (mpdp_query_graph * max(1, len(gas)))(*[a.s for a in gas])
+        rb_arr = (mpdp_result * max(1, len(rbs)))(*[b.s for b in rbs])
+        self._check(self.L.mpdp_optimize_batch(self.h, ga_arr, len(gas), rb_arr))
+        out = []
+        for i, b in enumerate(rbs):
+            C.memmove(C.byref(b.s), C.byref(rb_arr[i]), C.sizeof(mpdp_result))
+            out.append(b.to_result())
+        return out
 
     def mpdp_stage(self, g):
         self._ga = GraphArgs(g)

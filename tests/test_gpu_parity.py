@@ -295,6 +295,26 @@ def test_star_kernel_parity(ctx, n, seed, hub):
         check(r2, o, g)
 
 
+def test_optimize_batch(ctx):
+    """mpdp_optimize_batch: small tree queries share one launch (one CTA
+    each), the others run one by one; every result equals the oracle's and the
+    single-query call's."""
+    gs = [W.generate(t, n, s) for s, (t, n) in enumerate(
+        [("star", 2), ("chain", 3), ("star", 10), ("snowflake", 13), ("chain", 13), ("snowflake", 9),
+         ("clique", 8), ("star", 16), ("cycle", 9), ("snowflake", 12), ("star", 13)])]
+    gs[5].leaf_cost = [float(i % 3) for i in range(gs[5].n)]
+    rs = ctx.mpdp_optimize_batch(gs)
+    assert len(rs) == len(gs)
+    for g, r in zip(gs, rs):
+        o = O.optimize(g)
+        check(r, o, g)
+        r1 = ctx.mpdp_optimize(g)
+        assert r.tree() == r1.tree() and r.cost == r1.cost
+        small = len(g.edges) == g.n - 1 and g.n <= 13
+        assert (r.memo_kind == 3) == small, (g.name, r.memo_kind)
+    assert ctx.mpdp_optimize_batch([]) == []
+
+
 def test_small_kernel_leaf_costs_and_dpsub():
     """Composite leaves (non-zero leaf costs) on the small kernel; the
     DPSUB-enumeration ablation (general-graph kernels) agrees on the cost."""
