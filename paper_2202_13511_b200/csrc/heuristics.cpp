@@ -58,6 +58,8 @@ struct Driver {
     unsigned long long pairs = 0, ccp = 0, csg = 0, calls = 0;
     std::string err;
 
+    InnerBatchSolver solve_batch = nullptr;   // optional: independent sub-problems in one call
+
     Driver(const Query& q, InnerSolver s, void* u) : Q(q), solve(s), user(u) {}
 
     int leaf(int r) {
@@ -69,15 +71,20 @@ struct Driver {
         return (int)pool.size() - 1;
     }
 
-    // Solve the sub-problem whose relations are the composites `nodes` (pool
-    // roots covering disjoint relation sets `rels`); returns the pool root of
-    // the optimal subplan (composites expanded), or -1.
-    int solve_sub(const std::vector<int>& nodes, const std::vector<std::vector<int>>& rels,
-                  const std::vector<int>& owner_of_rel_local) {
+    // A sub-problem over the composites `nodes` (pool roots covering disjoint
+    // relation sets): its query graph (merged edges: product of selectivities
+    // in edge-id order) and the buffers of its result.
+    struct SubGraph {
+        std::vector<int> nodes;
+        std::vector<double> card, lc, es;
+        std::vector<uint32_t> ed;
+        std::vector<mpdp_plan_node> out;
+        mpdp_query_graph g;
+        mpdp_result r;
+    };
+    void prepare_sub(const std::vector<int>& nodes, const std::vector<int>& owner_of_rel_local, SubGraph& sg) {
         const int m = (int)nodes.size();
-        if (m == 1) return nodes[0];
-        (void)rels;
-        // merged edges between composites: product of selectivities in edge-id order
+        sg.nodes = nodes;
         std::map<std::pair<int, int>, double> merged;
         for (size_t e = 0; e < Q.edges.size(); e++) {
             const int a = owner_of_rel_local[Q.edges[e].first], b = owner_of_rel_local[Q.edges[e].second];
@@ -87,45 +94,40 @@ struct Driver {
             if (it == merged.end()) merged.emplace(key, Q.sel[e]);
             else it->second = it->second * Q.sel[e];
         }
-        std::vector<double> card(m), lc(m);
+        sg.card.resize(m);
+        sg.lc.resize(m);
         for (int i = 0; i < m; i++) {
-            card[i] = pool[nodes[i]].card;
-            lc[i] = pool[nodes[i]].cost;
+            sg.card[i] = pool[nodes[i]].card;
+            sg.lc[i] = pool[nodes[i]].cost;
         }
-        std::vector<uint32_t> ed;
-        std::vector<double> es;
         for (auto& kv : merged) {
-            ed.push_back((uint32_t)kv.first.first);
-            ed.push_back((uint32_t)kv.first.second);
-            es.push_back(kv.second);
+            sg.ed.push_back((uint32_t)kv.first.first);
+            sg.ed.push_back((uint32_t)kv.first.second);
+            sg.es.push_back(kv.second);
         }
-        mpdp_query_graph g;
-        g.n = (uint32_t)m;
-        g.cardinalities = card.data();
-        g.n_edges = (uint32_t)es.size();
-        g.edges = ed.data();
-        g.selectivities = es.data();
-        g.leaf_costs = lc.data();
-        std::vector<mpdp_plan_node> out(2 * m - 1);
-        mpdp_result r;
-        memset(&r, 0, sizeof(r));
-        r.nodes = out.data();
-        r.capacity = (uint32_t)out.size();
-        const mpdp_status st = solve(user, &g, &r);
-        calls++;
-        if (st != MPDP_OK) {
-            err = "inner DP failed (status " + std::to_string((int)st) + ")";
-            return -1;
-        }
+        sg.g.n = (uint32_t)m;
+        sg.g.cardinalities = sg.card.data();
+        sg.g.n_edges = (uint32_t)sg.es.size();
+        sg.g.edges = sg.ed.data();
+        sg.g.selectivities = sg.es.data();
+        sg.g.leaf_costs = sg.lc.data();
+        sg.out.assign(2 * m - 1, mpdp_plan_node{});
+        memset(&sg.r, 0, sizeof(sg.r));
+        sg.r.nodes = sg.out.data();
+        sg.r.capacity = (uint32_t)sg.out.size();
+    }
+    // counters + translation of a solved sub-problem: local leaf i -> composite
+    // nodes[i]; returns the pool root of the subplan
+    int finish_sub(const SubGraph& sg) {
+        const mpdp_result& r = sg.r;
         pairs += r.pairs_evaluated;
         ccp += r.ccp_pairs;
         csg += r.csg_count;
-        // translate the inner plan: local leaf i -> composite nodes[i]
         std::vector<int> map(r.n_nodes, -1);
         for (uint32_t i = 0; i < r.n_nodes; i++) {
-            const mpdp_plan_node& nd = out[i];
+            const mpdp_plan_node& nd = sg.out[i];
             if (nd.relation >= 0) {
-                map[i] = nodes[nd.relation];
+                map[i] = sg.nodes[nd.relation];
                 continue;
             }
             HNode h;
@@ -138,6 +140,22 @@ struct Driver {
             map[i] = id;
         }
         return map[r.n_nodes - 1];
+    }
+    // Solve the sub-problem whose relations are the composites `nodes`;
+    // returns the pool root of the optimal subplan (composites expanded), or -1.
+    int solve_sub(const std::vector<int>& nodes, const std::vector<std::vector<int>>& rels,
+                  const std::vector<int>& owner_of_rel_local) {
+        (void)rels;
+        if (nodes.size() == 1) return nodes[0];
+        SubGraph sg;
+        prepare_sub(nodes, owner_of_rel_local, sg);
+        const mpdp_status st = solve(user, &sg.g, &sg.r);
+        calls++;
+        if (st != MPDP_OK) {
+            err = "inner DP failed (status " + std::to_string((int)st) + ")";
+            return -1;
+        }
+        return finish_sub(sg);
     }
 
     // card/cost of a join node from its children (recurrence of the header)
@@ -474,19 +492,57 @@ static int uniondp(Driver& D, int k) {
         for (int i = 0; i < m; i++) parts[find(i)].push_back(i);
         std::vector<int> newcomp;
         std::vector<int> new_of_old(m);
+        // the partitions of this level are independent sub-problems: with a
+        // batch solver they are solved in one call (one CTA per small one on
+        // the GPU), then translated in partition order as before
+        std::vector<Driver::SubGraph> subs;
+        subs.reserve(parts.size());
+        std::vector<int> sub_of_part;
         for (auto& [r, members] : parts) {
+            if (members.size() == 1) {
+                sub_of_part.push_back(-1);
+                continue;
+            }
             std::vector<int> nodes;
-            std::vector<std::vector<int>> rels;
             std::vector<int> owner(Q.n, -1);
             for (size_t i = 0; i < members.size(); i++) {
                 nodes.push_back(comp[members[i]]);
                 std::vector<int> rr;
                 D.collect(comp[members[i]], rr);
                 for (int x : rr) owner[x] = (int)i;
-                rels.push_back(rr);
             }
-            const int sub = D.solve_sub(nodes, rels, owner);
-            if (sub < 0) return -1;
+            subs.emplace_back();
+            D.prepare_sub(nodes, owner, subs.back());
+            sub_of_part.push_back((int)subs.size() - 1);
+        }
+        if (D.solve_batch && subs.size() > 1) {
+            std::vector<mpdp_query_graph> gs;
+            std::vector<mpdp_result> rs;
+            for (auto& sg : subs) {
+                gs.push_back(sg.g);
+                rs.push_back(sg.r);
+            }
+            const mpdp_status st = D.solve_batch(D.user, gs.data(), (uint32_t)gs.size(), rs.data());
+            D.calls += subs.size();
+            if (st != MPDP_OK) {
+                D.err = "inner DP batch failed (status " + std::to_string((int)st) + ")";
+                return -1;
+            }
+            for (size_t i = 0; i < subs.size(); i++) subs[i].r = rs[i];
+        } else {
+            for (auto& sg : subs) {
+                const mpdp_status st = D.solve(D.user, &sg.g, &sg.r);
+                D.calls++;
+                if (st != MPDP_OK) {
+                    D.err = "inner DP failed (status " + std::to_string((int)st) + ")";
+                    return -1;
+                }
+            }
+        }
+        size_t pi = 0;
+        for (auto& [r, members] : parts) {
+            const int si = sub_of_part[pi++];
+            const int sub = si < 0 ? comp[members[0]] : D.finish_sub(subs[si]);
             for (int x : members) new_of_old[x] = (int)newcomp.size();
             newcomp.push_back(sub);
         }
@@ -564,7 +620,7 @@ static mpdp_status load(const mpdp_query_graph* g, Query& Q, std::string& err) {
 }
 
 mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolver solve, void* user,
-                mpdp_result* out, std::string& err) {
+                mpdp_result* out, std::string& err, InnerBatchSolver solve_batch) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!out) {
         err = "out is NULL";
@@ -583,6 +639,7 @@ mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolv
         return MPDP_ERR_INVALID_ARGUMENT;
     }
     Driver D(Q, solve, user);
+    D.solve_batch = solve_batch;
     D.pool.reserve(8 * (size_t)n);
     int root;
     if (n == 1) root = D.leaf(0);

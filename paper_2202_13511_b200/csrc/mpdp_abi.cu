@@ -1068,6 +1068,33 @@ static mpdp_status gpu_inner_solver(void* user, const mpdp_query_graph* sub, mpd
     return st;
 }
 
+extern "C" mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uint32_t count,
+                                           mpdp_result* results);
+// independent sub-problems of a UnionDP level in one call (recorded like the
+// single ones)
+static mpdp_status gpu_inner_batch(void* user, const mpdp_query_graph* subs, uint32_t count, mpdp_result* outs) {
+    mpdp_ctx* c = static_cast<mpdp_ctx*>(user);
+    const mpdp_status st = mpdp_optimize_batch(c, subs, count, outs);
+    if (st == MPDP_OK && (c->flags & MPDP_FLAG_RECORD_SUBPROBLEMS)) {
+        for (uint32_t i = 0; i < count; i++) {
+            const mpdp_query_graph* sub = subs + i;
+            const mpdp_result* out = outs + i;
+            mpdp_ctx::SubProblem sp;
+            sp.card.assign(sub->cardinalities, sub->cardinalities + sub->n);
+            sp.sel.assign(sub->selectivities, sub->selectivities + sub->n_edges);
+            sp.edges.assign(sub->edges, sub->edges + 2 * sub->n_edges);
+            if (sub->leaf_costs) sp.leaf.assign(sub->leaf_costs, sub->leaf_costs + sub->n);
+            sp.nodes.assign(out->nodes, out->nodes + out->n_nodes);
+            sp.res = *out;
+            sp.res.nodes = nullptr;
+            sp.res.level_csg = sp.res.level_ccp = sp.res.level_pairs = nullptr;
+            sp.res.level_ms = nullptr;
+            c->subs.push_back(std::move(sp));
+        }
+    }
+    return st;
+}
+
 // ------------------------------------------------------------ C ABI
 extern "C" {
 
@@ -1414,7 +1441,7 @@ mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo
         case MPDP_ALGO_UNIONDP_MPDP: {
             c->subs.clear();
             std::string err;
-            const mpdp_status st = mpdp_heur::run(g, algo, k, gpu_inner_solver, c, out, err);
+            const mpdp_status st = mpdp_heur::run(g, algo, k, gpu_inner_solver, c, out, err, gpu_inner_batch);
             if (st != MPDP_OK) return fail(c, st, err.empty() ? c->err : err);
             return MPDP_OK;
         }
