@@ -24,6 +24,7 @@
 namespace mpdp {
 
 constexpr int kStarMinBlocks = 3;
+constexpr unsigned int kStarSolo = 300;     // levels of at most this many sets run on CTA 0 alone
 
 // leaf space: the vertices other than the hub, vertex v -> v - (v > hub)
 __device__ __forceinline__ uint32_t star_compress(uint32_t S, int hub) {
@@ -70,9 +71,19 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
     __syncthreads();
     const int n = p.n, hub = p.star_hub, nl = n - 1;
     const bool leaf_costs = q.pad != 0;
-    const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
-    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // Levels with at most kStarSolo sets (the first and last few) run on CTA 0
+    // alone with __syncthreads as the level barrier; the grid barrier is taken
+    // only where a full-grid level follows (a grid barrier costs ~1.5 us plus a
+    // global round trip of every set's data).
+    auto solo = [&](int k) { return k >= p.k_begin && k <= p.k_end && p.share_hi[k] - p.share_lo[k] <= kStarSolo; };
     for (int k = p.k_begin; k <= p.k_end; k++) {
+        const bool one = solo(k);
+        if (one && blockIdx.x != 0) {                         // CTA 0's level: join at the next grid barrier
+            if (!solo(k + 1) && k < p.k_end) grid_sync(p.gbar, nbar, &p.result->error);
+            continue;
+        }
+        const unsigned long long T = one ? blockDim.x : (unsigned long long)gridDim.x * blockDim.x;
+        const unsigned long long gtid = one ? threadIdx.x : (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
         const int kl = k - 1;                                 // leaves per set
         // this launch's share [lo, lo + C) of the level's C(n-1, k-1) sets
@@ -181,7 +192,8 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
             const unsigned long long pairs = nsets * (unsigned long long)kl, nprobe = k >= 3 ? pairs : 0ull;
             flush_counters(&p.desc[k], pairs, pairs, nprobe, nsets);
         }
-        grid_sync(p.gbar, nbar, &p.result->error);
+        if (one && (solo(k + 1) || k == p.k_end)) __syncthreads();   // CTA 0 continues alone
+        else grid_sync(p.gbar, nbar, &p.result->error);
     }
     if (!(p.do_extract && blockIdx.x == 0 && threadIdx.x < 32)) return;
     // ---- counters and plan extraction, warp 0 of CTA 0
