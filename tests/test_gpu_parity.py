@@ -421,3 +421,37 @@ def test_dpsub_star_closed_form(dpsub_ctx):
     r = dpsub_ctx.mpdp_optimize(g)
     assert r.pairs_evaluated == 3 ** 19 - 2 ** 19
     assert r.ccp_pairs == 19 * 2 ** 18
+
+
+def test_randomized_sweep_all_paths(ctx):
+    """Seeded sweep over topologies and sizes that hit every single-GPU kernel
+    (single-CTA small / tree1, star, list, clique, general) and the batch entry
+    point; every result equals the oracle's."""
+    import random
+    from paper_2202_13511_b200 import mpdp
+    rng = random.Random(2202)
+    gs = []
+    for i in range(48):
+        topo = rng.choice(["star", "snowflake", "chain", "cycle", "clique", "random"])
+        hi = {"clique": 13, "random": 13, "cycle": 16, "star": 19, "snowflake": 19, "chain": 22}[topo]
+        g = W.generate(topo, rng.randint(2 if topo in ("star", "chain", "snowflake") else 3, hi), 1000 + i)
+        if topo == "star" and g.n >= 3 and rng.random() < 0.5:        # hub moved off vertex 0
+            h = rng.randrange(g.n)
+            perm = list(range(g.n))
+            perm[0], perm[h] = perm[h], perm[0]
+            card = [0.0] * g.n
+            for v in range(g.n):
+                card[perm[v]] = g.card[v]
+            edges = [(min(perm[a], perm[b]), max(perm[a], perm[b])) for a, b in g.edges]
+            g = W.QueryGraph(g.n, card, edges, list(g.sel), name=f"{g.name}-hub{h}")
+        if rng.random() < 0.3:
+            g.leaf_cost = [float(rng.choice([0, 1, 7, 1000])) for _ in range(g.n)]
+        gs.append(g)
+    oracle = [O.optimize(g) for g in gs]
+    for g, o in zip(gs, oracle):
+        check(ctx.mpdp_optimize(g), o, g)
+    for g, o, r in zip(gs, oracle, ctx.mpdp_optimize_batch(gs)):
+        check(r, o, g)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_NO_SMALL | mpdp.FLAG_NO_STAR) as c:
+        for g, o in zip(gs[:16], oracle[:16]):
+            check(c.mpdp_optimize(g), o, g)
