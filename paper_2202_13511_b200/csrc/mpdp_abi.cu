@@ -878,7 +878,11 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
     } else if (!occ || c->fused_n[CLS] != n) {
-        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        // function attributes are process-wide (shared by every context): always
+        // raise the limit to the largest n, never lower it below another
+        // context's launch
+        CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)level_loop_smem<CLS>(32)));
         CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "fused kernel does not fit on an SM");
         c->fused_n[CLS] = n;

@@ -455,3 +455,18 @@ def test_randomized_sweep_all_paths(ctx):
     with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_NO_SMALL | mpdp.FLAG_NO_STAR) as c:
         for g, o in zip(gs[:16], oracle[:16]):
             check(c.mpdp_optimize(g), o, g)
+
+
+def test_contexts_share_kernel_attributes(ctx):
+    """Kernel attributes (dynamic shared memory limits) are process-wide: a
+    sharded context running a small query must not lower the limit another
+    context's larger query launches with (regression: cooperative launch
+    'invalid argument' after a simulated-world run of a smaller n)."""
+    from paper_2202_13511_b200 import mpdp
+    small, big = W.snowflake(14, 3), W.snowflake(22, 4)
+    ob = O.optimize(big)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, world=2,
+                      flags=mpdp.FLAG_SIMULATE_WORLD | mpdp.FLAG_SHARD_ALL_LEVELS) as sh:
+        check(ctx.mpdp_optimize(big), ob, big)
+        check(sh.mpdp_optimize(small), O.optimize(small), small)
+        check(ctx.mpdp_optimize(big), ob, big)
