@@ -10,6 +10,7 @@
     on cliques / general graphs
   * no-small (MPDP_FLAG_NO_SMALL): small / thin tree queries on the multi-CTA
     list kernel instead of the single-CTA kernels
+  * no-star (MPDP_FLAG_NO_STAR): star queries on the general tree kernel
 Usage: python tools/ablation.py [reps] [config ...]"""
 import os
 import statistics
@@ -24,7 +25,8 @@ reps = int(args.pop(0)) if args and args[0].isdigit() else 5
 configs = args or ["star-10", "star-20", "star-25", "snowflake-20", "chain-25", "clique-14", "clique-18", "cycle-16",
                    "random-18"]
 modes = [("mpdp", 0), ("per-level", mpdp.FLAG_NO_FUSED), ("dpsub", mpdp.FLAG_DPSUB_ENUM),
-         ("no-ccc", mpdp.FLAG_NO_CCC), ("rank-memo", mpdp.FLAG_RANK_MEMO), ("no-small", mpdp.FLAG_NO_SMALL)]
+         ("no-ccc", mpdp.FLAG_NO_CCC), ("rank-memo", mpdp.FLAG_RANK_MEMO), ("no-small", mpdp.FLAG_NO_SMALL),
+         ("no-star", mpdp.FLAG_NO_STAR)]
 ctxs = {m: mpdp.Context(device=0, workspace_bytes=8 << 30, flags=f) for m, f in modes}
 print(f"{'config':13s} {'mode':10s} {'ms':>10s} {'pairs_evaluated':>16s} {'ccp_pairs':>12s} {'pairs/ccp':>10s} {'time/mpdp':>9s}")
 for name in configs:
