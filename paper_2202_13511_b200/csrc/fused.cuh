@@ -392,9 +392,26 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 }
 
 // lanes per set of w pairs: the power of two nearest (w + 1) / 8, 1..32
-__host__ __device__ __forceinline__ unsigned int clique_group(unsigned long long w) {
+// Lanes per set for the whole-set group path: the fewest lanes (a power of
+// two) that keep each lane at <= kCliquePPL pairs, widened while fewer than a
+// quarter of the grid's threads would hold a set.  Few lanes per set amortise
+// the per-set work (unrank, card, group min) and keep a lane's consecutive
+// pairs in nearby memo lines; the fill rule keeps small levels parallel.
+// Returns 0 (pair chunks per warp, the split path) for levels of fewer sets
+// than warps whose sets exceed 32 * kCliquePPL pairs.  (A fixed ~8 pairs per
+// lane: clique-18 1.04 ms, clique-16 0.27, clique-20 7.5 ms; kCliquePPL = 64 /
+// 128 / 256 / 512: clique-18 0.81 / 0.76 / 0.75 / 0.80 ms, clique-16 0.23 /
+// 0.25 / 0.29 / 0.34 ms, clique-20 5.8 / 5.4 / 4.9 / 4.2 ms.)
+#ifndef CLIQUE_PPL
+#define CLIQUE_PPL 128
+#endif
+constexpr unsigned long long kCliquePPL = CLIQUE_PPL;
+__device__ __forceinline__ unsigned int clique_group(unsigned long long w, unsigned long long C,
+                                                     unsigned long long T) {
     unsigned int G = 1;
-    while (G < 32 && 8ull * G < w + 1) G <<= 1;
+    while (G < 32 && w + 1 > kCliquePPL * G) G <<= 1;
+    while (G < 32 && 2ull * G <= w + 1 && 4ull * C * G < T) G <<= 1;
+    if (G == 32 && w + 1 > 32ull * kCliquePPL && 32ull * C < T) return 0;
     return G;
 }
 
@@ -457,16 +474,16 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         p.memo.dcost[1u << gtid] = q.leaf[gtid];
         p.memo.dcard[1u << gtid] = q.card[gtid];
     }
-    // G lanes per set, about 8 pairs per lane: G = 1, 2, 4, 8, 16 up to
-    // w = 127; whole sets, contiguous runs per group (Gosper successor)
-    const unsigned int G = clique_group(w);
-    if (G < 32) {
+    // whole sets per group of G lanes (clique_group), or pair chunks per warp
+    const unsigned int G = clique_group(w, C, nthreads);
+    if (G) {
         switch (G) {
             case 1: clique_groups<1>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
             case 2: clique_groups<2>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
             case 4: clique_groups<4>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
             case 8: clique_groups<8>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-            default: clique_groups<16>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 16: clique_groups<16>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            default: clique_groups<32>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
         }
         return;
     }
