@@ -393,24 +393,29 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 
 // lanes per set of w pairs: the power of two nearest (w + 1) / 8, 1..32
 // Lanes per set for the whole-set group path: the fewest lanes (a power of
-// two) that keep each lane at <= kCliquePPL pairs, widened while fewer than a
-// quarter of the grid's threads would hold a set.  Few lanes per set amortise
+// two) that keep each lane at <= kCliquePPL pairs, widened while fewer than
+// half of the grid's threads would hold a set.  Few lanes per set amortise
 // the per-set work (unrank, card, group min) and keep a lane's consecutive
 // pairs in nearby memo lines; the fill rule keeps small levels parallel.
 // Returns 0 (pair chunks per warp, the split path) for levels of fewer sets
 // than warps whose sets exceed 32 * kCliquePPL pairs.  (A fixed ~8 pairs per
 // lane: clique-18 1.04 ms, clique-16 0.27, clique-20 7.5 ms; kCliquePPL = 64 /
 // 128 / 256 / 512: clique-18 0.81 / 0.76 / 0.75 / 0.80 ms, clique-16 0.23 /
-// 0.25 / 0.29 / 0.34 ms, clique-20 5.8 / 5.4 / 4.9 / 4.2 ms.)
+// 0.25 / 0.29 / 0.34 ms, clique-20 5.8 / 5.4 / 4.9 / 4.2 ms at a quarter;
+// widening to half of the threads with 256 pairs: clique-18 0.72 ms, clique-16
+// 0.28 ms, clique-20 4.9 ms.)
 #ifndef CLIQUE_PPL
-#define CLIQUE_PPL 128
+#define CLIQUE_PPL 256
+#endif
+#ifndef CLIQUE_FILL
+#define CLIQUE_FILL 2ull                   // widen while fewer than T / CLIQUE_FILL threads hold a set
 #endif
 constexpr unsigned long long kCliquePPL = CLIQUE_PPL;
 __device__ __forceinline__ unsigned int clique_group(unsigned long long w, unsigned long long C,
                                                      unsigned long long T) {
     unsigned int G = 1;
     while (G < 32 && w + 1 > kCliquePPL * G) G <<= 1;
-    while (G < 32 && 2ull * G <= w + 1 && 4ull * C * G < T) G <<= 1;
+    while (G < 32 && 2ull * G <= w + 1 && CLIQUE_FILL * C * G < T) G <<= 1;
     if (G == 32 && w + 1 > 32ull * kCliquePPL && 32ull * C < T) return 0;
     return G;
 }
