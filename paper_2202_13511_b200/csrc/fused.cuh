@@ -392,32 +392,32 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 }
 
 // lanes per set of w pairs: the power of two nearest (w + 1) / 8, 1..32
-// Lanes per set for the whole-set group path: the fewest lanes (a power of
-// two) that keep each lane at <= kCliquePPL pairs, widened while fewer than
-// half of the grid's threads would hold a set.  Few lanes per set amortise
-// the per-set work (unrank, card, group min) and keep a lane's consecutive
-// pairs in nearby memo lines; the fill rule keeps small levels parallel.
+// Lanes per set for the whole-set group path.  A level of C sets of w pairs
+// on T threads with G lanes per set takes ceil(C * G / T) rounds of w / G pairs
+// per lane plus a per-set overhead (unrank, card, group min, scatter) worth
+// about kCliqueSetCost pairs; G (a power of two up to 32, at most w + 1) minimises
+// rounds * (w / G + kCliqueSetCost), ties to the smaller G.  Few lanes per set
+// amortise the per-set work and keep a lane's consecutive pairs in nearby memo
+// lines; more lanes fill the grid and shorten the level's last round.
 // Returns 0 (pair chunks per warp, the split path) for levels of fewer sets
-// than warps whose sets exceed 32 * kCliquePPL pairs.  (A fixed ~8 pairs per
-// lane: clique-18 1.04 ms, clique-16 0.27, clique-20 7.5 ms; kCliquePPL = 64 /
-// 128 / 256 / 512: clique-18 0.81 / 0.76 / 0.75 / 0.80 ms, clique-16 0.23 /
-// 0.25 / 0.29 / 0.34 ms, clique-20 5.8 / 5.4 / 4.9 / 4.2 ms at a quarter;
-// widening to half of the threads with 256 pairs: clique-18 0.72 ms, clique-16
-// 0.28 ms, clique-20 4.9 ms.)
-#ifndef CLIQUE_PPL
-#define CLIQUE_PPL 256
-#endif
-#ifndef CLIQUE_FILL
-#define CLIQUE_FILL 2ull                   // widen while fewer than T / CLIQUE_FILL threads hold a set
-#endif
-constexpr unsigned long long kCliquePPL = CLIQUE_PPL;
+// than warps whose sets exceed 8192 pairs.  Measured (clique-18 / 16 / 20):
+// fixed ~8 pairs per lane 1.04 / 0.27 / 7.5 ms; <= 256 pairs per lane widened
+// to half the threads 0.72 / 0.28 / 4.9 ms; this model (cost 64) 0.66 / 0.29 /
+// 3.9 ms (cost 32: 0.77 / 0.29 / 4.0; cost 128: 0.66 / 0.29 / 3.9).
+constexpr double kCliqueSetCost = 64.0;
 __device__ __forceinline__ unsigned int clique_group(unsigned long long w, unsigned long long C,
                                                      unsigned long long T) {
-    unsigned int G = 1;
-    while (G < 32 && w + 1 > kCliquePPL * G) G <<= 1;
-    while (G < 32 && 2ull * G <= w + 1 && CLIQUE_FILL * C * G < T) G <<= 1;
-    if (G == 32 && w + 1 > 32ull * kCliquePPL && 32ull * C < T) return 0;
-    return G;
+    if (w + 1 > 8192 && 32ull * C < T) return 0;
+    unsigned int best_g = 1;
+    double best = 1e300;
+    for (unsigned int G = 1; G <= 32 && G <= w + 1; G <<= 1) {
+        const double cost = (double)((C * G + T - 1) / T) * ((double)(w + G - 1) / G + kCliqueSetCost);
+        if (cost < best) {
+            best = cost;
+            best_g = G;
+        }
+    }
+    return best_g;
 }
 
 template <int G>
