@@ -19,7 +19,12 @@
  *   tie-break    = among equal costs the split with the numerically smaller
  *                  min(L, R) bitmask wins (R7); costs compare exactly
  *   counters     = csg_count incl. singletons (R1), unordered ccp_pairs (R2),
- *                  pairs_evaluated = sum over blocks (2^(b-1) - 1) (R3)
+ *                  pairs_evaluated = sum over blocks (2^(b-1) - 1) (R3).
+ *                  Counter convention: UNORDERED join pairs ({A,B} counted
+ *                  once); the ordered convention of SPEC ("including the
+ *                  symmetric ones") is exactly 2x ccp_pairs and 2x
+ *                  pairs_evaluated.  Every pairs/s figure uses the unordered
+ *                  count.
  *
  * Threading: a context is used by one host thread at a time.  All pointers
  * passed in are borrowed for the duration of the call and never retained.
@@ -33,7 +38,12 @@ extern "C" {
 #endif
 
 #define MPDP_ABI_VERSION 1
-#define MPDP_MAX_RELATIONS_EXACT 56   /* exact algorithms: n <= 56 (unranking bound) */
+/* exact algorithms: n <= 56.  SURVEY §8(b) asks for 64; the bound is the
+ * 57 x 57 u64 binomial table staged per query (colex unranking of 64-bit masks)
+ * and it is not binding in practice: a connected query with n > 40 only fits
+ * the memo when it is sparse (the open-addressing memo holds its csg).        */
+#define MPDP_MAX_RELATIONS_EXACT 56
+#define MPDP_MAX_RELATIONS_HEURISTIC 16384  /* IDP2 / UnionDP drivers (O(n^2) host work) */
 
 typedef enum {
     MPDP_OK = 0,
@@ -49,8 +59,11 @@ typedef enum {
 } mpdp_status;
 
 typedef enum {
-    MPDP_ALGO_DPSIZE_REF = 0,      /* the CPU reference: NOT in this library (it is
-                                      the test oracle, oracle/liboracle.so) ->
+    MPDP_ALGO_DPSIZE_REF = 0,      /* the CPU reference: NOT in this library, by
+                                      design and final.  The reference DP is the
+                                      test oracle (oracle/liboracle.so), which the
+                                      product may never link or call, so this value
+                                      is reserved and always returns
                                       MPDP_ERR_UNSUPPORTED                          */
     MPDP_ALGO_MPDP = 1,            /* exact MPDP on the GPU                        */
     MPDP_ALGO_IDP2_MPDP = 2,       /* IDP2 with MPDP inner DP, bound k */
@@ -190,7 +203,8 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* ctx);
 /* Optimise one query end to end: validate, copy the graph host->device, run
  * every level, extract the plan on the device and copy the result back.
  * Blocks until the result is in *out.
- *   algo MPDP: k must be 0.  IDP2_MPDP / UNIONDP_MPDP: 2 <= k <= 25.
+ *   algo MPDP: k must be 0.  IDP2_MPDP / UNIONDP_MPDP: 2 <= k <= 32 (the
+ *   paper uses 15 and 25).
  * Errors: INVALID_ARGUMENT (NULL pointers, n == 0, u >= v, v >= n, duplicate
  * edge, selectivity outside (0,1], cardinality < 0 or non-finite, negative or
  * non-finite leaf cost, out->capacity < 2n-1 with out->nodes != NULL, sum of
@@ -208,7 +222,9 @@ mpdp_status mpdp_optimize(mpdp_ctx* ctx, const mpdp_query_graph* graph, mpdp_alg
  * caller-owned, capacity >= 2n-1); batched results report the launch's device
  * time.  Errors: as mpdp_optimize (the first one is returned; results of the
  * queries before it are valid).  Not for world > 1 contexts' sharded queries
- * (those run one by one).                                                       */
+ * (those run one by one).  A batch replaces any query staged by mpdp_stage:
+ * mpdp_run / mpdp_fetch after it fail with INVALID_ARGUMENT until the next
+ * mpdp_stage.                                                                   */
 mpdp_status mpdp_optimize_batch(mpdp_ctx* ctx, const mpdp_query_graph* graphs, uint32_t count,
                                 mpdp_result* results);
 
@@ -222,8 +238,8 @@ mpdp_status mpdp_run(mpdp_ctx* ctx);
 mpdp_status mpdp_fetch(mpdp_ctx* ctx, mpdp_result* out);
 
 /* ---- IDP2 / UnionDP (algo IDP2_MPDP / UNIONDP_MPDP) ------------
- * Heuristic plans for large queries (n up to 2^20; plan node `set` masks are
- * only filled when n <= 64).  The driver repeatedly solves sub-problems of at
+ * Heuristic plans for large queries (n <= MPDP_MAX_RELATIONS_HEURISTIC, else
+ * CAPACITY; plan node `set` masks are only filled when n <= 64).  The driver repeatedly solves sub-problems of at
  * most k relations exactly with the GPU MPDP (composite nodes carry
  * card = card of their subplan and leaf_cost = its cost).  result: the final
  * plan, its C_out cost recomputed over the whole tree, the counters summed over
@@ -253,6 +269,20 @@ int mpdp_abi_version(void);
 /* Debug: phase timestamps of CTA 0 of the last fused run (builds with
  * -DMPDP_TRACE; otherwise returns 0).  Entry = ns << 8 | level << 3 | phase. */
 int mpdp_debug_trace(const mpdp_ctx* ctx, unsigned long long* out, int cap);
+
+/* Debug: per subset size k (index k of caller-owned arrays of `cap` doubles)
+ * of the last single-GPU whole-query run: when level k started and (dataflow
+ * kernels k_dp_star / k_dp_clique) when its last chunk finished, in
+ * microseconds after the first level start; 0 = not recorded.  Returns the
+ * number of entries written (n + 2, at most cap). */
+int mpdp_debug_level_span(const mpdp_ctx* ctx, double* start_us, double* done_us, int cap);
+
+/* Debug: with the environment variable MPDP_DEBUG_DF_STATS set while the last
+ * query ran on a dataflow kernel (k_dp_star / k_dp_clique), copies up to cap
+ * words: per CTA 8 words {control warp: ns waiting for a free slot, ns waiting
+ * for dependencies, ns in its loop, chunks; compute warp 0: ns waiting for a
+ * chunk, ns in its loop, 0, 0}.  Returns the number of words (0 otherwise). */
+int mpdp_debug_df_stats(const mpdp_ctx* ctx, unsigned long long* out, int cap);
 
 /* Multi-GPU bootstrap: 128-byte NCCL unique id (call on rank 0 only). */
 mpdp_status mpdp_nccl_get_unique_id(void* out128);

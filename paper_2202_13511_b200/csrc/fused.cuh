@@ -13,6 +13,7 @@
 // at the end.  One launch per query instead of 2-3 per level.
 #pragma once
 #include "level_kernels.cuh"
+#include "dataflow.cuh"
 
 namespace mpdp {
 
@@ -47,16 +48,23 @@ __device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int& nbar,
         nbar++;
         const unsigned int target = nbar * gridDim.x;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        if (ld_acquire_u32(bar) < target) {
-            const unsigned long long t0 = globaltimer_ns();
-            while (ld_acquire_u32(bar) < target) {
-                __nanosleep(20);
-                if (watchdog_expired(t0)) {   // never hang the device: flag and fall through
+        // poll with relaxed loads (an acquire load invalidates the SM's L1 on
+        // every poll, under co-resident warps that use it for memo probes),
+        // then one acquire fence; the watchdog clock is read every 1024 polls
+        unsigned int spins = 0;
+        unsigned long long t0 = 0;
+        while (ld_relaxed_u32(bar) < target) {
+            __nanosleep(20);
+            if ((++spins & 1023u) == 0) {
+                if (!t0) {
+                    t0 = globaltimer_ns();
+                } else if (watchdog_expired(t0)) {   // never hang the device: flag and fall through
                     atomicOr(err, ERR_HANG);
                     break;
                 }
             }
         }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
 }
@@ -322,26 +330,31 @@ __device__ void small_phase(const Params<uint32_t>& p, int k, const SQ<uint32_t>
 // its join pairs are j = 0 .. w-1 with w = 2^(k-1) - 1:
 //     A_j = lowbit(S) | deposit(j, S \ lowbit(S)),   B_j = S \ A_j
 // (Alg. mpdp_generalization P:545-568 with one block and no CCP checks).
-// The level's pair space [0, C(n,k) * w) is cut into one contiguous chunk per
-// warp (>= 512 pairs), lanes interleaved over j so that a warp's probes fall
-// into few memo lines -- no enumeration, compaction, look-back or heavy list.
-// A set cut by chunk boundaries is merged from per-chunk partial keys: a pair
-// count on the slot of the first chunk that touches it elects the last
-// contributor, which reduces the partials and scatters; the count slots
-// alternate between two buffers by level parity and each warp clears its slot
-// of the next level's buffer.  Sets with fewer than 32
-// pairs (k <= 5) take G = 2^(k-1) lanes each, one pair per lane.
+// No enumeration, compaction, look-back or heavy list.  Two ways to cut a
+// level (clique_group picks one from a cost model of the level's rounds):
+//  * group path (most levels): whole sets per group of G = 1..32 lanes, G
+//    minimising rounds x (pairs per lane + per-set overhead); lanes take
+//    interleaved j so a group's probes fall into few memo lines;
+//  * split path (levels of fewer sets than warps whose sets exceed 8192
+//    pairs): the pair space [0, C(n,k) * w) is cut into one contiguous chunk
+//    per warp (>= 512 pairs).  A set cut by chunk boundaries is merged from
+//    per-chunk partial keys: a pair count on the slot of the first chunk that
+//    touches it elects the last contributor, which reduces the partials and
+//    scatters; the count slots alternate between two buffers by level parity
+//    and each warp clears its slot of the next level's buffer.
 // Memo entries of level 1 (leaf cost, card) are written at k = 2, so probes
 // of levels >= 3 are branch-free loads.
 template <int G>
 __device__ __forceinline__ void clique_eval_span(const SQ<uint32_t>& q, const double* __restrict__ dcost, uint32_t S,
                                                  uint32_t lo, uint32_t R, uint32_t DG, uint32_t sub,
-                                                 unsigned int j, unsigned int b, double cS, bool leaves, Key& best) {
+                                                 unsigned int j, unsigned int b, double cS, bool leaves, Key& best,
+                                                 unsigned long long& npairs) {
     // pairs j, j + G, j + 2G, ... of the set (w < 2^31 pairs); 4 pairs (8
     // probes) in flight; the min in f64 / u32 registers (costs are >= 0, so
-    // the f64 order is the bit order of the Key)
+    // the f64 order is the bit order of the Key); every evaluated pair counted
     double bc = __longlong_as_double((long long)best.c);
     uint32_t bl = (uint32_t)best.l;
+    unsigned int cnt = 0;
     for (; j < b; j += 4 * G) {
         uint32_t A[4];
         double ca[4], cb[4];
@@ -363,11 +376,14 @@ __device__ __forceinline__ void clique_eval_span(const SQ<uint32_t>& q, const do
         for (int u = 0; u < 4; u++) {
             const double c = __dadd_rn(__dadd_rn(ca[u], cb[u]), cS);
             const uint32_t B = S ^ A[u], l = A[u] < B ? A[u] : B;
-            const bool better = j + G * u < b && (c < bc || (c == bc && l < bl));
+            const bool ok = j + G * u < b;
+            const bool better = ok && (c < bc || (c == bc && l < bl));
             bc = better ? c : bc;
             bl = better ? l : bl;
+            cnt += ok;
         }
     }
+    npairs += cnt;
     if (bl != 0xffffffffu) best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
 }
 
@@ -391,7 +407,6 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
     P.dcard[S] = cS;
 }
 
-// lanes per set of w pairs: the power of two nearest (w + 1) / 8, 1..32
 // Lanes per set for the whole-set group path.  A level of C sets of w pairs
 // on T threads with G lanes per set takes ceil(C * G / T) rounds of w / G pairs
 // per lane plus a per-set overhead (unrank, card, group min, scatter) worth
@@ -400,13 +415,13 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 // amortise the per-set work and keep a lane's consecutive pairs in nearby memo
 // lines; more lanes fill the grid and shorten the level's last round.
 // Returns 0 (pair chunks per warp, the split path) for levels of fewer sets
-// than warps whose sets exceed 8192 pairs.  Measured (clique-18 / 16 / 20):
-// fixed ~8 pairs per lane 1.04 / 0.27 / 7.5 ms; <= 256 pairs per lane widened
-// to half the threads 0.72 / 0.28 / 4.9 ms; this model (cost 64) 0.66 / 0.29 /
-// 3.9 ms (cost 32: 0.77 / 0.29 / 4.0; cost 128: 0.66 / 0.29 / 3.9).
+// than warps whose sets exceed 8192 pairs.  Measured (round 1, level barrier;
+// clique-18 / 16 / 20): fixed ~8 pairs per lane 1.04 / 0.27 / 7.5 ms; <= 256
+// pairs per lane widened to half the threads 0.72 / 0.28 / 4.9 ms; this model
+// (cost 64) 0.66 / 0.29 / 3.9 ms (cost 32: 0.77 / 0.29 / 4.0; cost 128: 0.66 /
+// 0.29 / 3.9).  Host and device share it (the host plans the dataflow chunks).
 constexpr double kCliqueSetCost = 64.0;
-__device__ __forceinline__ unsigned int clique_group(unsigned long long w, unsigned long long C,
-                                                     unsigned long long T) {
+__host__ __device__ inline unsigned int clique_group(unsigned long long w, unsigned long long C, unsigned long long T) {
     if (w + 1 > 8192 && 32ull * C < T) return 0;
     unsigned int best_g = 1;
     double best = 1e300;
@@ -420,82 +435,59 @@ __device__ __forceinline__ unsigned int clique_group(unsigned long long w, unsig
     return best_g;
 }
 
+// Group path, one chunk: sets [lo, hi) of clique level k on the CTA's compute
+// threads, G lanes per set, group-consecutive sets (the warp's groups work on
+// colex neighbours, whose probes share lines).
 template <int G>
-__device__ void clique_groups(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
-                              const unsigned int* bin, unsigned int C, unsigned long long w,
-                              unsigned long long probes_per_set, bool leaves, unsigned long long& pairs,
-                              unsigned long long& nccp, unsigned long long& nprobe, unsigned long long& nsets) {
+__device__ void clique_group_chunk(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                                   const unsigned int* bin, unsigned int lo, unsigned int hi,
+                                   unsigned long long& npairs, unsigned long long& nsets) {
     constexpr int MEMO = MEMO_MASK;
-    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const unsigned long long ngroups = nthreads / G, grp = gtid / G;
-    const unsigned int sub = threadIdx.x & (G - 1);
-    // group-consecutive sets (h = it * ngroups + grp), each one unranked: the
-    // warp's groups work on colex neighbours, whose probes share lines
-    // (per-group Gosper runs: clique-16 316 vs 291 us)
-    const unsigned long long rounds = (C + ngroups - 1) / ngroups;
-    uint32_t S = 0;
-    for (unsigned long long it = 0; it < rounds; it++) {
-        const unsigned long long h = it * ngroups + grp;
-        const bool act = h < C;
-        if (act) S = unrank_colex32(bin, q.n, k, (unsigned int)h);
+    constexpr unsigned int NG = kDfCompute / G;
+    const unsigned int w = (1u << (k - 1)) - 1u;
+    const bool leaves = k == 2;
+    const unsigned int grp = threadIdx.x / G, sub = threadIdx.x & (G - 1);
+    for (unsigned int h0 = lo; h0 < hi; h0 += NG) {           // uniform trip count
+        const unsigned int h = h0 + grp;
+        const bool act = h < hi;
         Key best = key_inf();
         double cS = 0.0;
+        uint32_t S = 0;
         if (act) {
-            cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, (unsigned int)h);
-            const uint32_t lo = S & (0u - S), R = S ^ lo;
-            clique_eval_span<G>(q, p.memo.dcost, S, lo, R, deposit_small(G, R), deposit_small(sub, R), sub,
-                                (unsigned int)w, cS, leaves, best);
+            S = unrank_colex32(bin, q.n, k, h);
+            cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, h);
+            const uint32_t lo1 = S & (0u - S), R = S ^ lo1;
+            clique_eval_span<G>(q, p.memo.dcost, S, lo1, R, deposit_small(G, R), deposit_small(sub, R), sub, w, cS,
+                                leaves, best, npairs);
         }
         best = group_min(best, G);
         if (act && sub == 0) {
             clique_write(p.memo, S, best, cS);
-            pairs += w;
-            nccp += w;
-            nprobe += probes_per_set;
             nsets++;
         }
     }
 }
 
-__device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
-                             const unsigned int* bin, unsigned long long& pairs, unsigned long long& nccp,
-                             unsigned long long& nprobe, unsigned long long& nsets) {
+// Split path, one warp chunk c of level k: pairs [c * csize, (c+1) * csize) of
+// the level's pair space C(n,k) * w.  A set cut by chunk boundaries is merged
+// from per-chunk partial keys: a pair count on the slot of the first chunk
+// that touches it elects the last contributor, which reduces the partials
+// with its warp, scatters, and publishes the set (dataflow.cuh) -- no
+// contended 128-bit CAS (clique-18 k = 18: ~100 chunks meet on one set).
+// Merge slots: key_first / key_last / count per chunk of this level, from
+// slot0 on (counts zeroed by the previous launch's last CTA or k_init).
+__device__ void clique_split_chunk(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                                   const unsigned int* bin, const DfLevel& L, unsigned int c,
+                                   unsigned long long& npairs, unsigned long long& nsets) {
     constexpr int MEMO = MEMO_MASK;
     const int n = q.n;
-    const unsigned int C = bin[n * 33 + k];
-    const unsigned long long w = (1ull << (k - 1)) - 1;
-    const unsigned long long probes_per_set = k >= 3 ? 2 * w - (unsigned long long)k : 0ull;
     const unsigned int lane = threadIdx.x & 31;
-    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const unsigned long long nwarps = nthreads >> 5, gw = gtid >> 5;
-    Key* key_first = p.bkey;               // per chunk: key of its first / last set segment
-    Key* key_last = p.bkey + nwarps;
-    unsigned long long* slot_done = p.bdone + (k & 1) * nwarps;
-    if (lane == 0) p.bdone[((k + 1) & 1) * nwarps + gw] = 0;   // this warp's counter slot of level k+1
-    const bool leaves = k == 2;
-    if (leaves && gtid < (unsigned long long)n) {      // level-1 entries
-        p.memo.dcost[1u << gtid] = q.leaf[gtid];
-        p.memo.dcard[1u << gtid] = q.card[gtid];
-    }
-    // whole sets per group of G lanes (clique_group), or pair chunks per warp
-    const unsigned int G = clique_group(w, C, nthreads);
-    if (G) {
-        switch (G) {
-            case 1: clique_groups<1>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-            case 2: clique_groups<2>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-            case 4: clique_groups<4>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-            case 8: clique_groups<8>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-            case 16: clique_groups<16>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-            default: clique_groups<32>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
-        }
-        return;
-    }
-    const unsigned long long P = (unsigned long long)C * w;
-    unsigned long long csize = (P + nwarps - 1) / nwarps;
-    if (csize < 512) csize = 512;        // (1024: clique-16 291 vs 278 us)
-    const unsigned long long c0 = gw * csize;
+    const unsigned long long w = (1ull << (k - 1)) - 1;
+    const unsigned long long P = (unsigned long long)bin[n * 33 + k] * w, csize = L.chunk;
+    Key* key_first = p.bkey + 2ull * L.slot0;
+    Key* key_last = key_first + L.nslot;
+    unsigned long long* slot_done = p.bdone + L.slot0;
+    const unsigned long long c0 = (unsigned long long)c * csize;
     if (c0 >= P) return;
     const unsigned long long c1 = c0 + csize < P ? c0 + csize : P;
     unsigned long long h = c0 / w, a = c0 - h * w;
@@ -511,29 +503,18 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         const uint32_t sub = ((da | ~R) + deposit_small(lane, R)) & R;
         Key best = key_inf();
         clique_eval_span<32>(q, p.memo.dcost, S, lo, R, D32, sub, (unsigned int)(a + lane), (unsigned int)b, cS, false,
-                             best);
+                             best, npairs);
         best = warp_min(best);
-        if (lane == 0) {
-            pairs += b - a;
-            nccp += b - a;
-        }
+        bool wrote = false;
         if (a == 0 && b == w) {
-            if (lane == 0) {
-                clique_write(p.memo, S, best, cS);
-                nprobe += probes_per_set;
-                nsets++;
-            }
+            if (lane == 0) clique_write(p.memo, S, best, cS);
+            wrote = true;
         } else {
-            // split set: this chunk's partial key goes to its first / last
-            // segment slot (plain stores); the pair count on the slot of the
-            // first chunk touching the set elects the last contributor, which
-            // reduces the partial keys of all chunks of the set with its warp
-            // (no contended 128-bit CAS: 128 chunks meet at clique-18 k = 18)
             const bool is_first = h == c0 / w, is_last = hw + b >= c1;
             unsigned int last = 0;
             if (lane == 0) {
-                if (is_first) key_first[gw] = best;
-                if (is_last) key_last[gw] = best;
+                if (is_first) key_first[c] = best;
+                if (is_last) key_last[c] = best;
                 __threadfence();
                 const unsigned long long old = atomicAdd(&slot_done[hw / csize], b - a);
                 last = old + (b - a) == w;
@@ -543,17 +524,19 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
                 const unsigned long long cf = hw / csize, cl = (hw + w - 1) / csize;
                 Key m = key_inf();
                 if (lane == 0) m = ld_key(&key_last[cf]);
-                for (unsigned long long c = cf + 1 + lane; c <= cl; c += 32) {
-                    const Key t = ld_key(&key_first[c]);
+                for (unsigned long long x = cf + 1 + lane; x <= cl; x += 32) {
+                    const Key t = ld_key(&key_first[x]);
                     if (key_less(t, m)) m = t;
                 }
                 m = warp_min(m);
-                if (lane == 0) {
-                    clique_write(p.memo, S, m, cS);
-                    nprobe += probes_per_set;
-                    nsets++;
-                }
+                if (lane == 0) clique_write(p.memo, S, m, cS);
+                wrote = true;
             }
+        }
+        if (wrote && lane == 0) {          // publish the finished set (release: fence + add)
+            nsets++;
+            __threadfence();
+            df_red_add(&p.df->done[k][31 - __clz(S)], 1u);
         }
         if (hw + b >= c1) break;
         h++;
@@ -859,12 +842,299 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     }
 }
 
+template <int G>
+__device__ void clique_groups(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                              const unsigned int* bin, unsigned int C, unsigned long long w,
+                              unsigned long long probes_per_set, bool leaves, unsigned long long& pairs,
+                              unsigned long long& nccp, unsigned long long& nprobe, unsigned long long& nsets) {
+    constexpr int MEMO = MEMO_MASK;
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long ngroups = nthreads / G, grp = gtid / G;
+    const unsigned int sub = threadIdx.x & (G - 1);
+    // group-consecutive sets (h = it * ngroups + grp), each one unranked: the
+    // warp's groups work on colex neighbours, whose probes share lines
+    // (per-group Gosper runs: clique-16 316 vs 291 us)
+    const unsigned long long rounds = (C + ngroups - 1) / ngroups;
+    uint32_t S = 0;
+    for (unsigned long long it = 0; it < rounds; it++) {
+        const unsigned long long h = it * ngroups + grp;
+        const bool act = h < C;
+        if (act) S = unrank_colex32(bin, q.n, k, (unsigned int)h);
+        Key best = key_inf();
+        double cS = 0.0;
+        if (act) {
+            cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, (unsigned int)h);
+            const uint32_t lo = S & (0u - S), R = S ^ lo;
+            clique_eval_span<G>(q, p.memo.dcost, S, lo, R, deposit_small(G, R), deposit_small(sub, R), sub,
+                                (unsigned int)w, cS, leaves, best, pairs);
+        }
+        best = group_min(best, G);
+        if (act && sub == 0) {
+            clique_write(p.memo, S, best, cS);
+            nprobe += probes_per_set;
+            nsets++;
+        }
+    }
+}
+
+__device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
+                             const unsigned int* bin, unsigned long long& pairs, unsigned long long& nccp,
+                             unsigned long long& nprobe, unsigned long long& nsets) {
+    constexpr int MEMO = MEMO_MASK;
+    const int n = q.n;
+    const unsigned int C = bin[n * 33 + k];
+    const unsigned long long w = (1ull << (k - 1)) - 1;
+    const unsigned long long probes_per_set = k >= 3 ? 2 * w - (unsigned long long)k : 0ull;
+    const unsigned int lane = threadIdx.x & 31;
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long nwarps = nthreads >> 5, gw = gtid >> 5;
+    Key* key_first = p.bkey;               // per chunk: key of its first / last set segment
+    Key* key_last = p.bkey + nwarps;
+    unsigned long long* slot_done = p.bdone + (k & 1) * nwarps;
+    if (lane == 0) p.bdone[((k + 1) & 1) * nwarps + gw] = 0;   // this warp's counter slot of level k+1
+    const bool leaves = k == 2;
+    if (leaves && gtid < (unsigned long long)n) {      // level-1 entries
+        p.memo.dcost[1u << gtid] = q.leaf[gtid];
+        p.memo.dcard[1u << gtid] = q.card[gtid];
+    }
+    // whole sets per group of G lanes (clique_group), or pair chunks per warp
+    const unsigned int G = clique_group(w, C, nthreads);
+    (void)nccp;                            // every evaluated pair is a ccp (Lemma 8): counted as pairs
+    if (G) {
+        switch (G) {
+            case 1: clique_groups<1>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 2: clique_groups<2>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 4: clique_groups<4>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 8: clique_groups<8>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            case 16: clique_groups<16>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+            default: clique_groups<32>(p, k, q, v, bin, C, w, probes_per_set, leaves, pairs, nccp, nprobe, nsets); break;
+        }
+        return;
+    }
+    const unsigned long long P = (unsigned long long)C * w;
+    unsigned long long csize = (P + nwarps - 1) / nwarps;
+    if (csize < 512) csize = 512;        // (1024: clique-16 291 vs 278 us)
+    const unsigned long long c0 = gw * csize;
+    if (c0 >= P) return;
+    const unsigned long long c1 = c0 + csize < P ? c0 + csize : P;
+    unsigned long long h = c0 / w, a = c0 - h * w;
+    uint32_t S = unrank_colex32(bin, n, k, (unsigned int)h);
+    while (true) {
+        const unsigned long long hw = h * w;
+        const unsigned long long b = c1 - hw < w ? c1 - hw : w;
+        const double cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, (unsigned int)h);
+        const uint32_t lo = S & (0u - S), R = S ^ lo;
+        const uint32_t D32 = deposit_small(32, R);
+        // deposit(a + lane) = deposit(a) (+) deposit(lane) in R's domain
+        const uint32_t da = a ? deposit<uint32_t>(a, R) : 0u;
+        const uint32_t sub = ((da | ~R) + deposit_small(lane, R)) & R;
+        Key best = key_inf();
+        clique_eval_span<32>(q, p.memo.dcost, S, lo, R, D32, sub, (unsigned int)(a + lane), (unsigned int)b, cS, false,
+                             best, pairs);
+        best = warp_min(best);
+        if (a == 0 && b == w) {
+            if (lane == 0) {
+                clique_write(p.memo, S, best, cS);
+                nprobe += probes_per_set;
+                nsets++;
+            }
+        } else {
+            // split set: this chunk's partial key goes to its first / last
+            // segment slot (plain stores); the pair count on the slot of the
+            // first chunk touching the set elects the last contributor, which
+            // reduces the partial keys of all chunks of the set with its warp
+            // (no contended 128-bit CAS: 128 chunks meet at clique-18 k = 18)
+            const bool is_first = h == c0 / w, is_last = hw + b >= c1;
+            unsigned int last = 0;
+            if (lane == 0) {
+                if (is_first) key_first[gw] = best;
+                if (is_last) key_last[gw] = best;
+                __threadfence();
+                const unsigned long long old = atomicAdd(&slot_done[hw / csize], b - a);
+                last = old + (b - a) == w;
+            }
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+                __threadfence();
+                const unsigned long long cf = hw / csize, cl = (hw + w - 1) / csize;
+                Key m = key_inf();
+                if (lane == 0) m = ld_key(&key_last[cf]);
+                for (unsigned long long c = cf + 1 + lane; c <= cl; c += 32) {
+                    const Key t = ld_key(&key_first[c]);
+                    if (key_less(t, m)) m = t;
+                }
+                m = warp_min(m);
+                if (lane == 0) {
+                    clique_write(p.memo, S, m, cS);
+                    nprobe += probes_per_set;
+                    nsets++;
+                }
+            }
+        }
+        if (hw + b >= c1) break;
+        h++;
+        a = 0;
+        S = gosper(S);
+    }
+}
+
+
+// Dataflow variant of the clique kernel (ablation, MPDP_DEBUG_CLIQUE_DF):
+// levels as dataflow chunks (dataflow.cuh): group levels hand whole sets to groups of G lanes,
+// split levels hand warp chunks of one level's pair space; the first small
+// levels run as one solo chunk.  A chunk of level k needs level k-1 up to the
+// largest element of its last set.  Plan extraction by the last CTA out.
+constexpr int kCliqueMinBlocks = 3;
+__host__ __device__ constexpr size_t clique_smem_bytes() { return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33; }
+
+struct CliqueSched {
+    const Params<uint32_t>& p;
+    const unsigned int* bin;
+    __device__ unsigned int total() const { return p.dfl[p.k_end + 1].base; }
+    __device__ void locate(unsigned int t, DfSlot& d) const {
+        int k = p.k_begin;
+        while (t >= p.dfl[k + 1].base) k++;
+        const DfLevel& L = p.dfl[k];
+        d.t = t;
+        d.k = k;
+        d.k2 = L.solo > k ? L.solo : k;
+        if (L.split) {                                  // warp chunks [lo, hi) of the level
+            d.lo = (t - L.base) * (kDfCompute / 32);
+            d.hi = min(d.lo + kDfCompute / 32, L.nslot);
+        } else {
+            d.lo = p.share_lo[k] + (t - L.base) * L.chunk;
+            d.hi = min(d.lo + L.chunk, p.share_hi[k]);
+        }
+    }
+    // largest element of the last set the chunk touches
+    __device__ unsigned int last_set(const DfSlot& d) const {
+        const DfLevel& L = p.dfl[d.k];
+        if (!L.split) return d.hi - 1;
+        const unsigned long long w = (1ull << (d.k - 1)) - 1;
+        const unsigned long long P = (unsigned long long)bin[p.n * 33 + d.k] * w;
+        const unsigned long long e = min((unsigned long long)d.hi * L.chunk, P);
+        return (unsigned int)((e - 1) / w);
+    }
+    __device__ int need(const DfSlot& d) const {
+        return (d.k >= 3 && d.k - 1 >= p.k_begin) ? colex_top(bin, d.k, last_set(d)) : -1;
+    }
+    // sets of level k1 whose largest element is j
+    __device__ unsigned int need_count(int k1, int j) const { return bin[j * 33 + k1 - 1]; }
+    __device__ void publish(const DfSlot& d) const {
+        if (p.dfl[d.k].split) return;                   // split sets are published by their last contributor
+        df_publish_colex(p, bin, d.k, d.k, d.lo, d.hi);
+        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex(p, bin, k, k, p.share_lo[k], p.share_hi[k]);
+    }
+};
+
+__device__ __noinline__ void clique_extract(const Params<uint32_t>& p, const SQ<uint32_t>& q, const MemoView& v,
+                                            const unsigned int* bin) {
+    if (threadIdx.x == 0) p.result->t_level[p.n + 1] = globaltimer_ns();
+    level_counters_warp(p, p.result);
+    if (threadIdx.x == 0) {
+        if (ld_relaxed_u32(&p.df->error)) {
+            p.result->n_nodes = 0;
+        } else {
+            p.result->error = 0;
+            extract_phase<uint32_t, MEMO_MASK>(p, q, v, bin, p.q->gen);
+        }
+        atomicMax(&p.df->t_done[p.n + 1], globaltimer_ns());
+    }
+}
+
+__global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(const __grid_constant__ Params<uint32_t> p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
+    unsigned int* bin = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));   // 33 x 33
+    __shared__ MemoView v;
+    __shared__ DfCounters sc;
+    __shared__ DfShared sh;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[0] = globaltimer_ns();   // kernel start
+    load_query(q, p.q);
+    for (int j = threadIdx.x; j <= kMaxN; j += blockDim.x) {
+        v.off[j] = 0;
+        v.nb[j] = 0;
+        sh.ready[j] = j < p.k_begin ? 64 : -1;
+    }
+    for (int i = threadIdx.x; i < (kMaxN + 1) * 3; i += blockDim.x) (&sc.v[0][0])[i] = 0;
+    if (threadIdx.x < kDfSlots) sh.done[threadIdx.x] = 0;
+    constexpr int NB = MaxN<uint32_t>::value + 1;
+    for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
+        const int a = i / 33, b = i % 33;
+        bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
+    }
+    // level-1 entries (leaf cost, card), written by every CTA before its first
+    // chunk: the same values everywhere, and a CTA's own later probes are
+    // ordered after its own writes
+    __syncthreads();
+    for (int u = threadIdx.x; u < q.n; u += blockDim.x) {
+        p.memo.dcost[1u << u] = q.leaf[u];
+        p.memo.dcard[1u << u] = q.card[u];
+    }
+    __syncthreads();
+    if (threadIdx.x >= kDfCompute) {
+        df_control(p, CliqueSched{p, bin}, sh);
+    } else {
+        int kc = p.k_begin;
+        unsigned long long npairs = 0, nsets = 0;      // this thread, level kc
+        auto flush = [&]() {
+            // probes of non-singleton sides: 2w - k per set of a level >= 3
+            const unsigned long long wk = (1ull << (kc - 1)) - 1;
+            df_count(sc, kc, npairs, kc >= 3 ? nsets * (2 * wk - (unsigned long long)kc) : 0ull, nsets);
+            npairs = nsets = 0;
+        };
+        DfSlot d;
+        unsigned long long st_take = 0;
+        const unsigned long long st0 = p.df_stats ? globaltimer_ns() : 0ull;
+        unsigned long long* stp = (p.df_stats && threadIdx.x == 0) ? &st_take : nullptr;
+        for (unsigned int i = 0; df_take(sh, i, d, stp); i++) {
+            for (int k = d.k; k <= d.k2; k++) {
+                if (k != kc) {
+                    flush();
+                    kc = k;
+                }
+                if (k > d.k) {
+                    asm volatile("bar.sync 3, %0;" ::"r"(kDfCompute) : "memory");
+                    if (threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+                }
+                const DfLevel& L = p.dfl[k];
+                if (L.split) {
+                    const unsigned int c = d.lo + (threadIdx.x >> 5);
+                    if (c < d.hi) clique_split_chunk(p, k, q, v, bin, L, c, npairs, nsets);
+                    continue;
+                }
+                const unsigned int lo = k == d.k ? d.lo : p.share_lo[k], hi = k == d.k ? d.hi : p.share_hi[k];
+                switch (L.G) {
+                    case 1: clique_group_chunk<1>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                    case 2: clique_group_chunk<2>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                    case 4: clique_group_chunk<4>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                    case 8: clique_group_chunk<8>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                    case 16: clique_group_chunk<16>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                    default: clique_group_chunk<32>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                }
+            }
+            df_finish(sh, i);
+        }
+        if (stp) {
+            p.df_stats[8ull * blockIdx.x + 4] = st_take;
+            p.df_stats[8ull * blockIdx.x + 5] = globaltimer_ns() - st0;
+        }
+        flush();
+    }
+    if (!df_exit(p, sc)) return;
+    if (p.do_extract && threadIdx.x < 32) clique_extract(p, q, v, bin);
+    df_reset(p);
+}
+
 // Whole-query kernel for cliques with the bitmask memo: clique_level per level
 // (one phase, one grid barrier), then the extraction.  A kernel of its own so
 // its register budget (and so its occupancy: kCliqueMinBlocks CTAs per SM) is
-// not set by the tile machinery of k_dp_fused.
-constexpr int kCliqueMinBlocks = 3;
-__host__ __device__ constexpr size_t clique_smem_bytes() { return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33; }
+// not set by the tile machinery of k_dp_fused.  The level barrier stays here:
+// the dataflow variant (k_dp_clique_df) measured slower on cliques -- 72% of
+// clique-18's level k+1 needs ALL of level k (every set with the largest
+// element), so only the short colex prefix can overlap a level's tail, and
+// the per-chunk handover costs more than the barrier saves.
 
 __global__ void __launch_bounds__(kBlock, kCliqueMinBlocks) k_dp_clique(const __grid_constant__ Params<uint32_t> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -882,15 +1152,27 @@ __global__ void __launch_bounds__(kBlock, kCliqueMinBlocks) k_dp_clique(const __
         bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
     }
     unsigned int nbar = 0;
+    __shared__ unsigned int s_abort;
+    const unsigned long long t_start = globaltimer_ns();
     __syncthreads();
     for (int k = p.k_begin; k <= p.k_end; k++) {
         if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
         unsigned long long pairs = 0, nccp = 0, nprobe = 0, nsets = 0;
         clique_level(p, k, q, v, bin, pairs, nccp, nprobe, nsets);
         if ((p.count_levels >> k) & 1ull) {
-            flush_counters(&p.desc[k], pairs, nccp, nprobe, nsets);
+            flush_counters(&p.desc[k], pairs, pairs, nprobe, nsets);   // (pairs evaluated = ccp, Lemma 8)
         }
+        // device deadline: a CTA past it raises the abort flag before
+        // the barrier; after the barrier every CTA reads the same flag
+        if (threadIdx.x == 0 && p.timeout_ns && globaltimer_ns() - t_start > p.timeout_ns)
+            atomicExch(&p.df->abort, 1u);
         grid_sync(p.gbar, nbar, &p.result->error);
+        if (threadIdx.x == 0) s_abort = ld_relaxed_u32(&p.df->abort);
+        __syncthreads();
+        if (s_abort) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&p.result->error, ERR_TIMEOUT);
+            return;
+        }
     }
     if (p.do_extract && blockIdx.x == 0 && threadIdx.x < 32) {
         if (threadIdx.x == 0) p.result->t_level[p.n + 1] = globaltimer_ns();

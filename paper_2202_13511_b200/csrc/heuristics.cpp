@@ -630,6 +630,13 @@ mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolv
         err = "k must be in [2, 32] for IDP2/UnionDP";
         return MPDP_ERR_INVALID_ARGUMENT;
     }
+    // the drivers do O(n) host work per GOO merge / IDP2 iteration (scans of the
+    // components and temp tables), O(n^2) per query: bounded where that is
+    // still milliseconds
+    if (g && g->n > (uint32_t)kMaxHeuristicN) {
+        err = "IDP2/UnionDP drivers support n <= " + std::to_string(kMaxHeuristicN);
+        return MPDP_ERR_CAPACITY;
+    }
     Query Q;
     mpdp_status st = load(g, Q, err);
     if (st != MPDP_OK) return st;

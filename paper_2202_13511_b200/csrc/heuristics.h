@@ -5,6 +5,7 @@
 #include "mpdp.h"
 
 namespace mpdp_heur {
+constexpr int kMaxHeuristicN = MPDP_MAX_RELATIONS_HEURISTIC;
 typedef mpdp_status (*InnerSolver)(void* user, const mpdp_query_graph* sub, mpdp_result* out);
 // optional: `count` independent sub-problems in one call (UnionDP levels)
 typedef mpdp_status (*InnerBatchSolver)(void* user, const mpdp_query_graph* subs, uint32_t count, mpdp_result* outs);

@@ -38,12 +38,41 @@ struct __align__(64) TileRec {            // decoupled look-back record (ring sl
 constexpr int kTraceCap = 512;
 constexpr int kMaxGrid = 2048;            // CTAs of a persistent whole-query kernel
 
+// Barrier-free level scheduling of the closed-form whole-query kernels
+// (k_dp_star, k_dp_clique; dataflow.cuh).  The sets of one level are
+// independent and level k reads only levels < k; in
+// colex order the sets whose largest element is <= m are a prefix of every
+// level, and all subsets of such a set lie in those prefixes.  So a chunk of
+// level k can start as soon as level k-1 is finished up to the largest
+// element of the chunk's last set -- no grid barrier between levels.
+constexpr int kDfMaxElem = 32;
+// Self-resetting: all zero between launches (the workspace is zeroed at
+// context creation and by k_init; the last CTA out of a dataflow launch
+// zeroes it again), so the dataflow kernels need no init launch.
+struct DataflowDev {
+    unsigned int ticket;                   // next chunk of the launch (level-major, colex order)
+    unsigned int exited;                   // CTAs that ran out of chunks (the last one extracts)
+    unsigned int abort;                    // timeout / watchdog: stop claiming and waiting
+    unsigned int error;                    // ERR_* bits, kept until the extracting launch copies them
+    unsigned long long t_done[kMaxN + 2];  // per level: when its last chunk finished (idem)
+    unsigned int done[kMaxN + 1][kDfMaxElem];   // finished sets per (level, largest element)
+};
+struct DfLevel {
+    unsigned int base;                     // first ticket of the level (dfl[k_end + 1].base = total)
+    unsigned int chunk;                    // sets per ticket, or (split) pairs per warp chunk
+    unsigned int slot0;                    // split levels: first merge slot of the level
+    unsigned int nslot;                    // split levels: warp chunks (merge slots) of the level
+    unsigned char G, run, split;           // lanes per set, consecutive sets per group, split mode
+    unsigned char solo;                    // > k: levels k..solo are ONE chunk (small levels, one CTA)
+};
+
 struct ResultDev {
     double cost;
     unsigned long long csg, ccp, pairs, probes;
     unsigned int n_nodes, error;
     unsigned long long lvl_csg[kMaxN + 1], lvl_ccp[kMaxN + 1], lvl_pairs[kMaxN + 1];
     unsigned long long t_level[kMaxN + 2];  // fused kernel: globaltimer at each level start (+ end)
+    unsigned long long t_done[kMaxN + 2];   // dataflow kernels: globaltimer when the level's last chunk finished
     unsigned long long trace[kTraceCap];    // MPDP_TRACE builds: (ns << 8 | level << 3 | phase) of block 0
     mpdp_plan_node nodes[2 * kMaxN - 1];
 };
@@ -82,6 +111,14 @@ template <typename M> struct Params {
     int no_ccc;                            // MPDP_FLAG_NO_CCC: lane-contiguous candidates (ablation)
     int star_hub;                          // k_dp_star: the hub relation
     unsigned long long star_off[kMaxN + 1];   // k_dp_star: first memo entry of level k (C(n-1, k-1) per level)
+    // dataflow scheduling (k_dp_star, k_dp_clique): per level its tickets and
+    // chunk geometry, the shared state, and the timeout (0 = none)
+    DataflowDev* df;
+    DfLevel dfl[kMaxN + 2];
+    unsigned long long timeout_ns;
+    unsigned long long zero_words;         // k_init: bdone[0 .. zero_words) cleared (clique merge counts)
+    int mask_leaves;                       // k_init: level-1 entries of the bitmask memo (cliques)
+    unsigned long long* df_stats;          // debug (MPDP_DEBUG_DF_STATS): per CTA 8 timing words, else null
 };
 
 // ------------------------------------------------------------- mem helpers
@@ -175,8 +212,20 @@ __global__ void k_init(const __grid_constant__ Params<M> p) {
         p.result->error = 0;
         if (p.gbar) p.gbar[0] = 0;         // grid barrier arrival counter of the next launch
     }
-    for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) p.result->t_level[i] = 0;
+    for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) p.result->t_level[i] = p.result->t_done[i] = 0;
     for (int i = threadIdx.x; i < kTraceCap; i += blockDim.x) p.result->trace[i] = 0;
+    if (p.df) {                            // dataflow state of the next launch
+        unsigned int* w = reinterpret_cast<unsigned int*>(p.df);
+        for (unsigned int i = threadIdx.x; i < sizeof(DataflowDev) / 4; i += blockDim.x) w[i] = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) p.result->t_done[0] = globaltimer_ns();   // (t_done[0]: k_init ran)
+    }
+    for (unsigned long long i = threadIdx.x; i < p.zero_words; i += blockDim.x) p.bdone[i] = 0;
+    if (p.mask_leaves)                     // bitmask memo: level-1 entries (leaf cost, card)
+        for (int v = threadIdx.x; v < p.q->n; v += blockDim.x) {
+            p.memo.dcost[1ull << v] = p.q->leaf[v];
+            p.memo.dcard[1ull << v] = p.q->card[v];
+        }
 }
 
 // ------------------------------------------------------------ k_enum

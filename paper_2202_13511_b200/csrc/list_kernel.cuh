@@ -71,10 +71,18 @@ __device__ void enum_to_list(const Params<uint32_t>& p, int k, const SQ<uint32_t
         base = __shfl_sync(0xffffffffu, base, 31);
         if (c) {
             unsigned long long d = base + inc - c;
-            uint32_t X = S0;
-            for (int i = 0; i < kListChunk && r0 + i < b1; i++) {
-                if ((flags >> i) & 1u) seg[d++] = ((r0 + i) << 32) | X;
-                if (r0 + i + 1 < b1) X = gosper(X);
+            // the segment end must stay inside the list (plan_layout may clamp
+            // list_cap to the scratch space): overflow is an error, never a
+            // write past the list
+            const unsigned long long seg0 = (unsigned long long)blockIdx.x * blockDim.x * rpt;
+            if (seg0 + d + c > p.list_cap) {
+                atomicOr(&p.result->error, ERR_CAPACITY);
+            } else {
+                uint32_t X = S0;
+                for (int i = 0; i < kListChunk && r0 + i < b1; i++) {
+                    if ((flags >> i) & 1u) seg[d++] = ((r0 + i) << 32) | X;
+                    if (r0 + i + 1 < b1) X = gosper(X);
+                }
             }
         }
     }

@@ -27,7 +27,8 @@ namespace mpdp {
 
 enum MemoKind : int { MEMO_HASH = 0, MEMO_DENSE = 1, MEMO_MASK = 2 };
 
-enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u, ERR_HANG = 16u };
+enum ErrBits : unsigned int { ERR_CAPACITY = 1u, ERR_PROBE = 2u, ERR_ITEMS = 4u, ERR_TABLE_FULL = 8u, ERR_HANG = 16u,
+                             ERR_TIMEOUT = 32u };
 
 // Watchdog for device spin-waits: a bug must surface as an error, never as a
 // hung GPU.  Returns true once `t0` (from globaltimer_ns) is more than 2 s old.

@@ -31,7 +31,7 @@ namespace {
 thread_local std::string g_tls_error;
 
 struct DevLayout {
-    size_t query = 0, desc = 0, result = 0, gbar = 0, segcnt = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
+    size_t query = 0, desc = 0, result = 0, gbar = 0, df = 0, segcnt = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
            hcard = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
@@ -153,9 +153,15 @@ struct mpdp_ctx {
     bool batch_attr = false;
     int star_hub = -1;                    // star queries: the relation adjacent to all others
     int star_occ = 0;                     // k_dp_star CTAs per SM
+    int clique_df_occ = 0;                // k_dp_clique_df (ablation) CTAs per SM
+    bool clique_df_attr = false;
     bool star = false;                    // last query ran k_dp_star (memo_kind 4)
     unsigned long long tree_max_level = 0;  // tree queries: largest level (connected sets of one size)
     bool fused = false;                  // last run used the fused kernel
+    // the level descriptors are zero (the dataflow kernels leave them zeroed;
+    // every k_init-based path leaves them dirty): the star / clique dataflow
+    // launch needs no k_init when this holds
+    bool desc_clean = true;
     bool sharded = false;                // last run used the sharded (multi-GPU) path
     struct SubProblem {                  // MPDP_FLAG_RECORD_SUBPROBLEMS
         std::vector<double> card, sel, leaf;
@@ -400,6 +406,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.desc = L.sh_desc[0];
     L.result = L.sh_result[0];
     L.gbar = take(64);
+    L.df = take(sizeof(DataflowDev));
     L.segcnt = take(4 * 2 * kMaxGrid);
     L.rank = take(sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25));
     off = align_up(off, 256);
@@ -418,7 +425,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     const bool mask = c->cls != CLS_TREE && W == 1 && !c->wide && n >= 2 && n <= kMaskMaxN &&
                       !(c->flags & (MPDP_FLAG_HASH_MEMO | MPDP_FLAG_RANK_MEMO | MPDP_FLAG_NO_FUSED |
                                     MPDP_FLAG_PROFILE_KERNELS)) &&
-                      c->timeout_ms <= 0;
+                      (c->timeout_ms <= 0 || c->cls == CLS_CLIQUE);   // (k_dp_clique checks the deadline)
     if (mask) dense_entries = std::max(dense_entries, 1ull << n);
     const size_t dense_bytes = 2 * align_up(8 * dense_entries, 256) + align_up(4 * dense_entries, 256);
     const bool dense_ok = !c->wide && !(c->flags & MPDP_FLAG_HASH_MEMO) &&
@@ -462,13 +469,14 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     if (c->cls == CLS_TREE)
         for (int k = 2; k < n; k++)
             list_cap = std::max(list_cap, sat_mul(binom_u64(n, k) + 2ull * kMaxGrid, (unsigned long long)(n - k)));
-    // cliques with the bitmask memo merge split sets through two buffers of
-    // one (key, count) slot per warp of the grid (clique_level)
+    // cliques with the bitmask memo merge split sets through (key, key, count)
+    // slots per warp chunk of each split level (about one per warp of the grid
+    // per split level: k_dp_clique)
     if (L.mask_memo && c->cls == CLS_CLIQUE)
-        heavy_cap = std::max<unsigned long long>(heavy_cap, 2ull * kMaxGrid * (kBlock / 32));
+        heavy_cap = std::max<unsigned long long>(heavy_cap, 8ull * kMaxGrid * (kBlock / 32));
     list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / 16);   // fused: two lists of (rank << 32 | mask)
     heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 40));
-    if (L.mask_memo && c->cls == CLS_CLIQUE && heavy_cap < 2ull * kMaxGrid * (kBlock / 32))
+    if (L.mask_memo && c->cls == CLS_CLIQUE && heavy_cap < 8ull * kMaxGrid * (kBlock / 32))
         return fail(c, MPDP_ERR_CAPACITY, "workspace too small for the clique merge slots");
     L.tiles = take(sizeof(TileRec) * tiles_cap);
     L.light = take(16 * list_cap);
@@ -508,6 +516,11 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.sh_result[shard])->error;
     p.memo_kind = L.memo_kind;
     p.gbar = reinterpret_cast<unsigned int*>(b + L.gbar);
+    p.df = reinterpret_cast<DataflowDev*>(b + L.df);
+    // debug: per-CTA timing words of the dataflow kernels in the (unused by
+    // them) level-list scratch
+    p.df_stats = getenv("MPDP_DEBUG_DF_STATS") ? reinterpret_cast<unsigned long long*>(b + L.light) : nullptr;
+    p.timeout_ns = c->timeout_ms > 0 ? (unsigned long long)(c->timeout_ms * 1e6) : 0ull;
     p.seg_cnt = reinterpret_cast<unsigned int*>(b + L.segcnt);
     p.heavy_levels = 0;
     for (int k = 2; k <= c->n; k++) {
@@ -642,6 +655,111 @@ static size_t level_loop_smem(int n) {
            sizeof(unsigned int) * (rank_geom(n).entries + 33 * 33 + (CLS == CLS_TREE ? 1 + 2 * 33 * 33 : 2 * kFusedTile));
 }
 
+// Dataflow chunks of the clique levels (k_dp_clique on `grid` CTAs): per
+// level the cost model's lanes per set (clique_group), or the split path's
+// warp chunks of >= 512 pairs with their merge slots; the first levels of at
+// most kCliqueSoloPairs pairs run as one solo chunk.  Returns false when the
+// merge slots exceed the workspace's.
+constexpr unsigned long long kCliqueSoloPairs = 512;
+static bool plan_clique_df(Params<uint32_t>& p, unsigned int grid, unsigned long long slot_cap) {
+    const unsigned long long T = (unsigned long long)grid * kDfCompute, nwarps = T / 32;
+    const int n = p.n;
+    unsigned int base = 0;
+    unsigned long long slot = 0;
+    unsigned long long target = 32768;
+    if (const char* e = getenv("MPDP_DEBUG_CLIQUE_PAIRS")) target = strtoull(e, nullptr, 10);   // experiments only
+    for (int k = p.k_begin; k <= p.k_end; k++) {
+        const unsigned long long C = binom_u64(n, k), w = (1ull << (k - 1)) - 1;
+        DfLevel& L = p.dfl[k];
+        L = DfLevel{};
+        L.base = base;
+        const unsigned int G = clique_group(w, C, T);
+        if (!G) {                                          // split path
+            const unsigned long long P = C * w;
+            const unsigned long long csize = std::max<unsigned long long>(512, (P + nwarps - 1) / nwarps);
+            L.split = 1;
+            L.chunk = (unsigned int)csize;
+            L.nslot = (unsigned int)((P + csize - 1) / csize);
+            L.slot0 = (unsigned int)slot;
+            slot += L.nslot;
+            base += (L.nslot + kDfCompute / 32 - 1) / (kDfCompute / 32);
+            continue;
+        }
+        if (C * w <= kCliqueSoloPairs && k < p.k_end) {    // a run of small levels: one chunk
+            int kb = k;
+            while (kb + 1 <= p.k_end && binom_u64(n, kb + 1) * ((1ull << kb) - 1) <= kCliqueSoloPairs) kb++;
+            if (kb > k) {
+                for (int j = k; j <= kb; j++) {
+                    const unsigned long long Cj = binom_u64(n, j), wj = (1ull << (j - 1)) - 1;
+                    DfLevel& Lj = p.dfl[j];
+                    Lj = DfLevel{};
+                    Lj.base = j == k ? base : base + 1;
+                    Lj.G = (unsigned char)std::max(1u, clique_group(wj, Cj, kDfCompute));
+                    Lj.chunk = (unsigned int)Cj;
+                }
+                L.solo = (unsigned char)kb;
+                base += 1;
+                k = kb;
+                continue;
+            }
+        }
+        // R rounds of the CTA per ticket: about `target` pairs per chunk (the
+        // control warp's per-chunk work -- fence, publish, claim -- must hide
+        // behind a chunk), but at least one ticket per CTA on the level
+        const unsigned long long round = kDfCompute / G;
+        unsigned long long R = std::max<unsigned long long>(1, (target + round * w - 1) / (round * w));
+        R = std::min(R, std::max<unsigned long long>(1, C / (round * grid)));
+        L.G = (unsigned char)G;
+        L.chunk = (unsigned int)(round * R);
+        base += (unsigned int)((C + L.chunk - 1) / L.chunk);
+    }
+    p.dfl[p.k_end + 1] = DfLevel{};
+    p.dfl[p.k_end + 1].base = base;
+    p.zero_words = slot;
+    return 2 * slot <= slot_cap;
+}
+
+static mpdp_status run_clique_df(mpdp_ctx* c, Params<uint32_t> p) {
+    const size_t smem = clique_smem_bytes();
+    int& occ = c->clique_df_occ;
+    if (!c->clique_df_attr) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_clique_df, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        c->clique_df_attr = true;
+    }
+    if (!occ) {
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_clique_df, kDfThreads, smem));
+        if (occ < 1) return fail(c, MPDP_ERR_CUDA, "clique kernel does not fit on an SM");
+    }
+    unsigned long long want = 1;
+    for (int k = 2; k <= c->n; k++) {
+        want = std::max(want, (binom_u64(c->n, k) + 511) / 512);
+        want = std::max(want, heavy_pair_bound(c->n, k, CLS_CLIQUE) / 2048);
+    }
+    const unsigned int grid = (unsigned int)std::min<unsigned long long>(
+        std::min<unsigned long long>(want, (unsigned long long)c->num_sms * occ), (unsigned long long)kMaxGrid);
+    if (!plan_clique_df(p, grid, c->lay.heavy_cap)) return fail(c, MPDP_ERR_CAPACITY, "clique merge slots exceed the workspace");
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    unsigned int nl = 1;
+    if (!c->desc_clean) {                  // (the dataflow kernels leave their state zeroed)
+        k_init<uint32_t><<<1, 256, 0, c->stream>>>(p);
+        nl++;
+    }
+    c->desc_clean = true;
+    void* args[] = {&p};
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_clique_df, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = nl;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
+}
+
 // The fused path: k_init, ONE cooperative persistent kernel for every level
 // and the extraction, then the D2H copy of the result.
 template <int CLS>
@@ -748,12 +866,71 @@ static mpdp_status run_tree1(mpdp_ctx* c, const Params<uint32_t>& p) {
 // Star queries on one GPU (k_dp_star): closed-form set indexing, memo of
 // C(n-1, k-1) entries per level inside the dense region.
 static bool star_eligible(const mpdp_ctx* c) {
-    if (c->cls != CLS_TREE || c->star_hub < 0 || c->wide || c->world > 1 || c->n < 3 || c->n > 32 ||
-        c->timeout_ms > 0)
-        return false;
+    // (honours timeout_ms on the device: the deadline is checked at every
+    // chunk claim and in every dependency wait, dataflow.cuh)
+    if (c->cls != CLS_TREE || c->star_hub < 0 || c->wide || c->world > 1 || c->n < 3 || c->n > 32) return false;
     if (c->flags & (MPDP_FLAG_NO_STAR | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
         return false;
     return c->lay.memo_kind == MEMO_DENSE;
+}
+
+// Chunk geometry of the star levels [k_begin, k_end] of one launch on `grid`
+// CTAs (dataflow tickets, one CTA's compute warps per ticket): G lanes per set
+// on levels with fewer sets than half the threads (G <= 4), runs of RUN
+// consecutive sets per group on levels with several sets per thread (one
+// unrank per run); one ticket = R rounds of the CTA (kDfCompute / G groups x
+// RUN sets) with R = 2 on the largest levels (star-25: 0.758 -> 0.749 ms).
+static void plan_star_df(Params<uint32_t>& p, unsigned int grid) {
+    const unsigned long long T = (unsigned long long)grid * kBlock;
+    int run_max = 4, rounds = 2;
+    if (const char* e = getenv("MPDP_DEBUG_STAR_RUN")) run_max = std::max(1, atoi(e));   // experiments only
+    if (const char* e = getenv("MPDP_DEBUG_STAR_ROUNDS")) rounds = std::max(1, atoi(e));
+    // runs of consecutive levels of at most `solo` sets are ONE chunk (one
+    // CTA, the compute warps' barrier between the levels): a level handoff
+    // through the dataflow counters costs a few us of fence / poll latency
+    unsigned long long solo = 300;
+    if (const char* e = getenv("MPDP_DEBUG_STAR_SOLO")) solo = strtoull(e, nullptr, 10);
+    unsigned int base = 0;
+    for (int k = p.k_begin; k <= p.k_end; k++) {
+        const unsigned long long C = p.share_hi[k] - p.share_lo[k];
+        const bool small = C <= solo && p.k_end > p.k_begin;
+        const unsigned long long TT = small ? (unsigned long long)kDfCompute : T;
+        unsigned int G = 1;
+        while (G < 4 && 2ull * G * C <= TT) G <<= 1;
+        unsigned int run = 1;
+        while ((int)run < run_max && C >= 4ull * run * TT) run <<= 1;
+        DfLevel& L = p.dfl[k];
+        L = DfLevel{};
+        L.base = base;
+        L.G = (unsigned char)G;
+        L.run = (unsigned char)run;
+        L.solo = 0;
+        if (small) {
+            int kb = k;                                    // the run of small levels k..kb
+            while (kb + 1 <= p.k_end && p.share_hi[kb + 1] - p.share_lo[kb + 1] <= solo) kb++;
+            if (kb > k) {
+                L.chunk = (unsigned int)C;
+                L.solo = (unsigned char)kb;
+                base += 1;
+                for (int j = k + 1; j <= kb; j++) {
+                    const unsigned long long Cj = p.share_hi[j] - p.share_lo[j];
+                    DfLevel& Lj = p.dfl[j];
+                    Lj = DfLevel{};
+                    Lj.base = base;                        // no tickets of their own
+                    Lj.G = 1;
+                    while (Lj.G < 4 && 2ull * Lj.G * Cj <= (unsigned long long)kDfCompute) Lj.G <<= 1;
+                    Lj.run = 1;
+                    Lj.chunk = (unsigned int)Cj;
+                }
+                k = kb;
+                continue;
+            }
+        }
+        L.chunk = (kDfCompute / G) * run * (C >= 8ull * T ? rounds : 1);
+        base += (unsigned int)((C + L.chunk - 1) / L.chunk);
+    }
+    p.dfl[p.k_end + 1] = DfLevel{};
+    p.dfl[p.k_end + 1].base = base;
 }
 
 static mpdp_status run_star(mpdp_ctx* c, Params<uint32_t> p) {
@@ -764,22 +941,31 @@ static mpdp_status run_star(mpdp_ctx* c, Params<uint32_t> p) {
     const size_t smem = star_smem_bytes();
     if (!c->star_occ) {
         CUDA_TRY(c, cudaFuncSetAttribute(k_dp_star, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->star_occ, k_dp_star, kBlock, smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->star_occ, k_dp_star, kDfThreads, smem));
         if (c->star_occ < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
     }
     unsigned long long want = 1;
     for (int k = 2; k <= c->n; k++) want = std::max(want, (binom_u64(c->n - 1, k - 1) + 255) / 256);
     const unsigned int grid = (unsigned int)std::min<unsigned long long>(
         std::min<unsigned long long>(want, (unsigned long long)c->num_sms * c->star_occ), (unsigned long long)kMaxGrid);
+    plan_star_df(p, grid);
     CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-    k_init<uint32_t><<<1, 64, 0, c->stream>>>(p);
+    // no k_init when the previous launch was a dataflow kernel: the dataflow
+    // state, the level descriptors and the error bits were returned to zero by
+    // its last CTA
+    unsigned int nl = 1;
+    if (!c->desc_clean) {
+        k_init<uint32_t><<<1, 256, 0, c->stream>>>(p);
+        nl++;
+    }
+    c->desc_clean = true;
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
     CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_star, dim3(grid), dim3(kBlock), args, smem, c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_star, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-    c->launches = 2;
+    c->launches = nl;
     c->enum_launches = 0;
     c->eval_launches = 1;
     c->nkev = 2;
@@ -873,9 +1059,10 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     const size_t smem = star ? star_smem_bytes() : level_loop_smem<CLS>(n);
     int occ_star = 0;
     int& occ = star ? occ_star : c->fused_occ[CLS];
+    const int block = star ? kDfThreads : kBlock;
     if (star) {
         CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
     } else if (!occ || c->fused_n[CLS] != n) {
         // function attributes are process-wide (shared by every context): always
@@ -894,13 +1081,15 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     c->launches = 0;
     for (int sh = 0; sh < nsh; sh++) {
         P[sh] = make_params<uint32_t>(c, sh);
-        k_init<uint32_t><<<1, 64, 0, c->stream>>>(P[sh]);
+        P[sh].timeout_ns = 0;              // (the sharded host loop has no device deadline)
+        k_init<uint32_t><<<1, 256, 0, c->stream>>>(P[sh]);
         c->launches++;
     }
     auto launch = [&](Params<uint32_t>& p, unsigned long long grid) -> mpdp_status {
         void* args[] = {&p};
         CUDA_TRY(c, cudaMemsetAsync(p.gbar, 0, sizeof(unsigned int), c->stream));   // barrier counter per launch
-        CUDA_TRY(c, cudaLaunchCooperativeKernel(kern, dim3((unsigned int)grid), dim3(kBlock), args, smem, c->stream));
+        if (star) plan_star_df(p, (unsigned int)grid);   // dataflow tickets of this launch's levels
+        CUDA_TRY(c, cudaLaunchCooperativeKernel(kern, dim3((unsigned int)grid), dim3(block), args, smem, c->stream));
         c->launches++;
         return MPDP_OK;
     };
@@ -969,6 +1158,9 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
 
 template <typename M, int CLS, int MEMO>
 static mpdp_status run_query(mpdp_ctx* c) {
+    const bool was_clean = c->desc_clean;
+    c->desc_clean = false;                 // every path but the dataflow kernels leaves them dirty
+    (void)was_clean;
     c->sharded = false;
     c->small = false;
     c->tree1 = false;
@@ -982,8 +1174,19 @@ static mpdp_status run_query(mpdp_ctx* c) {
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (small_eligible(c)) return run_small<CLS>(c, make_params<M>(c));
         if (tree1_eligible(c)) return run_tree1(c, make_params<M>(c));
-        if (star_eligible(c)) return run_star(c, make_params<M>(c));
-        if (c->timeout_ms <= 0 && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) && c->n >= 2)
+        if (star_eligible(c)) {
+            c->desc_clean = was_clean;
+            return run_star(c, make_params<M>(c));
+        }
+        const bool clique_mask = CLS == CLS_CLIQUE && c->lay.mask_memo && c->n >= 2 &&
+                                 !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS));
+        if (clique_mask && getenv("MPDP_DEBUG_CLIQUE_DF")) {   // ablation: the dataflow variant
+            c->desc_clean = was_clean;
+            return run_clique_df(c, make_params<M>(c));
+        }
+        // (k_dp_clique checks timeout_ms on the device at every level barrier)
+        if ((c->timeout_ms <= 0 || clique_mask) && !(c->flags & (MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS)) &&
+            c->n >= 2)
             return run_fused<CLS>(c, make_params<M>(c));
     }
     mpdp_status st = prepare_kernels<M, CLS, MEMO>(c);
@@ -1385,6 +1588,8 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
     }
     const ResultDev* r = c->h_result;
     if (r->error) {
+        if (r->error & ERR_TIMEOUT)
+            return fail(c, MPDP_ERR_TIMEOUT, "timeout_ms exceeded on the device (checked at every chunk of the level loop)");
         if (r->error & ERR_HANG)
             return fail(c, MPDP_ERR_INTERNAL, "device watchdog fired (a spin-wait exceeded 2 s); results discarded");
         if (r->error & (ERR_CAPACITY | ERR_ITEMS))
@@ -1502,8 +1707,11 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
                 return fail(c, MPDP_ERR_OOM, "batch staging allocation failed");
             c->batch_cap = cap;
         }
-        const int saved_n = c->n, saved_cls = c->cls;
+        // fill_query writes per-query context fields (n, class, width, star hub,
+        // largest tree level): the batch restores them afterwards
+        const int saved_n = c->n, saved_cls = c->cls, saved_hub = c->star_hub;
         const bool saved_wide = c->wide;
+        const unsigned long long saved_tml = c->tree_max_level;
         int maxn = 2;
         for (uint32_t b = 0; b < nb; b++) {
             const mpdp_query_graph& g = graphs[small[b]];
@@ -1516,6 +1724,8 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
         c->n = saved_n;
         c->cls = saved_cls;
         c->wide = saved_wide;
+        c->star_hub = saved_hub;
+        c->tree_max_level = saved_tml;
         if (!c->batch_attr) {
             CUDA_TRY(c, cudaFuncSetAttribute(k_dp_small_batch<CLS_TREE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)small_smem_bytes(kSmallMaxN)));
@@ -1571,6 +1781,10 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
         const mpdp_status st = mpdp_optimize(c, &graphs[i], MPDP_ALGO_MPDP, 0, &results[i]);
         if (st != MPDP_OK) return st;
     }
+    // a batch replaces whatever mpdp_stage had staged (the one-by-one queries
+    // restage the context): a later mpdp_run / mpdp_fetch must restage first
+    c->staged = false;
+    c->ran = false;
     return MPDP_OK;
 }
 
@@ -1598,6 +1812,36 @@ int mpdp_debug_trace(const mpdp_ctx* c, unsigned long long* out, int cap) {
         out[nn++] = c->h_result->trace[i];
     }
     return nn;
+}
+
+// Debug: per level k of the last whole-query run, the start (first chunk /
+// level start) and, for the dataflow kernels, the finish of its last chunk, in
+// us after the start of level 2 (0 = not recorded).  Returns n.
+int mpdp_debug_level_span(const mpdp_ctx* c, double* start_us, double* done_us, int cap) {
+    if (!c || !c->h_result || !start_us || !done_us) return 0;
+    const ResultDev* r = c->h_result;
+    unsigned long long t0 = ~0ull;
+    for (int k = 2; k <= c->n + 1 && k < kMaxN + 2; k++)
+        if (r->t_level[k]) t0 = std::min(t0, r->t_level[k]);
+    int nn = 0;
+    auto us = [&](unsigned long long t) { return t && t0 != ~0ull ? 1e-3 * ((double)t - (double)t0) : 0.0; };
+    for (int k = 0; k <= c->n + 1 && k < cap && k < kMaxN + 2; k++, nn++) {
+        start_us[k] = us(r->t_level[k]);
+        done_us[k] = us(r->t_done[k]);
+    }
+    return nn;
+}
+
+// Debug (MPDP_DEBUG_DF_STATS set when the query ran): per CTA of the last
+// dataflow launch 8 words {control: ns waiting for a free slot, ns waiting for
+// dependencies, ns in the loop, chunks; compute warp 0: ns waiting for chunks,
+// ns in the loop, -, -}.  Returns the words copied.
+int mpdp_debug_df_stats(const mpdp_ctx* c, unsigned long long* out, int cap) {
+    if (!c || !out || !getenv("MPDP_DEBUG_DF_STATS")) return 0;
+    const int words = std::min(cap, 8 * kMaxGrid);
+    if (cudaMemcpy(out, c->ws + c->lay.light, sizeof(unsigned long long) * words, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return words;
 }
 
 mpdp_status mpdp_nccl_get_unique_id(void* out128) {

@@ -18,13 +18,13 @@
 // levels give G = 2 or 4 lanes to a set.  One grid barrier per level.
 #pragma once
 #include "fused.cuh"
+#include "dataflow.cuh"
 
 #include <type_traits>
 
 namespace mpdp {
 
 constexpr int kStarMinBlocks = 3;
-constexpr unsigned int kStarSolo = 300;     // levels of at most this many sets run on CTA 0 alone
 
 // leaf space: the vertices other than the hub, vertex v -> v - (v > hub)
 __device__ __forceinline__ uint32_t star_compress(uint32_t S, int hub) {
@@ -50,68 +50,29 @@ __device__ __forceinline__ unsigned long long star_slot(const Params<uint32_t>& 
     return p.star_off[__popc(S)] + r;
 }
 
-__global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid_constant__ Params<uint32_t> p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
-    unsigned int* bin = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));   // 33 x 33
-    load_query(q, p.q);
-    constexpr int NB = MaxN<uint32_t>::value + 1;
-    for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
-        const int a = i / 33, b = i % 33;
-        bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
-    }
-    // (C(v, m+1), C(v, m+1) - C(v, m)) pairs of the descending walk, 8-byte aligned
-    uint2* binp = reinterpret_cast<uint2*>(smem_raw + ((sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33 + 7) & ~size_t(7)));
-    __syncthreads();
-    for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x) {
-        const int a = i / 32, b = i % 32;
-        binp[a * 33 + b] = make_uint2(bin[a * 33 + b + 1], bin[a * 33 + b + 1] - bin[a * 33 + b]);
-    }
-    unsigned int nbar = 0;
-    __syncthreads();
-    const int n = p.n, hub = p.star_hub, nl = n - 1;
+// Sets [lo, hi) of star level k on the CTA's compute threads, G lanes per
+// set, runs of RUN consecutive sets per group (one unrank, then Gosper):
+// lane-consecutive groups, so a warp's probes of the shared high elements
+// coalesce and the CTA's warps share L1 lines.  Counts the join pairs this
+// thread evaluated and the sets it wrote.
+template <int G>
+__device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
+                                           const uint2* binp, int k, unsigned int lo, unsigned int hi,
+                                           unsigned int RUN, unsigned long long& npairs, unsigned long long& nsets) {
+    const int hub = p.star_hub, nl = p.n - 1, kl = k - 1;   // kl leaves per set
     const bool leaf_costs = q.pad != 0;
-    // Levels with at most kStarSolo sets (the first and last few) run on CTA 0
-    // alone with __syncthreads as the level barrier; the grid barrier is taken
-    // only where a full-grid level follows (a grid barrier costs ~1.5 us plus a
-    // global round trip of every set's data).
-    auto solo = [&](int k) { return k >= p.k_begin && k <= p.k_end && p.share_hi[k] - p.share_lo[k] <= kStarSolo; };
-    for (int k = p.k_begin; k <= p.k_end; k++) {
-        const bool one = solo(k);
-        if (one && blockIdx.x != 0) {                         // CTA 0's level: join at the next grid barrier
-            if (!solo(k + 1) && k < p.k_end) grid_sync(p.gbar, nbar, &p.result->error);
-            continue;
-        }
-        const unsigned long long T = one ? blockDim.x : (unsigned long long)gridDim.x * blockDim.x;
-        const unsigned long long gtid = one ? threadIdx.x : (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-        if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
-        const int kl = k - 1;                                 // leaves per set
-        // this launch's share [lo, lo + C) of the level's C(n-1, k-1) sets
-        // (all of them on one GPU; a rank's segment when sharded)
-        const unsigned int lo = p.share_lo[k], C = p.share_hi[k] - lo;
-        const double* lvl = p.memo.dcost + p.star_off[k - 1];
-        const double* lcard = p.memo.dcard + p.star_off[k - 1];
-        const unsigned long long out = p.star_off[k];
-        unsigned int G = 1;                                   // lanes per set (small levels)
-        while (G < 4 && 2ull * G * C <= T) G <<= 1;
-        const unsigned long long ng = T / G, grp = gtid / G;
-        const unsigned int sub = threadIdx.x & (G - 1);
-        // lane-consecutive sets, each (run) unranked: colex neighbours share
-        // their high elements, so a warp's probes of those coalesce (per-thread
-        // Gosper runs over a whole share put lanes ~24 sets apart: 27 sectors
-        // per request instead of 8.4, star-25 1.19 vs 1.01 ms)
-        // runs of RUN consecutive sets per group (one unrank, then Gosper) on
-        // levels with several sets per thread: fewer unranks for slightly less
-        // coalescing (star-25: RUN 1 -> 2 1.006 -> 0.945 ms; 4 on the largest
-        // levels 0.83 -> 0.81 ms; RUN > 1 on small levels costs parallelism)
-        const unsigned int RUN = C >= 8ull * T ? 4u : (C >= 4ull * T ? 2u : 1u);
-        const unsigned long long rounds = (C + ng * RUN - 1) / (ng * RUN) * RUN;
-        uint32_t L = 0;
-        unsigned long long nsets = 0;
-        for (unsigned long long it = 0; it < rounds; it++) {
-            const unsigned long long h = lo + (it / RUN * ng + grp) * RUN + it % RUN;
-            const bool act = h < lo + (unsigned long long)C;
-            if (act) L = (it % RUN == 0) ? unrank_colex32(bin, nl, kl, (unsigned int)h) : gosper(L);
+    const double* lvl = p.memo.dcost + p.star_off[k - 1];
+    const double* lcard = p.memo.dcard + p.star_off[k - 1];
+    const unsigned long long out = p.star_off[k];
+    constexpr unsigned int NG = kDfCompute / G;              // groups per CTA
+    const unsigned int grp = threadIdx.x / G, sub = threadIdx.x & (G - 1);
+    uint32_t L = 0;
+    for (unsigned int r0 = lo; r0 < hi; r0 += NG * RUN) {     // uniform trip count
+        const unsigned int h0 = r0 + grp * RUN;
+        for (unsigned int it = 0; it < RUN; it++) {
+            const unsigned int h = h0 + it;
+            const bool act = h < hi;
+            if (act) L = (it == 0) ? unrank_colex32(bin, nl, kl, h) : gosper(L);
             Key best = key_inf();
             double cS = 0.0;
             uint32_t S = 0;
@@ -123,27 +84,33 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                     const double c = __dadd_rn(__dadd_rn(q.leaf[hub], q.leaf[v]), cS);
                     const uint32_t a = 1u << hub, b = 1u << v;
                     best = Key{(unsigned long long)__double_as_longlong(c), (unsigned long long)(a < b ? a : b)};
+                    npairs += sub == 0;
                 } else {
                     const int pl = 31 - __clz(L);             // max leaf (leaf space)
                     const int pv = star_vertex(pl, hub);
                     if (pv > hub) {                           // max(S) is a leaf: card(S) from card(S \ max)
-                        double x = __dmul_rn(__ldcs(lcard + ((unsigned int)h - bin[pl * 33 + kl])), q.card[pv]);
+                        double x = __dmul_rn(__ldcs(lcard + (h - bin[pl * 33 + kl])), q.card[pv]);
                         cS = __dmul_rn(x, q.sel[hub * q.n + pv]);
                     } else {
                         cS = card_of(q, S);
                     }
-                    // descending walk over L, 4 probes in flight
+                    // Pair ({v}, S \ {v}) per leaf v, walked from the largest
+                    // leaf down.  Tie-break key (reading R7, min(left, right)
+                    // as a mask) in leaf space: {v} for every leaf but the
+                    // largest vertex of S, whose pair's smaller side is
+                    // S \ {v} (key 32, above every singleton); so along the
+                    // descending walk a later candidate of equal cost always
+                    // has the smaller key, and "<=" is the exact R7 min.
                     double bc = __longlong_as_double(0x7ff0000000000000ll);   // +inf
-                    uint32_t bl = 0xffffffffu;
+                    int bl = 64;
                     unsigned int SD = 0;
                     uint32_t W = L;
                     int m = kl - 1;
-                    // batches of 4 elements: kl / 4 full ones without guards, then
-                    // the remainder
+                    const bool top_rb = pv > hub;             // the largest leaf is max(S)
                     auto batch = [&](auto guard) {
                         constexpr bool GUARD = decltype(guard)::value;
                         unsigned int rk[4];
-                        int vv[4];
+                        int ll[4];
                         bool ok[4];
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
@@ -151,10 +118,10 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                             const int l = has ? 31 - __clz(W) : 0;
                             W ^= has ? 1u << l : 0u;
                             const uint2 cc = binp[l * 33 + (has ? m : 0)];
-                            rk[u] = (unsigned int)h - cc.x - SD;
+                            rk[u] = h - cc.x - SD;
                             SD += has ? cc.y : 0u;
-                            ok[u] = has && ((unsigned int)m & (G - 1)) == sub;
-                            vv[u] = star_vertex(l, hub);
+                            ok[u] = has && (G == 1 || ((unsigned int)m & (G - 1)) == sub);
+                            ll[u] = (m == kl - 1 && top_rb) ? 32 : l;
                             m -= has ? 1 : 0;
                         }
                         double dv[4];
@@ -162,22 +129,26 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                         for (int u = 0; u < 4; u++) dv[u] = ok[u] ? lvl[rk[u]] : 0.0;
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
-                            // min of (cost, left) in f64 / u32 (costs are >= 0: the
-                            // f64 order is the bit order of the Key)
-                            const double a = leaf_costs ? __dadd_rn(q.leaf[vv[u]], dv[u]) : dv[u];
+                            const double a =
+                                leaf_costs ? __dadd_rn(q.leaf[star_vertex(ll[u] == 32 ? pl : ll[u], hub)], dv[u]) : dv[u];
                             const double c = __dadd_rn(a, cS);
-                            const uint32_t lb = 1u << vv[u], rb = S ^ lb, l = lb < rb ? lb : rb;
-                            const bool better = ok[u] && (c < bc || (c == bc && l < bl));
+                            const bool better = ok[u] && c <= bc;
                             bc = better ? c : bc;
-                            bl = better ? l : bl;
+                            bl = better ? ll[u] : bl;
+                            npairs += ok[u];
                         }
                     };
                     for (int bt = kl >> 2; bt > 0; bt--) batch(std::false_type{});
                     if (kl & 3) batch(std::true_type{});
-                    best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
+                    // the real left mask of the best key (group_min compares
+                    // masks across lanes)
+                    uint32_t lm = 0xffffffffu;
+                    if (bl == 32) lm = S ^ (1u << pv);
+                    else if (bl < 32) lm = 1u << star_vertex(bl, hub);
+                    best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)lm};
                 }
             }
-            best = group_min(best, G);
+            if (G > 1) best = group_min(best, G);
             if (act && sub == 0) {
                 const unsigned long long idx = out + h;
                 p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
@@ -186,29 +157,128 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
                 nsets++;
             }
         }
-        if ((p.count_levels >> k) & 1ull) {
-            // every written set evaluated its kl join pairs (kl non-singleton
-            // probes when k >= 3)
-            const unsigned long long pairs = nsets * (unsigned long long)kl, nprobe = k >= 3 ? pairs : 0ull;
-            flush_counters(&p.desc[k], pairs, pairs, nprobe, nsets);
-        }
-        if (one && (solo(k + 1) || k == p.k_end)) __syncthreads();   // CTA 0 continues alone
-        else grid_sync(p.gbar, nbar, &p.result->error);
     }
-    if (!(p.do_extract && blockIdx.x == 0 && threadIdx.x < 32)) return;
-    // ---- counters and plan extraction, warp 0 of CTA 0
+}
+
+__device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
+                                          int hub);
+
+// Star levels as dataflow chunks (dataflow.cuh): level k's sets are the
+// colex ranks of its (k-1)-leaf sets; a chunk needs level k-1 up to the
+// largest leaf of its last set.
+struct StarSched {
+    const Params<uint32_t>& p;
+    const unsigned int* bin;
+    __device__ unsigned int total() const { return p.dfl[p.k_end + 1].base; }
+    __device__ void locate(unsigned int t, DfSlot& d) const {
+        int k = p.k_begin;
+        while (t >= p.dfl[k + 1].base) k++;
+        const DfLevel& L = p.dfl[k];
+        d.t = t;
+        d.k = k;
+        d.k2 = L.solo > k ? L.solo : k;
+        d.lo = p.share_lo[k] + (t - L.base) * L.chunk;
+        d.hi = min(d.lo + L.chunk, p.share_hi[k]);
+    }
+    __device__ int need(const DfSlot& d) const {
+        return (d.k >= 3 && d.k - 1 >= p.k_begin) ? colex_top(bin, d.k - 1, d.hi - 1) : -1;
+    }
+    // sets of level k1 (k1 - 1 leaves) whose largest leaf is j
+    __device__ unsigned int need_count(int k1, int j) const { return bin[j * 33 + k1 - 2]; }
+    __device__ void publish(const DfSlot& d) const {
+        df_publish_colex(p, bin, d.k, d.k - 1, d.lo, d.hi);
+        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex(p, bin, k, k - 1, p.share_lo[k], p.share_hi[k]);
+    }
+};
+
+__global__ void __launch_bounds__(kDfThreads, kStarMinBlocks) k_dp_star(const __grid_constant__ Params<uint32_t> p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
+    unsigned int* bin = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));   // 33 x 33
+    __shared__ DfCounters sc;
+    __shared__ DfShared sh;
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[0] = globaltimer_ns();   // kernel start
+    load_query(q, p.q);
+    constexpr int NB = MaxN<uint32_t>::value + 1;
+    for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
+        const int a = i / 33, b = i % 33;
+        bin[i] = (a < NB && b < NB) ? (unsigned int)p.q->binom[a * NB + b] : 0u;
+    }
+    for (int i = threadIdx.x; i < (kMaxN + 1) * 3; i += blockDim.x) (&sc.v[0][0])[i] = 0;
+    for (int i = threadIdx.x; i <= kMaxN; i += blockDim.x) sh.ready[i] = i < p.k_begin ? 64 : -1;
+    if (threadIdx.x < kDfSlots) sh.done[threadIdx.x] = 0;
+    // (C(v, m+1), C(v, m+1) - C(v, m)) pairs of the descending walk, 8-byte aligned
+    uint2* binp = reinterpret_cast<uint2*>(smem_raw + ((sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33 + 7) & ~size_t(7)));
+    __syncthreads();
+    for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x) {
+        const int a = i / 32, b = i % 32;
+        binp[a * 33 + b] = make_uint2(bin[a * 33 + b + 1], bin[a * 33 + b + 1] - bin[a * 33 + b]);
+    }
+    __syncthreads();
+    const int n = p.n, hub = p.star_hub;
+    if (threadIdx.x >= kDfCompute) {
+        df_control(p, StarSched{p, bin}, sh);
+    } else {
+        int kc = p.k_begin;
+        unsigned long long npairs = 0, nsets = 0;      // this thread, level kc
+        DfSlot d;
+        unsigned long long st_take = 0;
+        const unsigned long long st0 = p.df_stats ? globaltimer_ns() : 0ull;
+        unsigned long long* stp = (p.df_stats && threadIdx.x == 0) ? &st_take : nullptr;
+        for (unsigned int i = 0; df_take(sh, i, d, stp); i++) {
+            // (a solo chunk runs whole small levels d.k..d.k2 back to back,
+            // the compute warps' named barrier 3 between them)
+            for (int k = d.k; k <= d.k2; k++) {
+                if (k != kc) {
+                    df_count(sc, kc, npairs, kc >= 3 ? npairs : 0ull, nsets);
+                    npairs = nsets = 0;
+                    kc = k;
+                }
+                if (k > d.k) {
+                    asm volatile("bar.sync 3, %0;" ::"r"(kDfCompute) : "memory");
+                    if (threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+                }
+                const DfLevel& L = p.dfl[k];
+                const unsigned int lo = k == d.k ? d.lo : p.share_lo[k], hi = k == d.k ? d.hi : p.share_hi[k];
+                switch (L.G) {
+                    case 1: star_chunk<1>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets); break;
+                    case 2: star_chunk<2>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets); break;
+                    default: star_chunk<4>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets); break;
+                }
+            }
+            df_finish(sh, i);
+        }
+        if (stp) {
+            p.df_stats[8ull * blockIdx.x + 4] = st_take;
+            p.df_stats[8ull * blockIdx.x + 5] = globaltimer_ns() - st0;
+        }
+        // every pair of a set of level >= 3 probes one memo entry (S \ {v}, >= 2 relations)
+        df_count(sc, kc, npairs, kc >= 3 ? npairs : 0ull, nsets);
+    }
+    if (!df_exit(p, sc)) return;
+    if (p.do_extract && threadIdx.x < 32) star_extract(p, q, bin, hub);
+    df_reset(p);
+}
+
+// Counters and plan extraction, warp 0 of the last CTA out.
+__device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
+                                          int hub) {
+    const int n = p.n;
     ResultDev* r = p.result;
-    const unsigned int lane = threadIdx.x;
+    const unsigned int lane = threadIdx.x;             // warp 0
     if (lane == 0) r->t_level[n + 1] = globaltimer_ns();
     level_counters_warp(p, r);
-    if (ld_relaxed_u32(&r->error)) {
+    if (ld_relaxed_u32(&p.df->error)) {
         if (lane == 0) r->n_nodes = 0;
         return;
     }
     // The optimal plan of a star set is a caterpillar: every join splits one
-    // leaf v off, ({v}, S \ {v}).  Walk the chain from V (one memo read per
-    // step; the colex rank of each set's leaf set is a warp sum of one binomial
-    // per element), then emit the post-order nodes from the recorded chain.
+    // leaf v off, ({v}, S \ {v}).  Walk the chain from V two steps per memo
+    // round trip: while lane 31 reads the entry of S, lane j reads the entry of
+    // S \ {leaf j} (the colex rank of its leaf set from two warp scans of the
+    // binomial terms), so once left(S) names v the entry of the next set is
+    // already in the registers of v's lane.  The recorded chain is then
+    // emitted as post-order nodes.
     __shared__ uint32_t c_set[32], c_left[32];
     __shared__ double c_cost[32], c_card[32];
     uint32_t S = n == 32 ? ~0u : (1u << n) - 1u;
@@ -216,22 +286,62 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
     while (__popc(S) >= 2) {
         const uint32_t L = star_compress(S, hub);
         const int kl = __popc(L);
-        unsigned int term = 0;
-        if ((int)lane < kl) term = bin[(__fns(L, 0, lane + 1)) * 33 + lane + 1];
-        for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
-        const unsigned long long idx = p.star_off[kl + 1] + term;
-        uint32_t left = 0;
+        const bool mine = (int)lane < kl;
+        const int lj = mine ? (int)__fns(L, 0, lane + 1) : 0;            // leaf j (leaf space)
+        const unsigned int a = mine ? bin[lj * 33 + lane + 1] : 0u;      // C(l_j, j+1): term of rank(L)
+        const unsigned int b = mine ? bin[lj * 33 + lane] : 0u;          // C(l_j, j): term once l_j moves down
+        unsigned int ia = a, ib = b;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned int x = __shfl_up_sync(0xffffffffu, ia, o), y = __shfl_up_sync(0xffffffffu, ib, o);
+            if ((int)lane >= o) {
+                ia += x;
+                ib += y;
+            }
+        }
+        const unsigned int ra = __shfl_sync(0xffffffffu, ia, 31), rb = __shfl_sync(0xffffffffu, ib, 31);
+        // S itself (lane 31), S \ {leaf j} (lane j < kl, when it keeps >= 2 relations)
+        unsigned long long idx = 0;
+        bool load = false;
+        if (lane == 31) {
+            idx = p.star_off[kl + 1] + ra;
+            load = true;
+        } else if (mine && kl >= 2) {
+            idx = p.star_off[kl] + (ia - a) + (rb - ib);
+            load = true;
+        }
+        uint32_t e_left = 0;
+        double e_cost = 0.0, e_card = 0.0;
+        if (load) {
+            e_left = __ldcg(p.memo.dleft + idx);
+            e_cost = __ldcg(p.memo.dcost + idx);
+            e_card = __ldcg(p.memo.dcard + idx);
+        }
+        const uint32_t left = __shfl_sync(0xffffffffu, e_left, 31);
+        const double cS = __shfl_sync(0xffffffffu, e_cost, 31), kS = __shfl_sync(0xffffffffu, e_card, 31);
         if (lane == 0) {
-            left = __ldcg(p.memo.dleft + idx);
             c_set[len] = S;
             c_left[len] = left;
-            c_cost[len] = __ldcg(p.memo.dcost + idx);
-            c_card[len] = __ldcg(p.memo.dcard + idx);
+            c_cost[len] = cS;
+            c_card[len] = kS;
         }
-        left = __shfl_sync(0xffffffffu, left, 0);
-        const uint32_t right = S ^ left;
-        S = (left & (left - 1)) ? left : right;           // the multi-relation side (a singleton at the end)
         len++;
+        const uint32_t right = S ^ left;
+        const uint32_t S1 = (left & (left - 1)) ? left : right;     // the multi-relation side
+        if ((S1 & (S1 - 1)) == 0) break;                            // S was a pair: chain complete
+        // S1 = S \ {v}: its entry sits in the lane of leaf v
+        const uint32_t vm = star_compress(S ^ S1, hub);              // {v} in leaf space
+        const int src = __popc(L & (vm - 1u));
+        const uint32_t l1 = __shfl_sync(0xffffffffu, e_left, src);
+        const double c1 = __shfl_sync(0xffffffffu, e_cost, src), k1 = __shfl_sync(0xffffffffu, e_card, src);
+        if (lane == 0) {
+            c_set[len] = S1;
+            c_left[len] = l1;
+            c_cost[len] = c1;
+            c_card[len] = k1;
+        }
+        len++;
+        const uint32_t r1 = S1 ^ l1;
+        S = (l1 & (l1 - 1)) ? l1 : r1;
         if ((S & (S - 1)) == 0) break;
     }
     if (lane != 0) return;
@@ -287,6 +397,7 @@ __global__ void __launch_bounds__(kBlock, kStarMinBlocks) k_dp_star(const __grid
         inner = nn++;
     }
     r->n_nodes = (unsigned int)nn;
+    atomicMax(&p.df->t_done[n + 1], globaltimer_ns());     // extraction end
     r->cost = r->nodes[nn - 1].cost;
 }
 

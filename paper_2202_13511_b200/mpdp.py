@@ -75,7 +75,8 @@ FLAG_NO_STAR = 4096
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_optimize_batch", "mpdp_stage",
            "mpdp_run", "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
            "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace", "mpdp_subproblem_count",
-           "mpdp_subproblem_get", "mpdp_heuristic_optimize"]
+           "mpdp_subproblem_get", "mpdp_heuristic_optimize", "mpdp_debug_level_span",
+           "mpdp_debug_df_stats"]
 
 _lib = None
 
@@ -104,6 +105,8 @@ def load_library(path: str = LIB_PATH):
         "mpdp_nccl_get_unique_id": (C.c_int, [P]),
         "mpdp_share": (None, [C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_uint64),
                               C.POINTER(C.c_uint64)]),
+        "mpdp_debug_level_span": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int]),
+        "mpdp_debug_df_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
