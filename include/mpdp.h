@@ -190,6 +190,11 @@ typedef struct {
 /* flags: run star queries (one relation adjacent to all others, n >= 14)
  * through the general tree kernel instead of k_dp_star (ablation)              */
 #define MPDP_FLAG_NO_STAR 4096u
+/* flags (testing, world == 1): create a real 1-rank NCCL communicator and run
+ * every query on the multi-GPU sharded path with EVERY level sharded, so the
+ * per-level ncclAllGather exchange and the counter ncclAllReduce execute on a
+ * single GPU (bit-identical results to the single-GPU kernels)            */
+#define MPDP_FLAG_NCCL_SELF 8192u
 
 typedef struct mpdp_ctx mpdp_ctx;
 

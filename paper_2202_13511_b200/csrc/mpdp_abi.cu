@@ -106,6 +106,10 @@ NcclApi* nccl_api(std::string& err) {
 struct mpdp_ctx {
     int device = 0, rank = 0, world = 1;
     bool simulate = false;                // world ranks simulated as shards on this device
+    // MPDP_FLAG_NCCL_SELF (testing): world == 1 with a real 1-rank NCCL
+    // communicator, every query on the sharded path with every level sharded
+    bool nccl_self = false;
+    bool multi = false;                   // the sharded path: world > 1 || nccl_self
     NcclApi* nccl = nullptr;
     ncclComm_t comm = nullptr;
     ResultDev* h_results = nullptr;       // pinned, one per local shard
@@ -422,7 +426,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k) + (unsigned long long)W;
     // MEMO_MASK: clique / general queries on one GPU through the whole-query
     // kernel index the same arrays by bitmask (2^n entries)
-    const bool mask = c->cls != CLS_TREE && W == 1 && !c->wide && n >= 2 && n <= kMaskMaxN &&
+    const bool mask = c->cls != CLS_TREE && !c->multi && !c->wide && n >= 2 && n <= kMaskMaxN &&
                       !(c->flags & (MPDP_FLAG_HASH_MEMO | MPDP_FLAG_RANK_MEMO | MPDP_FLAG_NO_FUSED |
                                     MPDP_FLAG_PROFILE_KERNELS)) &&
                       (c->timeout_ms <= 0 || c->cls == CLS_CLIQUE);   // (k_dp_clique checks the deadline)
@@ -432,7 +436,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
                           (size_t)nsh * dense_bytes + 1024 <= memo_bytes;
     L.memo_kind = dense_ok ? MEMO_DENSE : MEMO_HASH;
     L.mask_memo = dense_ok && mask;
-    if (W > 1 && !dense_ok)
+    if (c->multi && !dense_ok)
         return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs the perfect-hash memo (n <= 32) and " +
                                               std::to_string(nsh * dense_bytes >> 20) + " MiB of memo space");
     const unsigned long long buckets = (unsigned long long)(memo_bytes / (sizeof(Bucket) + 2 * msz));
@@ -816,7 +820,7 @@ static mpdp_status run_fused(mpdp_ctx* c, const Params<uint32_t>& p) {
 // round trips dominate: tree queries with n <= 13.
 static bool small_eligible(const mpdp_ctx* c) {
     const int n = c->n;
-    if (c->wide || c->world > 1 || n < 2 || n > kSmallMaxN || c->timeout_ms > 0) return false;
+    if (c->wide || c->multi || n < 2 || n > kSmallMaxN || c->timeout_ms > 0) return false;
     if (c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
         return false;
     // measured (B200): star-10 115 -> 54 us, snowflake-12 -> 74 us; cliques and
@@ -829,7 +833,7 @@ static bool small_eligible(const mpdp_ctx* c) {
 // Sparse tree queries whose every level fits the single-CTA kernel's shared
 // memory lists (k_dp_tree1; global colex-rank memo).
 static bool tree1_eligible(const mpdp_ctx* c) {
-    if (c->cls != CLS_TREE || c->wide || c->world > 1 || c->n < 3 || c->n > 32 || c->timeout_ms > 0) return false;
+    if (c->cls != CLS_TREE || c->wide || c->multi || c->n < 3 || c->n > 32 || c->timeout_ms > 0) return false;
     if (c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
         return false;
     // measured (B200): chain-25 (<= 24 sets per level) 290 -> 222 us; snowflake-20
@@ -868,7 +872,7 @@ static mpdp_status run_tree1(mpdp_ctx* c, const Params<uint32_t>& p) {
 static bool star_eligible(const mpdp_ctx* c) {
     // (honours timeout_ms on the device: the deadline is checked at every
     // chunk claim and in every dependency wait, dataflow.cuh)
-    if (c->cls != CLS_TREE || c->star_hub < 0 || c->wide || c->world > 1 || c->n < 3 || c->n > 32) return false;
+    if (c->cls != CLS_TREE || c->star_hub < 0 || c->wide || c->multi || c->n < 3 || c->n > 32) return false;
     if (c->flags & (MPDP_FLAG_NO_STAR | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
         return false;
     return c->lay.memo_kind == MEMO_DENSE;
@@ -1096,7 +1100,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     const unsigned long long min_shard = (c->flags & MPDP_FLAG_SHARD_ALL_LEVELS) ? 0ull : kShardMinRanks;
     for (int k = 2; k <= n; k++) {
         const unsigned long long C = star ? binom_u64(n - 1, k - 1) : binom_u64(n, k);
-        const bool sharded = W > 1 && C >= min_shard;
+        const bool sharded = (W > 1 && C >= min_shard) || c->nccl_self;
         const unsigned long long seg = (C + W - 1) / W;
         for (int sh = 0; sh < nsh; sh++) {
             const int rank = c->simulate ? sh : c->rank;
@@ -1166,9 +1170,9 @@ static mpdp_status run_query(mpdp_ctx* c) {
     c->tree1 = false;
     c->star = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
-        if (c->world > 1) return run_sharded<CLS>(c);
+        if (c->multi) return run_sharded<CLS>(c);
     }
-    if (c->world > 1) return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
+    if (c->multi) return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
     c->fused = false;
     c->small = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
@@ -1392,6 +1396,8 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
     c->rank = cfg->rank;
     c->world = cfg->world;
     c->simulate = simulate;
+    c->nccl_self = cfg->world == 1 && (cfg->flags & MPDP_FLAG_NCCL_SELF);
+    c->multi = cfg->world > 1 || c->nccl_self;
     c->timeout_ms = cfg->timeout_ms;
     c->flags = cfg->flags;
     if (cfg->load_factor > 0.0) c->load_factor = cfg->load_factor;
@@ -1430,12 +1436,16 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
         cudaMallocHost(&c->h_rank_pinned, sizeof(unsigned int) * rank_geom(32).entries) != cudaSuccess)
         return bail(fail(nullptr, MPDP_ERR_OOM, "pinned host allocation failed"));
     c->h_result = c->h_results;
-    if (cfg->world > 1 && !simulate) {     // one NCCL communicator per context
+    if ((cfg->world > 1 && !simulate) || c->nccl_self) {     // one NCCL communicator per context
         std::string err;
         c->nccl = nccl_api(err);
         if (!c->nccl) return bail(fail(nullptr, MPDP_ERR_NCCL, err));
         ncclUniqueId id;
-        memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        if (c->nccl_self) {                // a 1-rank communicator of our own
+            if (c->nccl->GetUniqueId(&id) != 0) return bail(fail(nullptr, MPDP_ERR_NCCL, "ncclGetUniqueId failed"));
+        } else {
+            memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        }
         const ncclResult_t r = c->nccl->CommInitRank(&c->comm, cfg->world, id, cfg->rank);
         if (r != 0)
             return bail(fail(nullptr, MPDP_ERR_NCCL, std::string("ncclCommInitRank: ") +
@@ -1669,7 +1679,7 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
     if (count && (!graphs || !results)) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "graphs/results is NULL");
     CUDA_TRY(c, cudaSetDevice(c->device));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));     // pinned staging is reused
-    const bool batchable = c->world == 1 && c->timeout_ms <= 0 &&
+    const bool batchable = !c->multi && c->timeout_ms <= 0 &&
                            !(c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS |
                                          MPDP_FLAG_HASH_MEMO | MPDP_FLAG_FORCE_WIDE_MASKS | MPDP_FLAG_DPSUB_ENUM));
     std::vector<uint32_t> small;               // queries of the batched launch

@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kDfThreads, kStarMinBlocks) k_dp_star(const __
         binp[a * 33 + b] = make_uint2(bin[a * 33 + b + 1], bin[a * 33 + b + 1] - bin[a * 33 + b]);
     }
     __syncthreads();
-    const int n = p.n, hub = p.star_hub;
+    const int hub = p.star_hub;
     if (threadIdx.x >= kDfCompute) {
         df_control(p, StarSched{p, bin}, sh);
     } else {

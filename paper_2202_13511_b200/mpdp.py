@@ -70,6 +70,7 @@ FLAG_RANK_MEMO = 512
 FLAG_NO_SMALL = 1024
 FLAG_NO_CCC = 2048
 FLAG_NO_STAR = 4096
+FLAG_NCCL_SELF = 8192
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_optimize_batch", "mpdp_stage",
