@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seeds", type=int, default=3)
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config sub-results")
     return ap.parse_args()
 
 
@@ -132,12 +133,25 @@ def oracle_step(g):
     return r, dt
 
 
+def host_cpu():
+    """Host CPU model and core count (stated next to the oracle)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(graph):
     """The oracle as it stands (single-threaded DPccp), one full query."""
     r, dt = oracle_step(graph)
     return {"value": r.pairs_evaluated / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"1 full {graph.name} query, DPccp (oracle/oracle.c), {dt:.2f} s on 1 host core",
-            "seconds": dt}
+            "seconds": dt, **host_cpu()}, r
 
 
 def run_reference(args):
@@ -146,15 +160,18 @@ def run_reference(args):
         return 0
     topo, n = args.workload.rsplit("-", 1)
     n = int(n)
-    # bound the whole run to a few minutes: shrink the instance until one step fits
-    budget = 150.0 / max(1, args.steps + args.warmup)
+    # bound the whole run to a few minutes: the bench workload itself when its
+    # steps fit (star-25: ~4.5 s per query on one core, 25 steps ~2 minutes),
+    # else shrink the instance until one step fits
+    budget = 240.0 / max(1, args.steps + args.warmup)
     probe_n = min(n, 20)
     _, dt = oracle_step(W.generate(topo, probe_n, 0))
+    grow = 2.2 if topo != "clique" else 3.0
     est = dt
     m = probe_n
-    while m < n and est * (2.2 if topo != "clique" else 3.0) <= budget:
+    while m < n and est * grow <= budget:
         m += 1
-        est *= (2.2 if topo != "clique" else 3.0)
+        est *= grow
     graphs = [W.generate(topo, m, s) for s in range(args.seeds)]
     for i in range(args.warmup):
         oracle_step(graphs[i % len(graphs)])
@@ -172,7 +189,9 @@ def run_reference(args):
             "config": {"workload": f"{topo}-{m}", "requested_workload": args.workload,
                        "seeds": args.seeds, "oracle": "DPccp"},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} x {topo}-{m} queries (bounded from {args.workload})"},
+                             "sample": (f"{args.steps} x {topo}-{m} queries (seeds 0..{args.seeds - 1})"
+                                        + ("" if m == n else f", bounded from {args.workload}")),
+                             **host_cpu()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -180,6 +199,71 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+SUB_CONFIGS = ["star-10", "snowflake-20", "clique-18", "chain-20", "cycle-20"]
+
+
+def l2_copy_gbs(torch, dev, mb=24, reps=50):
+    """Measured L2 bandwidth: device copy of a 24 MB buffer into another one
+    (48 MB, resident in the 126 MB L2), read + write bytes per second."""
+    a = torch.empty(mb << 20, dtype=torch.uint8, device=dev)
+    b = torch.empty_like(a)
+    for _ in range(5):
+        b.copy_(a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        b.copy_(a)
+    e1.record()
+    torch.cuda.synchronize()
+    return 2 * (mb << 20) * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+def config_results(ctx, flush, stream, torch, mpdp, traffic_all, sm_hz, peak, steps=5):
+    """BASELINE configs 1, 2, 4 and the chain / cycle shapes north_star names:
+    device time of the staged launch (L2 flushed), pairs/s, the kernel's
+    roofline fractions, and an oracle check of the timed result."""
+    from oracle import pyoracle as O
+    out = []
+    l2 = None
+    for name in SUB_CONFIGS:
+        topo, n = name.rsplit("-", 1)
+        g = W.generate(topo, int(n), 0)
+        for _ in range(2):
+            ctx.mpdp_optimize(g)
+        ts = []
+        for _ in range(steps):
+            ctx.mpdp_stage(g)
+            flush.fill_(7)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.mpdp_run()
+            e1.record(stream)
+            r = ctx.mpdp_fetch()
+            ts.append(e0.elapsed_time(e1))
+        o = O.optimize_dpccp(g)
+        match = (r.cost == o.cost and r.tree() == O.tree_of(o.nodes) and r.csg_count == o.csg_count
+                 and r.ccp_pairs == o.ccp_pairs and r.pairs_evaluated == o.pairs_evaluated
+                 and r.level_pairs == o.level_pairs)
+        ms = statistics.median(ts)
+        sets = r.csg_count - g.n
+        d = {"workload": name, "ms": ms, "pairs": r.pairs_evaluated, "pairs_per_s": r.pairs_evaluated / (ms / 1e3),
+             "memo_kind": r.memo_kind, "kernel_ms": r.eval_ms, "oracle_match": bool(match)}
+        kern_s = r.eval_ms / 1e3
+        if kern_s > 0:
+            d["frac_hbm_survey_bytes"] = (16 * r.probes + 48 * sets) / kern_s / 1e9 / peak
+            tr = traffic_all.get(name) or {}
+            if tr.get("warp_inst"):
+                d["frac_issue"] = tr["warp_inst"] / kern_s / (148 * 4 * sm_hz)
+            if topo == "clique":             # the memo (2 MB) lives in L2: against a measured L2 bandwidth
+                l2 = l2 or l2_copy_gbs(torch, flush.device)
+                d["l2_gbs_measured"] = l2
+                d["frac_l2"] = (8 * r.probes + 20 * sets) / kern_s / 1e9 / l2
+        out.append(d)
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -234,6 +318,8 @@ def run_ours(args):
             e1.record(stream)
             r = ctx.mpdp_fetch()
             memo_kind = r.memo_kind
+            if i == 0:
+                first = r                     # checked against the oracle below (cpu_baseline leg)
             step_ms.append(e0.elapsed_time(e1))
             pairs_total += r.pairs_evaluated
             probes_total += r.probes
@@ -270,44 +356,72 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_value = e2e_pairs / e2e_s
 
-    # ---- roofline of the dominant kernel: the whole-query level-loop kernel
-    # (one launch per query does unrank, filter, compaction, evaluate, min and
-    # memo scatter for every level; k_dp_list for tree queries, k_dp_fused
-    # otherwise).  DESIGN.md §6: perfect-hash memo = 8 B cost per probe + per
-    # connected set 16 B level-list write + read (the compaction of P:889) and
-    # 8 B cost + 4 B left insert; open-addressing memo = 16 B slot per probe,
-    # per set list write + read + 16 B slot + left.
+    # ---- roofline of the dominant kernel (the whole-query level-loop kernel:
+    # k_dp_star for star-25, ~96% of the step).  DESIGN.md §6.
+    #   frac: SURVEY §8(d)'s per-unit algorithmic bytes (what a memo-table
+    #     design must move: 16 B per non-singleton probe, 16 B per connected set
+    #     of compaction write + read, 32 B per set of memo insert; star-25 4.03
+    #     GB) over the kernel's measured device time, against the measured HBM
+    #     copy bandwidth;
+    #   builder_bytes: the bytes this design's kernels actually address (8 B
+    #     per probe, per set the card(S \ max) read and the cost/card/left
+    #     write, no lists) -- most of it served by L2, see `traffic`;
+    #   issue: warp instructions per launch (ncu, profiles/traffic.json) over
+    #     148 SMs x 4 schedulers x the SM clock under load -- the bound that
+    #     binds this latency / issue-limited kernel.
     msz = 4 if n <= 32 else 8
-    if memo_kind == 4:                        # star: no level lists; card(S \ max) read + cost/card/left write
-        alg_bytes = 8 * probes_total + sets_total * (8 + 8 + 8 + 4)
-    elif memo_kind in (1, 2, 3):              # colex-rank or bitmask-indexed arrays: same bytes
-        alg_bytes = 8 * probes_total + sets_total * (16 + 8 + 4)
-    else:
-        alg_bytes = 16 * probes_total + sets_total * (2 * msz + 16 + msz)
-    kernel_name = {4: "k_dp_star (star queries: closed-form level indexing, one launch per query)",
-                   3: "k_dp_small (single CTA, shared-memory memo)"}.get(memo_kind) or (
-        "k_dp_list (tree queries: whole level loop, one launch per query)" if topo_is_tree
-        else "k_dp_fused / k_dp_clique (whole level loop, one launch per query)")
     peak, peak_kind = measured_peaks()
     kern_s = kernel_ms / 1e3
-    achieved = alg_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
+    launches_k = max(1, kernel_launches)
+    survey_bytes = 16 * probes_total + sets_total * (16 + 32)
+    if memo_kind == 4:                        # star: no level lists; card(S \ max) read + cost/card/left write
+        own_bytes = 8 * probes_total + sets_total * (8 + 8 + 8 + 4)
+    elif memo_kind in (1, 2, 3):              # colex-rank or bitmask-indexed arrays
+        own_bytes = 8 * probes_total + sets_total * (16 + 8 + 4)
+    else:
+        own_bytes = 16 * probes_total + sets_total * (2 * msz + 16 + msz)
+    kernel_name = {4: "k_dp_star (star queries: closed-form level indexing, dataflow level schedule)",
+                   3: "k_dp_small (single CTA, shared-memory memo)"}.get(memo_kind) or (
+        "k_dp_list (tree queries: whole level loop, one launch per query)" if topo_is_tree
+        else "k_dp_clique / k_dp_fused (whole level loop, one launch per query)")
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get(args.workload)
+    clk_now = clk.summary()
+    sm_hz = 1e6 * (clk_now.get("sm_mhz") or 1965.0)
+    achieved = survey_bytes / kern_s / 1e9 if kern_s > 0 else 0.0
     roof = {"bound": "hbm",
             "kernel": kernel_name,
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "bytes_basis": "SURVEY 8(d) per-unit algorithmic bytes: 16 B/probe + 48 B/connected set",
+            "algorithmic_bytes_per_launch": survey_bytes / launches_k,
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
             "traffic_source": traffic.get("source") if traffic else None,
             "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+            "builder_bytes": {"bytes_per_launch": own_bytes / launches_k,
+                              "achieved_gbs": own_bytes / kern_s / 1e9 if kern_s > 0 else 0.0,
+                              "frac": (own_bytes / kern_s / 1e9) / peak if kern_s > 0 else 0.0},
             "memo": {1: "perfect-hash (colex rank)", 2: "bitmask-indexed (MEMO_MASK)",
                      3: "shared-memory bitmask memo (single CTA)",
                      4: "star memo (leaf-set colex rank, C(n-1,k-1) per level)"}.get(
                 memo_kind, "murmur3 open addressing"),
-            "algorithmic_bytes_per_launch": alg_bytes / max(1, kernel_launches),
-            "avg_launch_ms": kernel_ms / max(1, kernel_launches),
+            "avg_launch_ms": kernel_ms / launches_k,
             "share_of_step": kernel_ms / max(1e-9, sum(step_ms))}
+    if traffic and traffic.get("warp_inst"):
+        t_launch = kernel_ms / launches_k / 1e3
+        rate = traffic["warp_inst"] / t_launch
+        roof["issue"] = {"warp_inst_per_launch": traffic["warp_inst"], "achieved_inst_per_s": rate,
+                         "peak_inst_per_s": 148 * 4 * sm_hz, "frac": rate / (148 * 4 * sm_hz),
+                         "source": traffic.get("source")}
+
+    # ---- the other BASELINE configurations: device time through the same
+    # staged launch, every result checked against the oracle in this run
+    others = []
+    if world == 1 and not args.no_configs:
+        others = config_results(ctx, flush, stream, torch, mpdp, traffic_all=(json.load(open(tfile))
+                                                                              if os.path.exists(tfile) else {}),
+                                sm_hz=sm_hz, peak=peak)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -316,14 +430,23 @@ def run_ours(args):
             "config": {"workload": args.workload, "seeds": args.seeds,
                        "pairs_per_query": pairs_total / args.steps,
                        "l2": "flushed between steps (256 MiB write)",
+                       "pairs_convention": "unordered join pairs (reading R3; SPEC's ordered count is 2x)",
                        "parallelism": f"level-sharded x{world} (NCCL allgather per level)" if world > 1 else "single-gpu",
                        "opt_time_ms_median": statistics.median(step_ms)},
-            "clocks": clk.summary(), "roofline": roof,
+            "clocks": clk_now, "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": 1e3 * e2e_s / args.steps},
             "gpu_launches": launches}
+    if others:
+        line["configs"] = others
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(graphs[0])
+        cb, o = cpu_baseline(graphs[0])
+        line["cpu_baseline"] = cb
+        from oracle import pyoracle as O
+        # the first timed step's result (seed 0) against the oracle's
+        line["oracle_match"] = bool(first.cost == o.cost and first.tree() == O.tree_of(o.nodes)
+                                    and first.csg_count == o.csg_count and first.ccp_pairs == o.ccp_pairs
+                                    and first.pairs_evaluated == o.pairs_evaluated)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

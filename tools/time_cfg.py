@@ -11,9 +11,11 @@ import workload as W  # noqa: E402
 from paper_2202_13511_b200 import mpdp  # noqa: E402
 
 args = sys.argv[1:]
-reps, env = 20, None
+reps, env, seeds = 20, None, [0]
 if "--reps" in args:
     i = args.index("--reps"); reps = int(args[i + 1]); del args[i:i + 2]
+if "--seeds" in args:
+    i = args.index("--seeds"); seeds = list(range(int(args[i + 1]))); del args[i:i + 2]
 if "--env" in args:
     i = args.index("--env"); env = args[i + 1]; del args[i:i + 2]
 variants = [None]
@@ -22,9 +24,9 @@ if env:
     variants = [(k, v) for v in vs.split(",")]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ctx = mpdp.Context(device=0, workspace_bytes=8 << 30)
-for name in args:
+for name, seed in [(a, sd) for a in args for sd in seeds]:
     topo, n = name.rsplit("-", 1)
-    g = W.generate(topo, int(n), 0)
+    g = W.generate(topo, int(n), seed)
     for var in variants:
         if var:
             os.environ[var[0]] = var[1]
@@ -46,7 +48,7 @@ for name in args:
         st, dn = (C.c_double * 64)(), (C.c_double * 64)()
         nn = ctx.L.mpdp_debug_level_span(ctx.h, st, dn, 64)
         lv = f"init {dn[0]:.0f} start {st[0]:.0f} " + " ".join(f"{k}:{st[k]:.0f}-{dn[k]:.0f}" for k in range(2, nn))
-        print(f"{name:12s} {str(var or ''):28s} {ms:8.4f} ms kernel(ev) {r.eval_ms:.4f}  min {min(ts):.4f}  {r.pairs_evaluated / ms / 1e6:8.2f} Gpairs/s"
+        print(f"{name:12s} s{seed} {str(var or ''):26s} {ms:8.4f} ms kernel(ev) {r.eval_ms:.4f}  min {min(ts):.4f}  {r.pairs_evaluated / ms / 1e6:8.2f} Gpairs/s"
               f"  levels(us): {lv}", flush=True)
         if var:
             del os.environ[var[0]]

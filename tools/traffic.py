@@ -21,7 +21,8 @@ else:
 data = json.load(open(out_init)) if os.path.exists(out_init) else {}
 for cfg in sys.argv[2:]:
     csvp = os.path.join(DIR, f"{tag}_traffic_{cfg}.csv")
-    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+           "smsp__inst_executed.sum,lts__t_sectors_srcunit_tex_op_read.sum",
            "--clock-control", "none", "-k", "regex:k_dp_", "--csv", "--log-file", csvp,
            sys.executable, os.path.join(ROOT, "tools", "profile_one.py"), cfg, "1"]
     subprocess.run(cmd, check=True, capture_output=True)
@@ -40,8 +41,11 @@ for cfg in sys.argv[2:]:
     last = per[max(per, key=int)]               # the measured (2nd) query's kernel
     rd, wr = last.get("dram__bytes_read.sum", 0.0), last.get("dram__bytes_write.sum", 0.0)
     data[cfg] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                 "warp_inst": last.get("smsp__inst_executed.sum"),
+                 "l2_read_sectors_from_l1": last.get("lts__t_sectors_srcunit_tex_op_read.sum"),
                  "kernel_ns_ncu": last.get("gpu__time_duration.sum"), "kernel": last["name"][:60],
                  "source": f"profiles/{tag}_traffic_{cfg}.csv: ncu --metrics dram__bytes_read.sum,"
-                           f"dram__bytes_write.sum (2nd query, {last['name'].split('<')[0]})"}
+                           f"dram__bytes_write.sum,smsp__inst_executed.sum (2nd query, "
+                           f"{last['name'].split('<')[0]})"}
     print(cfg, data[cfg])
 json.dump(data, open(out, "w"), indent=1)
