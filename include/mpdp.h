@@ -265,6 +265,20 @@ mpdp_status mpdp_subproblem_get(const mpdp_ctx* ctx, uint32_t i, mpdp_query_grap
 typedef mpdp_status (*mpdp_inner_solver)(void* user, const mpdp_query_graph* sub, mpdp_result* out);
 mpdp_status mpdp_heuristic_optimize(const mpdp_query_graph* graph, mpdp_algo algo, uint32_t k,
                                     mpdp_inner_solver solver, void* user, mpdp_result* out);
+/* As mpdp_heuristic_optimize, with UnionDP's partition threshold t (0 = k;
+ * IDP2 accepts only 0 or k). */
+mpdp_status mpdp_heuristic_optimize_t(const mpdp_query_graph* graph, mpdp_algo algo, uint32_t k, uint32_t t,
+                                      mpdp_inner_solver solver, void* user, mpdp_result* out);
+
+/* UnionDP with the GPU MPDP inner DP and a partition threshold t
+ * separate from k: partitions grow while their union has at most t relations
+ * ("upper threshold t in [1, k]"), the recursion stops once at most
+ * k composites remain (their exact plan is the root).  The paper's GPU runs
+ * use k = 25, t = 15.  t = 0 means t = k (mpdp_optimize's
+ * UNIONDP_MPDP).  Meaning, ownership and errors as mpdp_optimize; also
+ * INVALID_ARGUMENT unless 2 <= t <= k <= 32. */
+mpdp_status mpdp_optimize_uniondp(mpdp_ctx* ctx, const mpdp_query_graph* graph, uint32_t k, uint32_t t,
+                                  mpdp_result* out);
 
 /* Thread-local description of the last error on this context (never NULL). */
 const char* mpdp_last_error(const mpdp_ctx* ctx);

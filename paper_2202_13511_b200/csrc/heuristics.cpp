@@ -416,9 +416,12 @@ static int idp2(Driver& D, int k) {
 // graph has more than k nodes: weight every edge by the C_out cost of joining
 // its two endpoints; union-find over nodes, repeatedly uniting the two sets of
 // the edge with minimal (combined size, weight, edge id) among edges whose sets
-// differ and whose combined size is <= k; optimise each partition with the
-// inner DP; contract partitions into composite nodes; recurse.
-static int uniondp(Driver& D, int k) {
+// differ and whose combined size is <= t; optimise each partition with the
+// inner DP; contract partitions into composite nodes; recurse.  k bounds the
+// final exact DP (the recursion ends once <= k composites remain), t <= k the
+// partitions (the paper's upper threshold, "t in [1, k]"; its GPU
+// runs use k = 25, t = 15).  t = k is Alg. uniondp as listed.
+static int uniondp(Driver& D, int k, int t) {
     const Query& Q = D.Q;
     std::vector<int> node_of(Q.n);          // relation -> current composite index
     std::vector<int> comp;                  // composite -> pool root
@@ -474,7 +477,7 @@ static int uniondp(Driver& D, int k) {
             const int ra = find(ce[i].a), rb = find(ce[i].b);
             if (ra == rb) continue;                    // joined already
             const int s = sz[ra] + sz[rb];
-            if (s > k) continue;                       // can only grow: never valid again
+            if (s > t) continue;                       // can only grow: never valid again
             if (s != s0) {                             // stale size: re-key
                 pq.emplace(s, w0, id0, i);
                 continue;
@@ -620,7 +623,7 @@ static mpdp_status load(const mpdp_query_graph* g, Query& Q, std::string& err) {
 }
 
 mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolver solve, void* user,
-                mpdp_result* out, std::string& err, InnerBatchSolver solve_batch) {
+                mpdp_result* out, std::string& err, InnerBatchSolver solve_batch, uint32_t t) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!out) {
         err = "out is NULL";
@@ -628,6 +631,11 @@ mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolv
     }
     if (k < 2 || k > 32) {
         err = "k must be in [2, 32] for IDP2/UnionDP";
+        return MPDP_ERR_INVALID_ARGUMENT;
+    }
+    if (t == 0) t = k;
+    if (t < 2 || t > k) {
+        err = "t must be in [2, k] for UnionDP";
         return MPDP_ERR_INVALID_ARGUMENT;
     }
     // the drivers do O(n) host work per GOO merge / IDP2 iteration (scans of the
@@ -650,7 +658,7 @@ mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolv
     D.pool.reserve(8 * (size_t)n);
     int root;
     if (n == 1) root = D.leaf(0);
-    else root = (algo == MPDP_ALGO_IDP2_MPDP) ? idp2(D, (int)k) : uniondp(D, (int)k);
+    else root = (algo == MPDP_ALGO_IDP2_MPDP) ? idp2(D, (int)k) : uniondp(D, (int)k, (int)t);
     if (root < 0) {
         err = D.err.empty() ? "heuristic failed" : D.err;
         return MPDP_ERR_INTERNAL;

@@ -1333,14 +1333,31 @@ mpdp_status mpdp_subproblem_get(const mpdp_ctx* c, uint32_t i, mpdp_query_graph*
     return MPDP_OK;
 }
 
-mpdp_status mpdp_heuristic_optimize(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k,
-                                    mpdp_inner_solver solver, void* user, mpdp_result* out) {
+mpdp_status mpdp_heuristic_optimize_t(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, uint32_t t,
+                                      mpdp_inner_solver solver, void* user, mpdp_result* out) {
     if (!solver) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "solver is NULL");
     if (algo != MPDP_ALGO_IDP2_MPDP && algo != MPDP_ALGO_UNIONDP_MPDP)
         return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "algo must be IDP2_MPDP or UNIONDP_MPDP");
+    if (algo == MPDP_ALGO_IDP2_MPDP && t != 0 && t != k)
+        return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "t applies to UNIONDP_MPDP only");
     std::string err;
-    const mpdp_status st = mpdp_heur::run(g, algo, k, solver, user, out, err);
+    const mpdp_status st = mpdp_heur::run(g, algo, k, solver, user, out, err, nullptr, t);
     if (st != MPDP_OK) return fail(nullptr, st, err);
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_heuristic_optimize(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k,
+                                    mpdp_inner_solver solver, void* user, mpdp_result* out) {
+    return mpdp_heuristic_optimize_t(g, algo, k, 0, solver, user, out);
+}
+
+mpdp_status mpdp_optimize_uniondp(mpdp_ctx* c, const mpdp_query_graph* g, uint32_t k, uint32_t t, mpdp_result* out) {
+    if (!c) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!out) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "out is NULL");
+    c->subs.clear();
+    std::string err;
+    const mpdp_status st = mpdp_heur::run(g, MPDP_ALGO_UNIONDP_MPDP, k, gpu_inner_solver, c, out, err, gpu_inner_batch, t);
+    if (st != MPDP_OK) return fail(c, st, err.empty() ? c->err : err);
     return MPDP_OK;
 }
 

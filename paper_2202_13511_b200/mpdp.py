@@ -77,7 +77,7 @@ EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_optimiz
            "mpdp_run", "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
            "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace", "mpdp_subproblem_count",
            "mpdp_subproblem_get", "mpdp_heuristic_optimize", "mpdp_debug_level_span",
-           "mpdp_debug_df_stats"]
+           "mpdp_debug_df_stats", "mpdp_heuristic_optimize_t", "mpdp_optimize_uniondp"]
 
 _lib = None
 
@@ -108,6 +108,8 @@ def load_library(path: str = LIB_PATH):
                               C.POINTER(C.c_uint64)]),
         "mpdp_debug_level_span": (C.c_int, [P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int]),
         "mpdp_debug_df_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
+        "mpdp_optimize_uniondp": (C.c_int, [P, C.POINTER(mpdp_query_graph), C.c_uint32, C.c_uint32,
+                                            C.POINTER(mpdp_result)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -253,6 +255,12 @@ class Context:
         return rb.to_result()
 
     optimize = mpdp_optimize
+
+    def mpdp_optimize_uniondp(self, g, k: int = 25, t: int = 0) -> Result:
+        """UnionDP with partition threshold t (0 = k)."""
+        ga, rb = GraphArgs(g), ResultBuf(g.n)
+        self._check(self.L.mpdp_optimize_uniondp(self.h, ga.ref(), k, t, rb.ref()))
+        return rb.to_result()
 
     def mpdp_optimize_batch(self, graphs) -> List[Result]:
         """mpdp_optimize(MPDP) of independent queries; small tree queries share

@@ -151,3 +151,36 @@ def test_invalid_k_rejected():
     g = W.snowflake(20, 0)
     with pytest.raises(AssertionError):
         run(g, "UNIONDP_MPDP", 1)
+
+
+def run_t(g, algo, k, t):
+    L, mp = _lib()
+    L.mpdp_heuristic_optimize_t.restype = C.c_int
+    L.mpdp_heuristic_optimize_t.argtypes = [C.POINTER(mp.mpdp_query_graph), C.c_int, C.c_uint32, C.c_uint32,
+                                            SOLVER, C.c_void_p, C.POINTER(mp.mpdp_result)]
+    solver = Oracle(mp, k)
+    ga, rb = mp.GraphArgs(g), mp.ResultBuf(g.n)
+    st = L.mpdp_heuristic_optimize_t(ga.ref(), mp.ALGOS[algo], k, t, solver.cb, None, rb.ref())
+    return st, rb.to_result() if st == 0 else None, solver.subs
+
+
+@pytest.mark.parametrize("n,k,t,seed", [(60, 12, 6, 0), (120, 15, 8, 1), (300, 14, 14, 2)])
+def test_uniondp_partition_threshold(n, k, t, seed):
+    """UnionDP's upper threshold t: every partition of a
+    recursion level has at most t relations; only the final exact DP may hold up
+    to k composites; t = k is the algorithm as listed (= mpdp_heuristic_optimize)."""
+    g = W.snowflake(n, seed)
+    st, res, subs = run_t(g, "UNIONDP_MPDP", k, t)
+    assert st == 0
+    assert recompute(g, res) == res.cost
+    assert all(q.n <= t for q in subs[:-1]) and subs[-1].n <= k
+    if t == k:
+        ref, _ = run(g, "UNIONDP_MPDP", k)
+        assert ref.cost == res.cost and ref.tree() == res.tree()
+
+
+def test_uniondp_threshold_rejected():
+    g = W.snowflake(30, 0)
+    for algo, k, t in [("UNIONDP_MPDP", 10, 11), ("UNIONDP_MPDP", 10, 1), ("IDP2_MPDP", 10, 5)]:
+        st, _, _ = run_t(g, algo, k, t)
+        assert st == 1                        # MPDP_ERR_INVALID_ARGUMENT
