@@ -121,7 +121,10 @@ typedef struct {
                                            3 = shared-memory bitmask memo of the
                                                single-CTA small-query kernel,
                                            4 = star memo (k_dp_star: C(n-1,k-1)
-                                               entries per level, leaf-set rank) */
+                                               entries per level, leaf-set rank),
+                                           5 = the shared open-addressing memo of
+                                               a batch, 128-bit {sub-problem,
+                                               mask} keys (mpdp_optimize_batch) */
     uint32_t inner_calls;          /* out, IDP2/UnionDP: inner exact DP calls          */
     double* level_ms;              /* optional [n+1]: device time of each level (fused
                                       kernel: %globaltimer at the level barriers; 0 on
@@ -220,9 +223,12 @@ mpdp_status mpdp_optimize(mpdp_ctx* ctx, const mpdp_query_graph* graph, mpdp_alg
                           uint32_t k, mpdp_result* out);
 
 /* mpdp_optimize(MPDP) of `count` independent queries (e.g. the partitions of
- * one UnionDP level).  Small tree queries (n <= 13) are solved together by ONE
- * launch with one CTA per query (the single-CTA shared-memory kernel); the
- * others run one by one as mpdp_optimize.  graphs[i] / results[i] have the
+ * one UnionDP level).  Small tree queries (n <= 13) are solved
+ * together by ONE launch with one CTA per query (memo in shared memory);
+ * tree queries with 14 <= n <= 32 whose levels hold at most 6144 connected
+ * sets by a second launch, one CTA per query, all sharing ONE open-addressing
+ * memo in HBM keyed by 128-bit {sub-problem, relation mask} (memo_kind 5);
+ * the others run one by one as mpdp_optimize.  graphs[i] / results[i] have the
  * meaning, layout and ownership of mpdp_optimize's graph / out (results[i].nodes
  * caller-owned, capacity >= 2n-1); batched results report the launch's device
  * time.  Errors: as mpdp_optimize (the first one is returned; results of the

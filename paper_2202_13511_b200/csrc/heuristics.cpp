@@ -17,6 +17,8 @@
 // recomputed bottom-up over the final tree with this recurrence.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -59,6 +61,8 @@ struct Driver {
     std::string err;
 
     InnerBatchSolver solve_batch = nullptr;   // optional: independent sub-problems in one call
+    double solve_ms = 0;                      // host wall time inside the inner solver calls
+    unsigned long long batch_calls = 0, batched = 0;
 
     Driver(const Query& q, InnerSolver s, void* u) : Q(q), solve(s), user(u) {}
 
@@ -149,7 +153,9 @@ struct Driver {
         if (nodes.size() == 1) return nodes[0];
         SubGraph sg;
         prepare_sub(nodes, owner_of_rel_local, sg);
+        const auto t0 = std::chrono::steady_clock::now();
         const mpdp_status st = solve(user, &sg.g, &sg.r);
+        solve_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         calls++;
         if (st != MPDP_OK) {
             err = "inner DP failed (status " + std::to_string((int)st) + ")";
@@ -525,8 +531,12 @@ static int uniondp(Driver& D, int k, int t) {
                 gs.push_back(sg.g);
                 rs.push_back(sg.r);
             }
+            const auto t0 = std::chrono::steady_clock::now();
             const mpdp_status st = D.solve_batch(D.user, gs.data(), (uint32_t)gs.size(), rs.data());
+            D.solve_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
             D.calls += subs.size();
+            D.batch_calls++;
+            D.batched += subs.size();
             if (st != MPDP_OK) {
                 D.err = "inner DP batch failed (status " + std::to_string((int)st) + ")";
                 return -1;
@@ -534,7 +544,9 @@ static int uniondp(Driver& D, int k, int t) {
             for (size_t i = 0; i < subs.size(); i++) subs[i].r = rs[i];
         } else {
             for (auto& sg : subs) {
+                const auto t0 = std::chrono::steady_clock::now();
                 const mpdp_status st = D.solve(D.user, &sg.g, &sg.r);
+                D.solve_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
                 D.calls++;
                 if (st != MPDP_OK) {
                     D.err = "inner DP failed (status " + std::to_string((int)st) + ")";
@@ -663,6 +675,12 @@ mpdp_status run(const mpdp_query_graph* g, mpdp_algo algo, uint32_t k, InnerSolv
         err = D.err.empty() ? "heuristic failed" : D.err;
         return MPDP_ERR_INTERNAL;
     }
+    if (getenv("MPDP_DEBUG_HEUR_TIME"))
+        fprintf(stderr, "[heuristic] %s n=%d k=%u t=%u: %.2f ms total, %.2f ms in %llu inner calls (%llu batched in %llu "
+                        "batch calls)\n",
+                algo == MPDP_ALGO_IDP2_MPDP ? "IDP2" : "UnionDP", n, k, t,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), D.solve_ms,
+                D.calls, D.batched, D.batch_calls);
     // recompute card/cost bottom-up over the final tree and emit post-order
     std::vector<int> post;
     std::vector<std::pair<int, int>> st2{{root, 0}};

@@ -22,6 +22,7 @@
 #include "list_kernel.cuh"
 #include "small_kernel.cuh"
 #include "star_kernel.cuh"
+#include "batch128.cuh"
 #include "heuristics.h"
 
 using namespace mpdp;
@@ -161,6 +162,16 @@ struct mpdp_ctx {
     bool clique_df_attr = false;
     bool star = false;                    // last query ran k_dp_star (memo_kind 4)
     unsigned long long tree_max_level = 0;  // tree queries: largest level (connected sets of one size)
+    unsigned long long tree_csg = 0;        // tree queries: connected sets (subtree count)
+    // mpdp_optimize_batch, mid-size tree sub-problems: one CTA each, a shared
+    // memo with 128-bit {sub-problem, mask} keys (batch128.cuh)
+    Key128* b_keys = nullptr;
+    Val128* b_vals = nullptr;
+    unsigned long long b_cap = 0;
+    unsigned int b_epoch = 0;
+    unsigned int* d_sub_ids = nullptr;
+    unsigned int* h_sub_ids = nullptr;
+    bool batch128_attr = false;
     bool fused = false;                  // last run used the fused kernel
     // the level descriptors are zero (the dataflow kernels leave them zeroed;
     // every k_init-based path leaves them dirty): the star / clique dataflow
@@ -339,7 +350,11 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
             f[v].swap(a);
         }
         c->tree_max_level = 0;
-        for (int x = 2; x <= n; x++) c->tree_max_level = std::max(c->tree_max_level, cnt[x]);
+        c->tree_csg = (unsigned long long)n;
+        for (int x = 2; x <= n; x++) {
+            c->tree_max_level = std::max(c->tree_max_level, cnt[x]);
+            c->tree_csg += cnt[x];
+        }
         c->star_hub = -1;
         for (int v = 0; v < n && n >= 3; v++)
             if (__builtin_popcountll(adj[v]) == n - 1) c->star_hub = v;
@@ -1488,6 +1503,10 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (c->h_br) cudaFreeHost(c->h_br);
     if (c->d_bq) cudaFree(c->d_bq);
     if (c->d_br) cudaFree(c->d_br);
+    if (c->b_keys) cudaFree(c->b_keys);
+    if (c->b_vals) cudaFree(c->b_vals);
+    if (c->d_sub_ids) cudaFree(c->d_sub_ids);
+    if (c->h_sub_ids) cudaFreeHost(c->h_sub_ids);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     for (auto& e : c->kev)
@@ -1699,8 +1718,11 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
     const bool batchable = !c->multi && c->timeout_ms <= 0 &&
                            !(c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS |
                                          MPDP_FLAG_HASH_MEMO | MPDP_FLAG_FORCE_WIDE_MASKS | MPDP_FLAG_DPSUB_ENUM));
-    std::vector<uint32_t> small;               // queries of the batched launch
-    std::vector<std::vector<unsigned long long>> adjs;
+    // three kinds: small trees (n <= 13: one CTA each, memo in shared memory),
+    // mid-size trees (n <= 32, every level <= kBatchListCap sets: one CTA each,
+    // the shared 128-bit-key memo), everything else one by one
+    std::vector<uint32_t> small, mid;
+    std::vector<std::vector<unsigned long long>> adj_small, adj_mid;
     for (uint32_t i = 0; i < count; i++) {
         std::vector<unsigned long long> adj;
         const mpdp_status st = validate(c, &graphs[i], adj);
@@ -1709,59 +1731,124 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
         if (results[i].nodes && results[i].capacity < (uint32_t)(2 * n - 1))
             return fail(c, MPDP_ERR_INVALID_ARGUMENT, "result capacity < 2n-1");
         const bool tree = n >= 2 && graphs[i].n_edges == (uint32_t)(n - 1);
-        if (batchable && tree && n <= kSmallMaxN) {
+        if (!batchable || !tree) continue;
+        if (n <= kSmallMaxN) {
             small.push_back(i);
-            adjs.push_back(std::move(adj));
+            adj_small.push_back(std::move(adj));
+        } else if (n <= kBatchMaxN) {
+            mid.push_back(i);
+            adj_mid.push_back(std::move(adj));
         }
     }
-    if (!small.empty()) {
-        const uint32_t nb = (uint32_t)small.size();
-        if (nb > c->batch_cap) {                // grow the staging
-            if (c->h_bq) cudaFreeHost(c->h_bq);
-            if (c->h_br) cudaFreeHost(c->h_br);
-            if (c->d_bq) cudaFree(c->d_bq);
-            if (c->d_br) cudaFree(c->d_br);
-            c->h_bq = nullptr;
-            c->h_br = nullptr;
-            c->d_bq = nullptr;
-            c->d_br = nullptr;
-            c->batch_cap = 0;
-            const uint32_t cap = std::max<uint32_t>(nb, 64);
-            if (cudaMallocHost(&c->h_bq, sizeof(QueryDev<uint32_t>) * cap) != cudaSuccess ||
-                cudaMallocHost(&c->h_br, sizeof(ResultDev) * cap) != cudaSuccess ||
-                cudaMalloc(&c->d_bq, sizeof(QueryDev<uint32_t>) * cap) != cudaSuccess ||
-                cudaMalloc(&c->d_br, sizeof(ResultDev) * cap) != cudaSuccess)
-                return fail(c, MPDP_ERR_OOM, "batch staging allocation failed");
-            c->batch_cap = cap;
+    const uint32_t ns = (uint32_t)small.size();
+    // fill_query writes per-query context fields (n, class, width, star hub,
+    // largest tree level, csg): the batch restores them afterwards
+    const int saved_n = c->n, saved_cls = c->cls, saved_hub = c->star_hub;
+    const bool saved_wide = c->wide;
+    const unsigned long long saved_tml = c->tree_max_level, saved_csg = c->tree_csg;
+    std::vector<uint32_t> mid_ok;                        // mid trees whose levels fit the lists
+    std::vector<unsigned long long> mid_csg;
+    if (ns + mid.size() > c->batch_cap) {                // grow the staging
+        if (c->h_bq) cudaFreeHost(c->h_bq);
+        if (c->h_br) cudaFreeHost(c->h_br);
+        if (c->d_bq) cudaFree(c->d_bq);
+        if (c->d_br) cudaFree(c->d_br);
+        if (c->h_sub_ids) cudaFreeHost(c->h_sub_ids);
+        if (c->d_sub_ids) cudaFree(c->d_sub_ids);
+        c->h_bq = nullptr;
+        c->h_br = nullptr;
+        c->d_bq = nullptr;
+        c->d_br = nullptr;
+        c->h_sub_ids = nullptr;
+        c->d_sub_ids = nullptr;
+        c->batch_cap = 0;
+        const uint32_t cap = std::max<uint32_t>(ns + (uint32_t)mid.size(), 64);
+        if (cudaMallocHost(&c->h_bq, sizeof(QueryDev<uint32_t>) * cap) != cudaSuccess ||
+            cudaMallocHost(&c->h_br, sizeof(ResultDev) * cap) != cudaSuccess ||
+            cudaMallocHost(&c->h_sub_ids, sizeof(unsigned int) * cap) != cudaSuccess ||
+            cudaMalloc(&c->d_bq, sizeof(QueryDev<uint32_t>) * cap) != cudaSuccess ||
+            cudaMalloc(&c->d_br, sizeof(ResultDev) * cap) != cudaSuccess ||
+            cudaMalloc(&c->d_sub_ids, sizeof(unsigned int) * cap) != cudaSuccess)
+            return fail(c, MPDP_ERR_OOM, "batch staging allocation failed");
+        c->batch_cap = cap;
+    }
+    int maxn = 2;
+    for (uint32_t b = 0; b < ns; b++) {
+        const mpdp_query_graph& g = graphs[small[b]];
+        c->n = (int)g.n;
+        c->cls = CLS_TREE;
+        c->wide = false;
+        fill_query<uint32_t>(c, &g, adj_small[b], c->h_bq + b);
+        maxn = std::max(maxn, (int)g.n);
+    }
+    unsigned long long csg_total = 0;
+    for (size_t b = 0; b < mid.size(); b++) {
+        const mpdp_query_graph& g = graphs[mid[b]];
+        c->n = (int)g.n;
+        c->cls = CLS_TREE;
+        c->wide = false;
+        const uint32_t at = ns + (uint32_t)mid_ok.size();
+        fill_query<uint32_t>(c, &g, adj_mid[b], c->h_bq + at);
+        if (c->tree_max_level > (unsigned long long)kBatchListCap) continue;   // one by one
+        c->h_sub_ids[at] = (uint32_t)mid_ok.size();
+        mid_ok.push_back(mid[b]);
+        mid_csg.push_back(c->tree_csg);
+        csg_total += c->tree_csg;
+    }
+    c->n = saved_n;
+    c->cls = saved_cls;
+    c->wide = saved_wide;
+    c->star_hub = saved_hub;
+    c->tree_max_level = saved_tml;
+    c->tree_csg = saved_csg;
+    const uint32_t nm = (uint32_t)mid_ok.size();
+    if (nm) {                                            // the shared memo: load factor <= 0.5
+        unsigned long long cap = 1024;
+        while (cap < 2 * csg_total) cap <<= 1;
+        if (cap > c->b_cap) {
+            if (c->b_keys) cudaFree(c->b_keys);
+            if (c->b_vals) cudaFree(c->b_vals);
+            c->b_keys = nullptr;
+            c->b_vals = nullptr;
+            c->b_cap = 0;
+            if (cudaMalloc(&c->b_keys, sizeof(Key128) * cap) != cudaSuccess ||
+                cudaMalloc(&c->b_vals, sizeof(Val128) * cap) != cudaSuccess)
+                return fail(c, MPDP_ERR_OOM, "batch memo allocation failed");
+            CUDA_TRY(c, cudaMemsetAsync(c->b_keys, 0, sizeof(Key128) * cap, c->stream));
+            c->b_cap = cap;
+            c->b_epoch = 0;
         }
-        // fill_query writes per-query context fields (n, class, width, star hub,
-        // largest tree level): the batch restores them afterwards
-        const int saved_n = c->n, saved_cls = c->cls, saved_hub = c->star_hub;
-        const bool saved_wide = c->wide;
-        const unsigned long long saved_tml = c->tree_max_level;
-        int maxn = 2;
-        for (uint32_t b = 0; b < nb; b++) {
-            const mpdp_query_graph& g = graphs[small[b]];
-            c->n = (int)g.n;
-            c->cls = CLS_TREE;
-            c->wide = false;
-            fill_query<uint32_t>(c, &g, adjs[b], c->h_bq + b);
-            maxn = std::max(maxn, (int)g.n);
+        if (++c->b_epoch >= (1u << 31)) {                // epochs wrapped: clear once
+            CUDA_TRY(c, cudaMemsetAsync(c->b_keys, 0, sizeof(Key128) * c->b_cap, c->stream));
+            c->b_epoch = 1;
         }
-        c->n = saved_n;
-        c->cls = saved_cls;
-        c->wide = saved_wide;
-        c->star_hub = saved_hub;
-        c->tree_max_level = saved_tml;
-        if (!c->batch_attr) {
-            CUDA_TRY(c, cudaFuncSetAttribute(k_dp_small_batch<CLS_TREE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)small_smem_bytes(kSmallMaxN)));
-            c->batch_attr = true;
-        }
+    }
+    const uint32_t nb = ns + nm;
+    if (nb) {
         CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
         CUDA_TRY(c, cudaMemcpyAsync(c->d_bq, c->h_bq, sizeof(QueryDev<uint32_t>) * nb, cudaMemcpyHostToDevice, c->stream));
-        k_dp_small_batch<CLS_TREE><<<nb, kSmallBlock, small_smem_bytes(maxn), c->stream>>>(c->d_bq, c->d_br);
-        CUDA_TRY(c, cudaGetLastError());
+        if (ns) {
+            if (!c->batch_attr) {
+                CUDA_TRY(c, cudaFuncSetAttribute(k_dp_small_batch<CLS_TREE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)small_smem_bytes(kSmallMaxN)));
+                c->batch_attr = true;
+            }
+            k_dp_small_batch<CLS_TREE><<<ns, kSmallBlock, small_smem_bytes(maxn), c->stream>>>(c->d_bq, c->d_br);
+            CUDA_TRY(c, cudaGetLastError());
+        }
+        if (nm) {
+            if (!c->batch128_attr) {
+                CUDA_TRY(c, cudaFuncSetAttribute(k_dp_tree_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)batch128_smem_bytes()));
+                c->batch128_attr = true;
+            }
+            CUDA_TRY(c, cudaMemcpyAsync(c->d_sub_ids + ns, c->h_sub_ids + ns, sizeof(unsigned int) * nm,
+                                        cudaMemcpyHostToDevice, c->stream));
+            Memo128 m{c->b_keys, c->b_vals, c->b_cap - 1, c->b_epoch};
+            k_dp_tree_batch<<<nm, kBatchBlock, batch128_smem_bytes(), c->stream>>>(c->d_bq + ns, c->d_br + ns, m,
+                                                                                c->d_sub_ids + ns);
+            CUDA_TRY(c, cudaGetLastError());
+        }
         CUDA_TRY(c, cudaMemcpyAsync(c->h_br, c->d_br, sizeof(ResultDev) * nb, cudaMemcpyDeviceToHost, c->stream));
         CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
         CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1769,9 +1856,13 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
         cudaEventElapsedTime(&ms, c->ev0, c->ev1);
         for (uint32_t b = 0; b < nb; b++) {
             const ResultDev* r = c->h_br + b;
-            mpdp_result* out = &results[small[b]];
-            const int n = (int)graphs[small[b]].n;
-            if (r->error) return fail(c, MPDP_ERR_INTERNAL, "device consistency check failed in a batched query");
+            const uint32_t qi = b < ns ? small[b] : mid_ok[b - ns];
+            mpdp_result* out = &results[qi];
+            const int n = (int)graphs[qi].n;
+            if (r->error) return fail(c, MPDP_ERR_INTERNAL, "device consistency check failed in a batched query (bits " +
+                                             std::to_string(r->error) + ")");
+            if (b >= ns && r->csg != mid_csg[b - ns])
+                return fail(c, MPDP_ERR_INTERNAL, "batched tree query: connected sets differ from the subtree count");
             out->time_ms = ms;                  // the whole batched launch
             out->n_nodes = r->n_nodes;
             out->root = r->n_nodes ? r->n_nodes - 1 : 0;
@@ -1785,7 +1876,7 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
             out->d2h_bytes = sizeof(ResultDev);
             out->enum_launches = 0;
             out->eval_launches = 1;
-            out->memo_kind = 3u;
+            out->memo_kind = b < ns ? 3u : 5u;
             out->inner_calls = 0;
             out->enum_ms = 0;
             out->eval_ms = ms;
@@ -1799,15 +1890,22 @@ mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uin
         }
     }
     // the rest one by one
-    size_t j = 0;
+    std::vector<char> done(count, 0);
+    for (uint32_t i : small) done[i] = 1;
+    for (uint32_t i : mid_ok) done[i] = 1;
+    const auto t1 = std::chrono::steady_clock::now();
+    unsigned int singles = 0, max_single_n = 0;
     for (uint32_t i = 0; i < count; i++) {
-        if (j < small.size() && small[j] == i) {
-            j++;
-            continue;
-        }
+        if (done[i]) continue;
         const mpdp_status st = mpdp_optimize(c, &graphs[i], MPDP_ALGO_MPDP, 0, &results[i]);
         if (st != MPDP_OK) return st;
+        singles++;
+        max_single_n = std::max(max_single_n, graphs[i].n);
     }
+    if (getenv("MPDP_DEBUG_HEUR_TIME"))
+        fprintf(stderr, "[batch] %u queries: %u small + %u mid in %.3f ms device time, %u one by one (max n %u) in %.3f ms\n",
+                count, ns, nm, nb ? results[ns ? small[0] : mid_ok[0]].time_ms : 0.0, singles, max_single_n,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
     // a batch replaces whatever mpdp_stage had staged (the one-by-one queries
     // restage the context): a later mpdp_run / mpdp_fetch must restage first
     c->staged = false;

@@ -310,9 +310,34 @@ def test_optimize_batch(ctx):
         check(r, o, g)
         r1 = ctx.mpdp_optimize(g)
         assert r.tree() == r1.tree() and r.cost == r1.cost
-        small = len(g.edges) == g.n - 1 and g.n <= 13
-        assert (r.memo_kind == 3) == small, (g.name, r.memo_kind)
+        tree = len(g.edges) == g.n - 1
+        assert (r.memo_kind == 3) == (tree and g.n <= 13), (g.name, r.memo_kind)
+        # mid-size trees whose levels fit the kernel's shared-memory lists
+        assert (r.memo_kind == 5) == (tree and 14 <= g.n <= 32 and max(o.level_csg) <= 6144), (g.name, r.memo_kind)
     assert ctx.mpdp_optimize_batch([]) == []
+
+
+def test_optimize_batch_128bit_memo(ctx):
+    """Mid-size tree sub-problems (14 <= n <= 32) of one batch share ONE memo
+    keyed by 128-bit {sub-problem, mask} (memo_kind 5); every result equals the
+    oracle's, also with composite leaf costs, across repeated batches (stale
+    slots of earlier batches are reused through the epoch) and with the same
+    graph twice in one batch (same masks, different sub-problem keys)."""
+    rng = random.Random(128)
+    gs = []
+    for i in range(24):
+        topo = rng.choice(["snowflake", "chain", "star"])
+        g = W.generate(topo, rng.randint(14, 22 if topo != "star" else 15), 500 + i)   # (star-15: 3432 sets per level at most)
+        if rng.random() < 0.5:
+            g.leaf_cost = [float(rng.choice([0, 3, 250, 1e4])) for _ in range(g.n)]
+        gs.append(g)
+    gs.append(gs[0])
+    oracle = [O.optimize(g) for g in gs]
+    for rep in range(3):
+        rs = ctx.mpdp_optimize_batch(gs if rep != 1 else gs[::-1])
+        for g, o, r in zip(gs if rep != 1 else gs[::-1], oracle if rep != 1 else oracle[::-1], rs):
+            assert r.memo_kind == 5, (g.name, r.memo_kind)
+            check(r, o, g)
 
 
 def test_small_kernel_leaf_costs_and_dpsub():

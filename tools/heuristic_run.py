@@ -18,10 +18,12 @@ with mpdp.Context(device=0, workspace_bytes=4 << 30, flags=mpdp.FLAG_RECORD_SUBP
     for seed in range(seeds):
         g = W.snowflake(n, seed)
         goo = ctx.mpdp_optimize(g, algo="IDP2_MPDP", k=2)
-        for algo in ("IDP2_MPDP", "UNIONDP_MPDP"):
-            ctx.mpdp_optimize(g, algo=algo, k=k)        # warm
+        for algo, t_part in (("IDP2_MPDP", 0), ("UNIONDP_MPDP", 0), ("UNIONDP_MPDP", 15)):
+            run = (lambda: ctx.mpdp_optimize(g, algo=algo, k=k)) if t_part == 0 else \
+                (lambda: ctx.mpdp_optimize_uniondp(g, k=k, t=t_part))
+            run()                                        # warm
             t = time.perf_counter()
-            r = ctx.mpdp_optimize(g, algo=algo, k=k)
+            r = run()
             dt = time.perf_counter() - t
             nsub = L.mpdp_subproblem_count(ctx.h)
             sizes = []
@@ -29,6 +31,6 @@ with mpdp.Context(device=0, workspace_bytes=4 << 30, flags=mpdp.FLAG_RECORD_SUBP
                 sg = mpdp.mpdp_query_graph()
                 L.mpdp_subproblem_get(ctx.h, i, C.byref(sg), None)
                 sizes.append(sg.n)
-            print(f"seed {seed} {algo:13s} n={n} k={k}: {dt*1e3:8.1f} ms, cost {r.cost:.6g} "
+            print(f"seed {seed} {algo:13s} n={n} k={k} t={t_part or k}: {dt*1e3:8.1f} ms, cost {r.cost:.6g} "
                   f"(GOO {goo.cost:.6g}, ratio {r.cost/goo.cost if goo.cost else float('nan'):.4f}), "
                   f"inner calls {r.inner_calls}, max sub n {max(sizes)}, pairs {r.pairs_evaluated}", flush=True)
