@@ -232,8 +232,12 @@ mpdp_status mpdp_optimize(mpdp_ctx* ctx, const mpdp_query_graph* graph, mpdp_alg
  * meaning, layout and ownership of mpdp_optimize's graph / out (results[i].nodes
  * caller-owned, capacity >= 2n-1); batched results report the launch's device
  * time.  Errors: as mpdp_optimize (the first one is returned; results of the
- * queries before it are valid).  Not for world > 1 contexts' sharded queries
- * (those run one by one).  A batch replaces any query staged by mpdp_stage:
+ * queries before it are valid).  Multi-GPU contexts (world > 1 over NCCL):
+ * rank r solves the queries i = r (mod world) with the single-GPU kernels and
+ * the ranks allgather the results (plan, cost, counters; the optional level
+ * arrays are not exchanged), so every rank returns every result -- UnionDP's
+ * independent partitions run on different GPUs.  A batch replaces
+ * any query staged by mpdp_stage:
  * mpdp_run / mpdp_fetch after it fail with INVALID_ARGUMENT until the next
  * mpdp_stage.                                                                   */
 mpdp_status mpdp_optimize_batch(mpdp_ctx* ctx, const mpdp_query_graph* graphs, uint32_t count,

@@ -119,6 +119,10 @@ template <typename M> struct Params {
     unsigned long long zero_words;         // k_init: bdone[0 .. zero_words) cleared (clique merge counts)
     int mask_leaves;                       // k_init: level-1 entries of the bitmask memo (cliques)
     unsigned long long* df_stats;          // debug (MPDP_DEBUG_DF_STATS): per CTA 8 timing words, else null
+    // sharded runs (multi-GPU, §8): only the memo COSTS are exchanged; card(S)
+    // is recomputed locally (reading R5's fold) and the chosen split of a
+    // plan node is re-derived at extraction from the replicated costs
+    int shard_local;
 };
 
 // ------------------------------------------------------------- mem helpers

@@ -1034,7 +1034,7 @@ static mpdp_status run_small(mpdp_ctx* c, const Params<uint32_t>& p) {
 constexpr unsigned long long kShardMinRanks = 1ull << 14;
 
 static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k, unsigned long long C,
-                                  unsigned long long seg, bool with_card, unsigned long long off) {
+                                  unsigned long long seg, bool with_card, unsigned long long off, bool with_left) {
     const int W = c->world;
     if (c->simulate) {
         for (int s = 0; s < W; s++) {
@@ -1044,8 +1044,9 @@ static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k,
                 if (t == s) continue;
                 CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dcost + off + lo, P[s].memo.dcost + off + lo, (hi - lo) * 8,
                                             cudaMemcpyDeviceToDevice, c->stream));
-                CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dleft + off + lo, P[s].memo.dleft + off + lo, (hi - lo) * 4,
-                                            cudaMemcpyDeviceToDevice, c->stream));
+                if (with_left)
+                    CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dleft + off + lo, P[s].memo.dleft + off + lo, (hi - lo) * 4,
+                                                cudaMemcpyDeviceToDevice, c->stream));
                 if (with_card)
                     CUDA_TRY(c, cudaMemcpyAsync(P[t].memo.dcard + off + lo, P[s].memo.dcard + off + lo, (hi - lo) * 8,
                                                 cudaMemcpyDeviceToDevice, c->stream));
@@ -1057,7 +1058,7 @@ static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k,
     unsigned int* dl = P[0].memo.dleft + off;
     ncclResult_t r = c->nccl->GroupStart();
     if (!r) r = c->nccl->AllGather(dc + c->rank * seg, dc, seg, kNcclFloat64, c->comm, c->stream);
-    if (!r) r = c->nccl->AllGather(dl + c->rank * seg, dl, seg, kNcclUint32, c->comm, c->stream);
+    if (!r && with_left) r = c->nccl->AllGather(dl + c->rank * seg, dl, seg, kNcclUint32, c->comm, c->stream);
     double* dk = P[0].memo.dcard + off;    // card(S \ max) feeds card_fast (trees, cliques)
     if (!r && with_card) r = c->nccl->AllGather(dk + c->rank * seg, dk, seg, kNcclFloat64, c->comm, c->stream);
     const ncclResult_t r2 = c->nccl->GroupEnd();
@@ -1101,6 +1102,7 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     for (int sh = 0; sh < nsh; sh++) {
         P[sh] = make_params<uint32_t>(c, sh);
         P[sh].timeout_ns = 0;              // (the sharded host loop has no device deadline)
+        P[sh].shard_local = star ? 1 : 0;
         k_init<uint32_t><<<1, 256, 0, c->stream>>>(P[sh]);
         c->launches++;
     }
@@ -1137,8 +1139,12 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
             if (st != MPDP_OK) return st;
         }
         if (sharded) {
-            // cards: card(S \ max) of the next level and the extraction read them
-            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, true, star ? P[0].star_off[k] : P[0].dense_off[k]);
+            // star: costs only (8 B per set; card(S) is recomputed locally and
+            // the extraction re-derives the chosen splits from the costs);
+            // others: costs, left masks and cards (card(S \ max) of the next
+            // level and the extraction read them)
+            const mpdp_status st = exchange_level(c, P.data(), k, C, seg, !star, star ? P[0].star_off[k] : P[0].dense_off[k],
+                                                  !star);
             if (st != MPDP_OK) return st;
         }
         CUDA_TRY(c, cudaGetLastError());
@@ -1277,7 +1283,22 @@ extern "C" mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpd
 // inner exact DP of IDP2/UnionDP: the GPU MPDP on the same context
 static mpdp_status gpu_inner_solver(void* user, const mpdp_query_graph* sub, mpdp_result* out) {
     mpdp_ctx* c = static_cast<mpdp_ctx*>(user);
+    // multi-GPU contexts: a sequential inner DP (IDP2's iterations depend on
+    // each other) of <= 32 relations runs redundantly on every rank
+    // with the single-GPU kernels -- per-level sharding of such small DPs
+    // would pay a collective per level for microseconds of work; independent
+    // sub-problems go through the distributed batch instead
+    const bool sm = c->multi, sn = c->nccl_self;
+    const int sw = c->world;
+    if (c->multi && !c->simulate) {
+        c->multi = false;
+        c->nccl_self = false;
+        c->world = 1;
+    }
     const mpdp_status st = mpdp_optimize(c, sub, MPDP_ALGO_MPDP, 0, out);
+    c->multi = sm;
+    c->nccl_self = sn;
+    c->world = sw;
     if (st == MPDP_OK && (c->flags & MPDP_FLAG_RECORD_SUBPROBLEMS)) {
         mpdp_ctx::SubProblem sp;
         sp.card.assign(sub->cardinalities, sub->cardinalities + sub->n);
@@ -1710,10 +1731,102 @@ mpdp_status mpdp_optimize(mpdp_ctx* c, const mpdp_query_graph* g, mpdp_algo algo
     return mpdp_fetch(c, out);
 }
 
+// Multi-GPU batch (independent sub-problems, e.g. one UnionDP level's
+// partitions): rank r solves the queries i = r (mod W) with the
+// single-GPU kernels and the ranks allgather the results (plan, cost,
+// counters) over NCCL, so every rank returns every result.
+struct BatchRec {
+    double cost, time_ms;
+    unsigned long long csg, ccp, pairs, probes;
+    unsigned int n_nodes, memo_kind, gpu_launches, status;
+    mpdp_plan_node nodes[2 * kMaxN - 1];
+};
+
+static mpdp_status batch_distributed(mpdp_ctx* c, const mpdp_query_graph* graphs, uint32_t count,
+                                     mpdp_result* results) {
+    const int W = c->nccl_self ? 1 : c->world, rank = c->nccl_self ? 0 : c->rank;
+    std::vector<mpdp_query_graph> lg;
+    std::vector<mpdp_result> lr;
+    std::vector<uint32_t> li;
+    for (uint32_t i = (uint32_t)rank; i < count; i += (uint32_t)W) {
+        li.push_back(i);
+        lg.push_back(graphs[i]);
+        lr.push_back(results[i]);
+    }
+    const bool sm = c->multi, sn = c->nccl_self;
+    const int sw = c->world;
+    c->multi = false;                      // this rank's share on the single-GPU kernels
+    c->nccl_self = false;
+    c->world = 1;
+    const mpdp_status st = li.empty() ? MPDP_OK : mpdp_optimize_batch(c, lg.data(), (uint32_t)lg.size(), lr.data());
+    c->multi = sm;
+    c->nccl_self = sn;
+    c->world = sw;
+    const unsigned long long seg = (count + (uint32_t)W - 1) / (uint32_t)W;
+    std::vector<BatchRec> mine(seg);
+    memset(mine.data(), 0, sizeof(BatchRec) * seg);
+    for (size_t j = 0; j < li.size(); j++) {
+        BatchRec& b = mine[j];
+        const mpdp_result& r = lr[j];
+        b.status = (unsigned int)st;
+        if (st != MPDP_OK) continue;
+        b.cost = r.cost;
+        b.time_ms = r.time_ms;
+        b.csg = r.csg_count;
+        b.ccp = r.ccp_pairs;
+        b.pairs = r.pairs_evaluated;
+        b.probes = r.probes;
+        b.n_nodes = r.n_nodes;
+        b.memo_kind = r.memo_kind;
+        b.gpu_launches = r.gpu_launches;
+        if (r.nodes) memcpy(b.nodes, r.nodes, sizeof(mpdp_plan_node) * std::min<uint32_t>(r.n_nodes, 2 * kMaxN - 1));
+        else b.n_nodes = 0;
+    }
+    if (st != MPDP_OK && W == 1) return st;
+    // allgather of the fixed-size records (device staging)
+    const size_t bytes = sizeof(BatchRec) * seg;
+    unsigned char* d = nullptr;
+    CUDA_TRY(c, cudaMalloc(&d, bytes * W));
+    std::vector<BatchRec> all(seg * W);
+    mpdp_status out = MPDP_OK;
+    if (cudaMemcpyAsync(d + bytes * rank, mine.data(), bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+        out = fail(c, MPDP_ERR_CUDA, "batch record upload failed");
+    } else {
+        ncclResult_t e = c->nccl->AllGather(d + bytes * rank, d, bytes, /*ncclInt8*/ 0, c->comm, c->stream);
+        if (e) out = fail(c, MPDP_ERR_NCCL, "ncclAllGather of the batch results failed");
+        else if (cudaMemcpyAsync(all.data(), d, bytes * W, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                 cudaStreamSynchronize(c->stream) != cudaSuccess)
+            out = fail(c, MPDP_ERR_CUDA, "batch record download failed");
+    }
+    cudaFree(d);
+    if (out != MPDP_OK) return out;
+    for (uint32_t i = 0; i < count; i++) {
+        const BatchRec& b = all[(i % (uint32_t)W) * seg + i / (uint32_t)W];
+        if (b.status != MPDP_OK) return fail(c, (mpdp_status)b.status, "a batched query failed on rank " + std::to_string(i % W));
+        mpdp_result& r = results[i];
+        r.cost = b.cost;
+        r.time_ms = b.time_ms;
+        r.csg_count = b.csg;
+        r.ccp_pairs = b.ccp;
+        r.pairs_evaluated = b.pairs;
+        r.probes = b.probes;
+        r.n_nodes = b.n_nodes;
+        r.root = b.n_nodes ? b.n_nodes - 1 : 0;
+        r.memo_kind = b.memo_kind;
+        r.gpu_launches = b.gpu_launches;
+        r.inner_calls = 0;
+        if (r.nodes) memcpy(r.nodes, b.nodes, sizeof(mpdp_plan_node) * b.n_nodes);
+    }
+    c->staged = false;
+    c->ran = false;
+    return MPDP_OK;
+}
+
 mpdp_status mpdp_optimize_batch(mpdp_ctx* c, const mpdp_query_graph* graphs, uint32_t count, mpdp_result* results) {
     if (!c) return fail(nullptr, MPDP_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (count && (!graphs || !results)) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "graphs/results is NULL");
     CUDA_TRY(c, cudaSetDevice(c->device));
+    if (c->multi && c->nccl && !c->simulate && count) return batch_distributed(c, graphs, count, results);
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));     // pinned staging is reused
     const bool batchable = !c->multi && c->timeout_ms <= 0 &&
                            !(c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS |

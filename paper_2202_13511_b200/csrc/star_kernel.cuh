@@ -88,7 +88,7 @@ __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<u
                 } else {
                     const int pl = 31 - __clz(L);             // max leaf (leaf space)
                     const int pv = star_vertex(pl, hub);
-                    if (pv > hub) {                           // max(S) is a leaf: card(S) from card(S \ max)
+                    if (pv > hub && !p.shard_local) {        // max(S) is a leaf: card(S) from card(S \ max)
                         double x = __dmul_rn(__ldcs(lcard + (h - bin[pl * 33 + kl])), q.card[pv]);
                         cS = __dmul_rn(x, q.sel[hub * q.n + pv]);
                     } else {
@@ -162,6 +162,67 @@ __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<u
 
 __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
                                           int hub);
+__device__ void star_emit_chain(const Params<uint32_t>& p, const SQ<uint32_t>& q, const uint32_t* c_set,
+                                const uint32_t* c_left, const double* c_cost, const double* c_card, int len);
+
+// Sharded extraction (p.shard_local): the ranks exchanged only the memo costs,
+// so every rank re-derives the chain's splits from its complete cost replica:
+// at S the warp evaluates the pairs ({v}, S \ {v}) exactly as the level did
+// (same C_out order of additions, reading R7's key on the real masks) and
+// takes their minimum; card(S) by reading R5's fold.  Lane 0 of warp 0.
+__device__ __noinline__ void star_extract_sharded(const Params<uint32_t>& p, const SQ<uint32_t>& q, int hub) {
+    const unsigned int lane = threadIdx.x & 31;
+    __shared__ uint32_t x_set[32], x_left[32];
+    __shared__ double x_cost[32], x_card[32];
+    const int n = p.n;
+    const bool leaf_costs = q.pad != 0;
+    uint32_t S = n == 32 ? ~0u : (1u << n) - 1u;
+    int len = 0;
+    while (__popc(S) >= 2) {
+        const uint32_t L = star_compress(S, hub);
+        const int kl = __popc(L);
+        const double cS = card_of(q, S);
+        Key best = key_inf();
+        for (int j = (int)lane; j < kl; j += 32) {
+            const int li = (int)__fns(L, 0, j + 1), v = star_vertex(li, hub);
+            const uint32_t lb = 1u << v, rb = S ^ lb;
+            double c;
+            if (kl == 1) {                                   // ({hub}, {v})
+                c = __dadd_rn(__dadd_rn(q.leaf[hub], q.leaf[v]), cS);
+            } else {
+                // rank of the leaf set L \ {li} among the (kl-1)-subsets
+                const uint32_t Lr = L & ~(1u << li);
+                unsigned int r = 0;
+                int i = 1;
+                for (uint32_t T = Lr; T; T &= T - 1, i++) {
+                    const int e = __ffs(T) - 1;
+                    unsigned long long b = 1;                // C(e, i)
+                    for (int t = 0; t < i; t++) b = b * (unsigned long long)(e - t) / (unsigned long long)(t + 1);
+                    r += e >= i ? (unsigned int)b : 0u;
+                }
+                const double dv = __ldcg(p.memo.dcost + p.star_off[kl] + r);
+                const double a = leaf_costs ? __dadd_rn(q.leaf[v], dv) : dv;
+                c = __dadd_rn(a, cS);
+            }
+            const uint32_t l = lb < rb ? lb : rb;
+            const Key cand{(unsigned long long)__double_as_longlong(c), (unsigned long long)l};
+            if (key_less(cand, best)) best = cand;
+        }
+        best = warp_min(best);
+        if (lane == 0) {
+            x_set[len] = S;
+            x_left[len] = (uint32_t)best.l;
+            x_cost[len] = __longlong_as_double((long long)best.c);
+            x_card[len] = cS;
+        }
+        len++;
+        const uint32_t left = (uint32_t)best.l, right = S ^ left;
+        S = (left & (left - 1)) ? left : right;
+        if ((S & (S - 1)) == 0) break;
+    }
+    __syncwarp();
+    if (lane == 0) star_emit_chain(p, q, x_set, x_left, x_cost, x_card, len);
+}
 
 // Star levels as dataflow chunks (dataflow.cuh): level k's sets are the
 // colex ranks of its (k-1)-leaf sets; a chunk needs level k-1 up to the
@@ -272,6 +333,10 @@ __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<ui
         if (lane == 0) r->n_nodes = 0;
         return;
     }
+    if (p.shard_local) {
+        star_extract_sharded(p, q, hub);
+        return;
+    }
     // The optimal plan of a star set is a caterpillar: every join splits one
     // leaf v off, ({v}, S \ {v}).  Walk the chain from V two steps per memo
     // round trip: while lane 31 reads the entry of S, lane j reads the entry of
@@ -344,7 +409,16 @@ __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<ui
         S = (l1 & (l1 - 1)) ? l1 : r1;
         if ((S & (S - 1)) == 0) break;
     }
-    if (lane != 0) return;
+    __syncwarp();
+    if (lane == 0) star_emit_chain(p, q, c_set, c_left, c_cost, c_card, len);
+}
+
+
+// Post-order plan nodes of a recorded caterpillar chain (one thread).
+__device__ void star_emit_chain(const Params<uint32_t>& p, const SQ<uint32_t>& q, const uint32_t* c_set,
+                                const uint32_t* c_left, const double* c_cost, const double* c_card, int len) {
+    ResultDev* r = p.result;
+    const int n = p.n;
     // post-order (left subtree, right subtree, node): with prefix_i = [v_i] when
     // the leaf is the left child and suffix_i = [v_i if it is the right child,
     // S_i], the sequence is prefix_0 .. prefix_{len-2}, the bottom pair (two

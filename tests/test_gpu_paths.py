@@ -102,3 +102,24 @@ def test_general_graphs_full_size(topo, n, seed, extra):
     g = W.generate(topo, n, seed) if extra is None else W.random_connected(n, seed, extra=extra)
     with mpdp.Context(device=0, workspace_bytes=4 << 30) as c:
         check(c.mpdp_optimize(g), O.optimize_dpccp(g), g)
+
+
+def test_nccl_self_batch_and_heuristics():
+    """Multi-GPU batch (MPDP_FLAG_NCCL_SELF: a real 1-rank communicator): the
+    independent queries go through the distributed path (per-rank share on the
+    single-GPU kernels, results allgathered over NCCL); UnionDP / IDP2 on such
+    a context give the single-GPU context's plans."""
+    from paper_2202_13511_b200 import mpdp
+    gs = [W.generate(t, n, 40 + i) for i, (t, n) in enumerate(
+        [("star", 9), ("snowflake", 16), ("chain", 20), ("clique", 9), ("cycle", 12), ("star", 15)])]
+    g = W.snowflake(200, 3)
+    with mpdp.Context(device=0, workspace_bytes=1 << 30) as one:
+        ref = [one.mpdp_optimize_uniondp(g, k=20, t=12), one.mpdp_optimize(g, algo="IDP2_MPDP", k=12)]
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_NCCL_SELF) as c:
+        for q, r in zip(gs, c.mpdp_optimize_batch(gs)):
+            o = O.optimize(q)
+            assert r.cost == o.cost and r.tree() == O.tree_of(o.nodes)
+            assert (r.csg_count, r.ccp_pairs, r.pairs_evaluated) == (o.csg_count, o.ccp_pairs, o.pairs_evaluated)
+        got = [c.mpdp_optimize_uniondp(g, k=20, t=12), c.mpdp_optimize(g, algo="IDP2_MPDP", k=12)]
+    for a, b in zip(ref, got):
+        assert a.cost == b.cost and a.tree() == b.tree() and a.pairs_evaluated == b.pairs_evaluated
