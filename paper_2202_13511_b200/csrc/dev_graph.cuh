@@ -26,11 +26,23 @@ template <typename M> struct QueryDev {
     unsigned long long binom[(N + 1) * (N + 1)];   // C(i, j) at i * (N + 1) + j
 };
 
+// Neighbourhood of a vertex set by byte lookups (32-bit masks): nb[c][b] = OR
+// of adj[8c + i] over the bits i of b, so N(F) = OR_c nb[c][byte_c(F)] -- four
+// shared-memory loads per BFS frontier step instead of a data-dependent loop
+// over the frontier's vertices (the CCP connectivity checks of general graphs
+// were 43% of k_dp_fused<GENERAL>'s instructions on random-20).  Built only by
+// the general-graph kernels (SQ::nbtab); 64-bit masks keep the loop.
+template <typename M> struct NbTab {};
+template <> struct NbTab<uint32_t> {
+    uint32_t t[4][256];
+};
+
 // The part every kernel keeps in shared memory (sel compacted to n x n).
 template <typename M> struct SQ {
     static constexpr int N = MaxN<M>::value;
     int n, cls, max_depth, pad;            // pad = has_leaf_costs (any leaf cost != 0)
-    int dpsub, pad1;                       // DPSUB-enumeration ablation (QueryDev::dpsub)
+    int dpsub, nbtab;                      // DPSUB-enumeration ablation (QueryDev::dpsub); nb is built
+    NbTab<M> nb;
     M adj[N];
     M desc[N];
     M depth_mask[N];
@@ -48,6 +60,7 @@ __device__ __forceinline__ void load_query(SQ<M>& s, const QueryDev<M>* q) {
         s.max_depth = q->max_depth;
         s.pad = q->has_leaf_costs;
         s.dpsub = q->dpsub;
+        s.nbtab = 0;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         s.adj[i] = q->adj[i];
@@ -74,6 +87,35 @@ __device__ __forceinline__ double card_of(const SQ<M>& q, M S) {
     return x;
 }
 
+// OR of adj[v] over the vertices v of F
+template <typename M>
+__device__ __forceinline__ M nbrs(const SQ<M>& q, M F) {
+    M N = 0;
+    for (M T = F; T; T &= T - 1) N |= q.adj[ctz(T)];
+    return N;
+}
+template <>
+__device__ __forceinline__ uint32_t nbrs(const SQ<uint32_t>& q, uint32_t F) {
+    if (q.nbtab) return q.nb.t[0][F & 255u] | q.nb.t[1][(F >> 8) & 255u] | q.nb.t[2][(F >> 16) & 255u] | q.nb.t[3][F >> 24];
+    uint32_t N = 0;
+    for (uint32_t T = F; T; T &= T - 1) N |= q.adj[ctz(T)];
+    return N;
+}
+
+// Build SQ::nb from the device query (call after load_query, before the
+// __syncthreads that publishes the shared query)
+__device__ __forceinline__ void build_nbtab(SQ<uint32_t>& s, const QueryDev<uint32_t>* q) {
+    const int n = q->n;
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
+        const int c = i >> 8, b = i & 255;
+        uint32_t x = 0;
+        for (int j = 0; j < 8; j++)
+            if (((b >> j) & 1) && 8 * c + j < n) x |= q->adj[8 * c + j];
+        s.nb.t[c][b] = x;
+    }
+    if (threadIdx.x == 0) s.nbtab = 1;
+}
+
 // grow(source, restriction) (Alg. grow): all vertices of the
 // restriction reachable from the source.  Frontier-at-a-time BFS in registers:
 // N = (OR adj[v] over the frontier) & restriction & ~V.
@@ -81,8 +123,7 @@ template <typename M>
 __device__ __forceinline__ M grow(const SQ<M>& q, M source, M restriction) {
     M V = source, F = source;
     while (F) {
-        M N = 0;
-        for (M T = F; T; T &= T - 1) N |= q.adj[ctz(T)];
+        M N = nbrs(q, F);
         N &= restriction & ~V;
         V |= N;
         F = N;
@@ -98,8 +139,7 @@ __device__ __forceinline__ bool connected(const SQ<M>& q, M S) {
     M V = lowbit(S), F = V;
     while (F) {
         if (V == S) return true;
-        M N = 0;
-        for (M T = F; T; T &= T - 1) N |= q.adj[ctz(T)];
+        M N = nbrs(q, F);
         N &= S & ~V;
         V |= N;
         F = N;

@@ -573,6 +573,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     __shared__ Tri s_excl, s_agg;
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
+    if constexpr (CLS == CLS_GENERAL && sizeof(M) == 4) build_nbtab(q, p.q);   // byte-table BFS steps
     unsigned int nbar = 0;                 // grid barriers passed (thread 0)
     const unsigned int gen = p.q->gen;
     const int n = p.n;

@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
     if (threadIdx.x == 0) {
         q.n = n;
         q.dpsub = p.q->dpsub;              // set_kind reads it
+        q.nbtab = 0;                       // connected() takes the loop (no byte tables here)
     }
     const unsigned long long rmask = p.tiles_ring - 1;
     const unsigned long long epoch = lookback_epoch(p, k);
