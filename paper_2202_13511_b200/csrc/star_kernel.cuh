@@ -88,12 +88,12 @@ __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<u
                 } else {
                     const int pl = 31 - __clz(L);             // max leaf (leaf space)
                     const int pv = star_vertex(pl, hub);
-                    if (pv > hub && !p.shard_local) {        // max(S) is a leaf: card(S) from card(S \ max)
-                        double x = __dmul_rn(__ldcs(lcard + (h - bin[pl * 33 + kl])), q.card[pv]);
-                        cS = __dmul_rn(x, q.sel[hub * q.n + pv]);
-                    } else {
-                        cS = card_of(q, S);
-                    }
+                    // max(S) is a leaf: card(S) from card(S \ max) (reading
+                    // R19); the load is issued here, the product formed after
+                    // the first batch of probes is in flight
+                    const bool fold = pv > hub && !p.shard_local;
+                    const double craw = fold ? __ldcs(lcard + (h - bin[pl * 33 + kl])) : 0.0;
+                    bool need_cs = true;
                     // Pair ({v}, S \ {v}) per leaf v, walked from the largest
                     // leaf down.  Tie-break key (reading R7, min(left, right)
                     // as a mask) in leaf space: {v} for every leaf but the
@@ -127,6 +127,10 @@ __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<u
                         double dv[4];
 #pragma unroll
                         for (int u = 0; u < 4; u++) dv[u] = ok[u] ? lvl[rk[u]] : 0.0;
+                        if (need_cs) {
+                            cS = fold ? __dmul_rn(__dmul_rn(craw, q.card[pv]), q.sel[hub * q.n + pv]) : card_of(q, S);
+                            need_cs = false;
+                        }
 #pragma unroll
                         for (int u = 0; u < 4; u++) {
                             const double a =
