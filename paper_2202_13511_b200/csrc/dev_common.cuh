@@ -12,6 +12,7 @@ constexpr int kBlock = 256;          // threads per CTA for every level kernel
 constexpr int kRanksPerThread = 16;  // unrank one, Gosper-step 15 more
 constexpr int kTile = kBlock * kRanksPerThread;
 constexpr uint64_t kLightMax = 32;   // sets with <= 32 join pairs: thread per set
+constexpr unsigned int kLightGeneral = 32;   // general graphs: CCP-checked sets above this go to CCC
 constexpr int kSinkPairs = 2;        // join pairs whose memo probes are issued together
 constexpr int kLightBlock = 128;     // k_eval_light CTA size
 constexpr int kLightMinBlocks = 5;   // k_eval_light occupancy target -> <= 102 registers

@@ -646,8 +646,11 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                     if (i < (int)rpt && r0 + i < r_hi) {
                         if (connected_cls<M, CLS>(q, S, k)) {
                             unsigned long long w;
-                            set_kind<M, CLS>(q, S, k, w);
-                            if (w <= kLightMax) {
+                            const int kind = set_kind<M, CLS>(q, S, k, w);
+                            // (general graphs: only sets without CCP checks,
+                            // or with few candidates, are evaluated by one thread)
+                            if (w <= kLightMax && (CLS != CLS_GENERAL || w <= p.light_max || kind == KIND_TREE ||
+                                                   kind == KIND_COMPLETE)) {
                                 lflag |= 1u << i;
                             } else {
                                 hflag |= 1u << i;

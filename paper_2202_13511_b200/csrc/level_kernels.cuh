@@ -123,6 +123,9 @@ template <typename M> struct Params {
     // is recomputed locally (reading R5's fold) and the chosen split of a
     // plan node is re-derived at extraction from the replicated costs
     int shard_local;
+    // general graphs: sets with more join-pair candidates than this go to the
+    // warp-parallel heavy phase (CCC) instead of one thread (light)
+    unsigned int light_max;
 };
 
 // ------------------------------------------------------------- mem helpers
@@ -394,8 +397,9 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
                 if (r0 + i < nranks) {
                     if (connected_cls<M, CLS>(q, S, k)) {
                         unsigned long long w;
-                        set_kind<M, CLS>(q, S, k, w);
-                        if (w <= kLightMax) {
+                        const int kind = set_kind<M, CLS>(q, S, k, w);
+                        if (w <= kLightMax && (CLS != CLS_GENERAL || w <= p.light_max || kind == KIND_TREE ||
+                                               kind == KIND_COMPLETE)) {
                             lflag |= 1u << i;
                         } else {
                             hflag |= 1u << i;

@@ -372,12 +372,21 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
     memcpy(q->binom, table.data(), sizeof(unsigned long long) * NB * NB);
 }
 
+// general graphs: sets with more CCP-checked candidates than this are heavy
+static unsigned int light_max_general() {
+    static const unsigned int v = [] {
+        const char* e = getenv("MPDP_DEBUG_LIGHT_GENERAL");     // experiments only
+        return e ? (unsigned int)std::max(1, std::min(32, atoi(e))) : kLightGeneral;
+    }();
+    return v;
+}
+
 static unsigned long long heavy_pair_bound(int n, int k, int cls) {
     const unsigned long long C = binom_u64(n, k);
     if (cls == CLS_TREE) return (k - 1 > (int)kLightMax) ? sat_mul(C, (unsigned long long)(k - 1)) : 0ull;
     if (k - 1 >= 63) return ~0ull;
     const unsigned long long w = (1ull << (k - 1)) - 1;
-    if (w <= kLightMax) return 0;
+    if (w <= (cls == CLS_GENERAL ? (unsigned long long)light_max_general() : kLightMax)) return 0;
     return sat_mul(C, w);
 }
 
@@ -577,6 +586,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.n = c->n;
     p.inv_load = 1.0 / c->load_factor;
     p.no_ccc = (c->flags & MPDP_FLAG_NO_CCC) ? 1 : 0;
+    p.light_max = light_max_general();
     p.star_hub = c->star_hub;
     {   // star levels: C(n-1, k-1) entries + `world` padding (equal rank segments, as dense_off)
         unsigned long long so = 0;
