@@ -415,14 +415,17 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 // amortise the per-set work and keep a lane's consecutive pairs in nearby memo
 // lines; more lanes fill the grid and shorten the level's last round.
 // Returns 0 (pair chunks per warp, the split path) for levels of fewer sets
-// than warps whose sets exceed 8192 pairs.  Measured (round 1, level barrier;
+// than warps whose sets exceed split_w - 1 pairs (4096 on the kernel since
+// round 2: clique-18 0.688 -> 0.674 ms, its level 14 of 3060 sets x 8191 pairs
+// ran at 219 G pairs/s as one warp per set; 2048 ties, 16384 0.746 ms).  Measured (round 1, level barrier;
 // clique-18 / 16 / 20): fixed ~8 pairs per lane 1.04 / 0.27 / 7.5 ms; <= 256
 // pairs per lane widened to half the threads 0.72 / 0.28 / 4.9 ms; this model
 // (cost 64) 0.66 / 0.29 / 3.9 ms (cost 32: 0.77 / 0.29 / 4.0; cost 128: 0.66 /
 // 0.29 / 3.9).  Host and device share it (the host plans the dataflow chunks).
 constexpr double kCliqueSetCost = 64.0;
-__host__ __device__ inline unsigned int clique_group(unsigned long long w, unsigned long long C, unsigned long long T) {
-    if (w + 1 > 8192 && 32ull * C < T) return 0;
+__host__ __device__ inline unsigned int clique_group(unsigned long long w, unsigned long long C, unsigned long long T,
+                                                     unsigned long long split_w = 8192) {
+    if (w + 1 > split_w && 32ull * C < T) return 0;
     unsigned int best_g = 1;
     double best = 1e300;
     for (unsigned int G = 1; G <= 32 && G <= w + 1; G <<= 1) {
@@ -904,7 +907,7 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         p.memo.dcard[1u << gtid] = q.card[gtid];
     }
     // whole sets per group of G lanes (clique_group), or pair chunks per warp
-    const unsigned int G = clique_group(w, C, nthreads);
+    const unsigned int G = clique_group(w, C, nthreads, p.clique_split_w);
     (void)nccp;                            // every evaluated pair is a ccp (Lemma 8): counted as pairs
     if (G) {
         switch (G) {

@@ -126,6 +126,7 @@ template <typename M> struct Params {
     // general graphs: sets with more join-pair candidates than this go to the
     // warp-parallel heavy phase (CCC) instead of one thread (light)
     unsigned int light_max;
+    unsigned long long clique_split_w;     // k_dp_clique: split levels whose sets exceed this many pairs + 1
 };
 
 // ------------------------------------------------------------- mem helpers
