@@ -424,12 +424,13 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 // 0.29 / 3.9).  Host and device share it (the host plans the dataflow chunks).
 constexpr double kCliqueSetCost = 64.0;
 __host__ __device__ inline unsigned int clique_group(unsigned long long w, unsigned long long C, unsigned long long T,
-                                                     unsigned long long split_w = 8192) {
+                                                     unsigned long long split_w = 8192,
+                                                     double set_cost = kCliqueSetCost) {
     if (w + 1 > split_w && 32ull * C < T) return 0;
     unsigned int best_g = 1;
     double best = 1e300;
     for (unsigned int G = 1; G <= 32 && G <= w + 1; G <<= 1) {
-        const double cost = (double)((C * G + T - 1) / T) * ((double)(w + G - 1) / G + kCliqueSetCost);
+        const double cost = (double)((C * G + T - 1) / T) * ((double)(w + G - 1) / G + set_cost);
         if (cost < best) {
             best = cost;
             best_g = G;
@@ -907,7 +908,7 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         p.memo.dcard[1u << gtid] = q.card[gtid];
     }
     // whole sets per group of G lanes (clique_group), or pair chunks per warp
-    const unsigned int G = clique_group(w, C, nthreads, p.clique_split_w);
+    const unsigned int G = clique_group(w, C, nthreads, p.clique_split_w, p.clique_set_cost);
     (void)nccp;                            // every evaluated pair is a ccp (Lemma 8): counted as pairs
     if (G) {
         switch (G) {
@@ -922,7 +923,7 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
     }
     const unsigned long long P = (unsigned long long)C * w;
     unsigned long long csize = (P + nwarps - 1) / nwarps;
-    if (csize < 512) csize = 512;        // (1024: clique-16 291 vs 278 us)
+    if (csize < p.clique_csize_min) csize = p.clique_csize_min;   // 512 (1024: clique-16 291 vs 278 us)
     const unsigned long long c0 = gw * csize;
     if (c0 >= P) return;
     const unsigned long long c1 = c0 + csize < P ? c0 + csize : P;

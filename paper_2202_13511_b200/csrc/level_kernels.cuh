@@ -127,6 +127,8 @@ template <typename M> struct Params {
     // warp-parallel heavy phase (CCC) instead of one thread (light)
     unsigned int light_max;
     unsigned long long clique_split_w;     // k_dp_clique: split levels whose sets exceed this many pairs + 1
+    double clique_set_cost;                // k_dp_clique: per-set overhead of the group cost model, in pairs
+    unsigned long long clique_csize_min;   // k_dp_clique: smallest warp chunk of the split path, in pairs
 };
 
 // ------------------------------------------------------------- mem helpers
