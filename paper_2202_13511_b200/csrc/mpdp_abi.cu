@@ -23,6 +23,7 @@
 #include "small_kernel.cuh"
 #include "star_kernel.cuh"
 #include "batch128.cuh"
+#include "cluster_kernel.cuh"
 #include "heuristics.h"
 
 using namespace mpdp;
@@ -158,6 +159,7 @@ struct mpdp_ctx {
     bool batch_attr = false;
     int star_hub = -1;                    // star queries: the relation adjacent to all others
     int star_occ = 0;                     // k_dp_star CTAs per SM
+    int cluster_size = 0;                 // k_dp_tree_cluster: CTAs per cluster (0 = not probed yet)
     int clique_df_occ = 0;                // k_dp_clique_df (ablation) CTAs per SM
     bool clique_df_attr = false;
     bool star = false;                    // last query ran k_dp_star (memo_kind 4)
@@ -870,6 +872,73 @@ static bool tree1_eligible(const mpdp_ctx* c) {
     return c->lay.memo_kind == MEMO_DENSE && c->tree_max_level <= (unsigned long long)kTree1MaxLevel;
 }
 
+// Sparse tree queries with up to kClusterMaxLevel sets per level (snowflakes):
+// one thread-block cluster runs the level loop (cluster_kernel.cuh).
+static bool cluster_eligible(const mpdp_ctx* c) {
+    if (c->cls != CLS_TREE || c->wide || c->multi || c->n < 3 || c->n > 32 || c->timeout_ms > 0) return false;
+    if (c->flags & (MPDP_FLAG_NO_SMALL | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS | MPDP_FLAG_HASH_MEMO))
+        return false;
+    if (getenv("MPDP_DEBUG_NO_CLUSTER")) return false;      // experiments only
+    return c->lay.memo_kind == MEMO_DENSE && c->tree_max_level <= (unsigned long long)kClusterMaxLevel &&
+           c->lay.list_cap >= c->tree_max_level;
+}
+
+static mpdp_status run_tree_cluster(mpdp_ctx* c, const Params<uint32_t>& p) {
+    const size_t smem = cluster_smem_bytes(p.memo.rg.entries);
+    if (!c->cluster_size) {                // largest cluster the device schedules: 16 (non-portable), else 8
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_tree_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)cluster_smem_bytes(rank_geom(32).entries)));
+        cudaFuncSetAttribute(k_dp_tree_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (int cs : {16, 8, 4}) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = cs;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(cs);
+            cfg.blockDim = dim3(kClusterBlock);
+            cfg.dynamicSmemBytes = cluster_smem_bytes(rank_geom(32).entries);
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_dp_tree_cluster, &cfg) == cudaSuccess && nclusters > 0) {
+                c->cluster_size = cs;
+                break;
+            }
+            cudaGetLastError();
+        }
+        if (!c->cluster_size) return fail(c, MPDP_ERR_CUDA, "no thread-block cluster fits the tree kernel");
+    }
+    int cs = c->cluster_size;
+    if (const char* e = getenv("MPDP_DEBUG_CLUSTER")) cs = std::max(1, std::min(cs, atoi(e)));   // experiments only
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kClusterBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    CUDA_TRY(c, cudaLaunchKernelEx(&cfg, k_dp_tree_cluster, p));
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = 1;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->d2h_bytes = sizeof(ResultDev);
+    return MPDP_OK;
+}
+
 static mpdp_status run_tree1(mpdp_ctx* c, const Params<uint32_t>& p) {
     const size_t smem = tree1_smem_bytes(p.memo.rg.entries);
     if (!c->tree1_attr) {
@@ -1212,6 +1281,7 @@ static mpdp_status run_query(mpdp_ctx* c) {
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
         if (small_eligible(c)) return run_small<CLS>(c, make_params<M>(c));
         if (tree1_eligible(c)) return run_tree1(c, make_params<M>(c));
+        if (!(c->star_hub >= 0 && star_eligible(c)) && cluster_eligible(c)) return run_tree_cluster(c, make_params<M>(c));
         if (star_eligible(c)) {
             c->desc_clean = was_clean;
             return run_star(c, make_params<M>(c));

@@ -123,3 +123,25 @@ def test_nccl_self_batch_and_heuristics():
         got = [c.mpdp_optimize_uniondp(g, k=20, t=12), c.mpdp_optimize(g, algo="IDP2_MPDP", k=12)]
     for a, b in zip(ref, got):
         assert a.cost == b.cost and a.tree() == b.tree() and a.pairs_evaluated == b.pairs_evaluated
+
+
+@pytest.mark.parametrize("n,seed", [(16, 0), (18, 1), (20, 2), (22, 3), (24, 4), (26, 5), (20, 6)])
+def test_cluster_tree_kernel(n, seed):
+    """Sparse trees with 513..6144 sets per level run on one thread-block
+    cluster (k_dp_tree_cluster: cluster barrier between levels, one global
+    reservation per CTA for the next level list); results equal the oracle's
+    and the multi-CTA list kernel's (MPDP_FLAG_NO_SMALL), with and without
+    composite leaf costs."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.snowflake(n, seed)
+    if seed % 2:
+        g.leaf_cost = [float((5 * i) % 7) for i in range(g.n)]
+    o = O.optimize(g)
+    with mpdp.Context(device=0, workspace_bytes=2 << 30) as c:
+        r = c.mpdp_optimize(g)
+        if 512 < max(o.level_csg) <= 6144:               # the cluster kernel's range: one launch
+            assert r.gpu_launches == 1 and r.memo_kind == 1
+        check(r, o, g)
+        check(c.mpdp_optimize(g), o, g)                  # repeated: counters and lists reset
+    with mpdp.Context(device=0, workspace_bytes=2 << 30, flags=mpdp.FLAG_NO_SMALL) as c:
+        check(c.mpdp_optimize(g), o, g)
