@@ -42,6 +42,11 @@ template <typename M> struct SQ {
     static constexpr int N = MaxN<M>::value;
     int n, cls, max_depth, pad;            // pad = has_leaf_costs (any leaf cost != 0)
     int dpsub, nbtab;                      // DPSUB-enumeration ablation (QueryDev::dpsub); nb is built
+    // general graphs on the bitmask-indexed memo (MEMO_MASK): the cost array,
+    // pre-filled with kMemoAbsent by the host, so that the connectivity of any
+    // proper subset of the set under evaluation is one probe (reading R20);
+    // null = connectivity by BFS
+    const double* mc;
     NbTab<M> nb;
     M adj[N];
     M desc[N];
@@ -61,6 +66,7 @@ __device__ __forceinline__ void load_query(SQ<M>& s, const QueryDev<M>* q) {
         s.pad = q->has_leaf_costs;
         s.dpsub = q->dpsub;
         s.nbtab = 0;
+        s.mc = nullptr;
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         s.adj[i] = q->adj[i];
@@ -147,6 +153,24 @@ __device__ __forceinline__ bool connected(const SQ<M>& q, M S) {
     return V == S;
 }
 
+// Reading R20 (memo connectivity).  Level by level, every connected set of
+// j < k relations is in the memo before level k starts, and with
+// the bitmask-indexed memo a set's slot is its mask.  The host fills the cost
+// array with kMemoAbsent (an all-ones NaN that no sum of non-negative costs
+// produces), so a proper subset X of a level-k set is connected iff its slot
+// holds anything else: the CCP-block tests of Alg. mpdp_generalization
+// ("lb is connected", "rb is connected") become one probe each
+// instead of a BFS (Alg. connected).  Singletons are connected.
+constexpr unsigned long long kMemoAbsent = ~0ull;
+__device__ __forceinline__ bool memo_present(double c) {
+    return (unsigned long long)__double_as_longlong(c) != kMemoAbsent;
+}
+template <typename M>
+__device__ __forceinline__ bool conn_sub(const SQ<M>& q, M X) {
+    if (q.mc) return (X & (X - 1)) == 0 ? X != 0 : memo_present(q.mc[X]);
+    return connected(q, X);
+}
+
 // 2|E(G[S])|
 template <typename M>
 __device__ __forceinline__ int induced_degree_sum(const SQ<M>& q, M S) {
@@ -167,10 +191,80 @@ __device__ __forceinline__ bool connected_cls(const SQ<M>& q, M S, int k) {
     return connected(q, S);
 }
 
+// Cut vertices of a connected G[S], |S| >= 3, with memo connectivity (reading
+// R20): v is a cut vertex iff S \ {v} is disconnected, i.e. absent from the
+// memo.  Eight probes in flight.
+template <typename M>
+__device__ __forceinline__ M cut_vertices_memo(const SQ<M>& q, M S) {
+    M cut = 0;
+    for (M T = S; T;) {
+        double c[8];
+        M b[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            b[i] = lowbit(T);
+            c[i] = 0.0;
+            if (T) {
+                c[i] = q.mc[S & ~b[i]];
+                T &= T - 1;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (!memo_present(c[i])) cut |= b[i];
+    }
+    return cut;
+}
+
+// Find-Blocks from the cut vertices (reading R21), registers and frontier BFS
+// only.  For a vertex x that is not a cut vertex, its block is
+//     B(x) = intersection over cut vertices c of (comp(S \ {c}, x) + c)
+// where comp(X, x) = grow({x}, X): each term contains B(x) (a block minus one
+// vertex stays connected), and a vertex y outside B(x) is cut off from x by the
+// cut vertex of B(x) on the way to y in the block-cut tree.  The same holds for
+// an edge (u, v) in place of x (comp taken from the endpoint that is not c),
+// which finds the blocks made only of cut vertices.  A pendant x (one
+// neighbour u in S) is the block {x, u} directly.
+template <typename M>
+__device__ __forceinline__ M block_of_edge(const SQ<M>& q, M S, M cut, int u, int v) {
+    M B = S;
+    for (M T = cut; T; T &= T - 1) {
+        const int c = ctz(T);
+        B &= grow(q, bitm<M>(c == u ? v : u), S & ~bitm<M>(c)) | bitm<M>(c);
+    }
+    return B;
+}
+template <typename M>
+__device__ int blocks_from_cut(const SQ<M>& q, M S, M cut, M* blk) {
+    int nb = 0;
+    M done = 0;
+    for (M rest = S & ~cut; rest; rest = S & ~cut & ~done) {
+        const int x = ctz(rest);
+        const M nx = q.adj[x] & S;
+        const M B = (nx & (nx - 1)) == 0 ? (bitm<M>(x) | nx) : block_of_edge(q, S, cut, x, ctz(nx));
+        blk[nb++] = B;
+        done |= B;
+    }
+    for (M U = cut; U; U &= U - 1) {       // blocks of cut vertices only
+        const int u = ctz(U);
+        for (M V = q.adj[u] & cut & ~(bitm<M>(u + 1) - 1); V; V &= V - 1) {
+            const int v = ctz(V);
+            const M uv = bitm<M>(u) | bitm<M>(v);
+            bool found = false;
+            for (int i = 0; i < nb && !found; i++) found = (blk[i] & uv) == uv;
+            if (!found) blk[nb++] = block_of_edge(q, S, cut, u, v);
+        }
+    }
+    return nb;
+}
+
 // Find-Blocks: biconnected components of G[S] by an iterative
 // Hopcroft-Tarjan DFS with a vertex stack; bitmask adjacency, small local arrays.
+// With memo connectivity (q.mc) the blocks come from the cut vertices instead
+// (reading R21: no DFS stacks in local memory).
 template <typename M>
 __device__ int find_blocks(const SQ<M>& q, M S, M* blk) {
+    if (q.mc) return blocks_from_cut(q, S, cut_vertices_memo(q, S), blk);
     constexpr int N = MaxN<M>::value;
     unsigned char disc[N], low[N], par[N], vst[N], dst[N];
     M rem[N];
@@ -227,6 +321,23 @@ template <typename M>
 __device__ __forceinline__ bool biconnected(const SQ<M>& q, M S) {
     for (M T = S; T; T &= T - 1)
         if (popc(q.adj[ctz(T)] & S) < 2) return false;
+    if (q.mc) {                            // reading R20: |S| - 1 >= 2, four probes in flight
+        for (M T = S; T;) {
+            double c[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                c[i] = 0.0;
+                if (T) {
+                    c[i] = q.mc[S & ~lowbit(T)];
+                    T &= T - 1;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                if (!memo_present(c[i])) return false;
+        }
+        return true;
+    }
     for (M T = S; T; T &= T - 1)
         if (!connected(q, S & ~lowbit(T))) return false;
     return true;
@@ -236,8 +347,12 @@ __device__ __forceinline__ bool biconnected(const SQ<M>& q, M S) {
 // tree-induced sets have one pair per edge (Alg. mpdp_trees);
 // complete sets are one block with 2^(k-1)-1 splits (Lemma generic:opt);
 // otherwise sum over blocks of 2^(b-1)-1 (Alg. mpdp_generalization).
+// (blk_out: the first kHeavyBlk blocks of a KIND_BLOCKS set and their count in
+// *nb_out, cached with the heavy list so that work items skip Find-Blocks)
+constexpr int kHeavyBlk = 8;
 template <typename M, int CLS>
-__device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned long long& w) {
+__device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned long long& w, M* blk_out = nullptr,
+                                        int* nb_out = nullptr) {
     if (CLS == CLS_TREE) {
         w = (unsigned long long)(k - 1);
         return KIND_TREE;
@@ -259,16 +374,49 @@ __device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned lon
         w = (1ull << (k - 1)) - 1;
         return KIND_COMPLETE;
     }
-    if (biconnected(q, S)) {               // one (non-complete) block: S
-        w = (1ull << (k - 1)) - 1;
-        return KIND_ONEBLOCK;
+    M blk[MaxN<M>::value];
+    int nb;
+    if (q.mc) {                            // reading R21: cut vertices by probes, blocks from them
+        const M cut = cut_vertices_memo(q, S);
+        if (!cut) {                        // one (non-complete) block: S
+            w = (1ull << (k - 1)) - 1;
+            return KIND_ONEBLOCK;
+        }
+        nb = blocks_from_cut(q, S, cut, blk);
+    } else {
+        if (biconnected(q, S)) {           // one (non-complete) block: S
+            w = (1ull << (k - 1)) - 1;
+            return KIND_ONEBLOCK;
+        }
+        nb = find_blocks(q, S, blk);
     }
+    unsigned long long s = 0;
+    for (int i = 0; i < nb; i++) s += (1ull << (popc(blk[i]) - 1)) - 1;
+    w = s;
+    if (blk_out) {
+        for (int i = 0; i < nb && i < kHeavyBlk; i++) blk_out[i] = blk[i];
+        *nb_out = nb;
+    }
+    return KIND_BLOCKS;
+}
+
+// Pair count of a set whose kind is already known (set_kind's w without its
+// tests): closed forms, or Find-Blocks for KIND_BLOCKS (blocks cached as in
+// set_kind).
+template <typename M, int CLS>
+__device__ __forceinline__ unsigned long long kind_pairs(const SQ<M>& q, M S, int k, int kind, M* blk_out = nullptr,
+                                                         int* nb_out = nullptr) {
+    if (kind == KIND_TREE) return (unsigned long long)(k - 1);
+    if (kind != KIND_BLOCKS || q.dpsub) return (1ull << (k - 1)) - 1;
     M blk[MaxN<M>::value];
     const int nb = find_blocks(q, S, blk);
     unsigned long long s = 0;
     for (int i = 0; i < nb; i++) s += (1ull << (popc(blk[i]) - 1)) - 1;
-    w = s;
-    return KIND_BLOCKS;
+    if (blk_out) {
+        for (int i = 0; i < nb && i < kHeavyBlk; i++) blk_out[i] = blk[i];
+        *nb_out = nb;
+    }
+    return s;
 }
 
 // colex combinadic unrank (reading R10): the r-th k-subset of {0..n-1} has

@@ -578,6 +578,8 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
     if constexpr (CLS == CLS_GENERAL && sizeof(M) == 4) build_nbtab(q, p.q);   // byte-table BFS steps
+    if constexpr (CLS == CLS_GENERAL && MEMO == MEMO_MASK)
+        if (threadIdx.x == 0 && p.memo_conn) q.mc = p.memo.dcost;               // reading R20
     unsigned int nbar = 0;                 // grid barriers passed (thread 0)
     const unsigned int gen = p.q->gen;
     const int n = p.n;
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             // ---- unrank + filter + classify (registers only)
             const unsigned int r0 = lo + (unsigned int)t0 + threadIdx.x * rpt;
             M S0 = 0;
-            unsigned int lflag = 0, hflag = 0;
+            unsigned int lflag = 0, hflag = 0, kinds = 0;   // kinds: 2 bits per rank (set_kind once)
             Tri mine = {0, 0, 0};
             if (r0 < r_hi) {
                 S0 = unrank_colex32(bin, n, k, r0);
@@ -651,6 +653,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                         if (connected_cls<M, CLS>(q, S, k)) {
                             unsigned long long w;
                             const int kind = set_kind<M, CLS>(q, S, k, w);
+                            kinds |= (unsigned int)kind << (2 * i);
                             // (general graphs: only sets without CCP checks,
                             // or with few candidates, are evaluated by one thread)
                             if (w <= kLightMax && (CLS != CLS_GENERAL || w <= p.light_max || kind == KIND_TREE ||
@@ -718,7 +721,10 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                     if ((lflag >> i) & 1) {
                         if (li < nloc) {
                             qmask[li] = S;
-                            qrank[li] = r0 + i;
+                            // (memo connectivity implies MEMO_MASK, whose slots
+                            // ignore the rank: bits 30-31 carry the set kind)
+                            qrank[li] = (CLS == CLS_GENERAL && q.mc) ? (r0 + i) | (((kinds >> (2 * i)) & 3u) << 30)
+                                                                     : r0 + i;
                         } else {
                             const unsigned long long d = s_small + (li - nloc);
                             if (d < p.list_cap)
@@ -730,7 +736,19 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                     }
                     if ((hflag >> i) & 1) {
                         unsigned long long w;
-                        set_kind<M, CLS>(q, S, k, w);
+                        if (CLS == CLS_GENERAL && q.mc) {
+                            M blk[kHeavyBlk];
+                            int nb = 0;
+                            const int kind = (int)((kinds >> (2 * i)) & 3u);
+                            w = kind_pairs<M, CLS>(q, S, k, kind, blk, &nb);
+                            if (hi < p.heavy_cap) {
+                                p.hinfo[hi] = (unsigned int)kind | ((unsigned int)nb << 2);
+                                for (int b = 0; b < nb && b < kHeavyBlk; b++) p.hblk[hi * kHeavyBlk + b] = blk[b];
+                                p.hcard[hi] = card_of(q, S);   // here, not in a phase of its own
+                            }
+                        } else {
+                            set_kind<M, CLS>(q, S, k, w);
+                        }
                         if (hi < p.heavy_cap) {
                             p.heavy[hi] = S;
                             p.wh[hi] = wi;
@@ -757,7 +775,13 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             for (unsigned int e = threadIdx.x; e < nloc; e += blockDim.x) {
                 const M S = qmask[e];
                 unsigned long long w;
-                const int kind = set_kind<M, CLS>(q, S, k, w);
+                int kind;
+                if (CLS == CLS_GENERAL && q.mc) {
+                    kind = (int)(qrank[e] >> 30);
+                    w = kind_pairs<M, CLS>(q, S, k, kind);
+                } else {
+                    kind = set_kind<M, CLS>(q, S, k, w);
+                }
                 pairs += w;
                 if constexpr (CLS == CLS_TREE && MEMO == MEMO_DENSE) {
                     if (k > 2) {
@@ -827,12 +851,15 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
         }
 #endif
         if (CLS != CLS_TREE && heavy_level) {
-            // card(S) of every heavy set once (one thread per set)
-            const unsigned long long nh = d.n_heavy < p.heavy_cap ? d.n_heavy : p.heavy_cap;
-            const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-            for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride)
-                p.hcard[h] = card_of(q, p.heavy[h]);
-            grid_sync(p.gbar, nbar, &p.result->error);
+            // card(S) of every heavy set once (one thread per set); general
+            // graphs with memo connectivity wrote it with the heavy list
+            if (!(CLS == CLS_GENERAL && q.mc)) {
+                const unsigned long long nh = d.n_heavy < p.heavy_cap ? d.n_heavy : p.heavy_cap;
+                const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+                for (unsigned long long h = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += stride)
+                    p.hcard[h] = card_of(q, p.heavy[h]);
+                grid_sync(p.gbar, nbar, &p.result->error);
+            }
             TRACE(7);
             heavy_phase<M, CLS, MEMO>(p, k, item, q, v, rtab, gen, d, sp, sc, spr);
             TRACE(7);

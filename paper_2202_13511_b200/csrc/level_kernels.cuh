@@ -87,6 +87,11 @@ template <typename M> struct Params {
     unsigned long long* wh;                // [heavy_cap + 1] exclusive heavy pair prefix
     Key* bkey;                             // [heavy_cap] cross-warp (cost, left) min
     double* hcard;                         // [heavy_cap] card(S) of heavy sets (computed once)
+    // general graphs with memo connectivity (q.mc): per heavy set its kind |
+    // (number of blocks << 2), and its first kHeavyBlk blocks (KIND_BLOCKS),
+    // written with the heavy list so work items skip set_kind / Find-Blocks
+    unsigned int* hinfo;                   // [heavy_cap]
+    M* hblk;                               // [heavy_cap * kHeavyBlk]
     unsigned long long* bdone;             // [heavy_cap] pairs merged so far
     unsigned int* first_heavy;             // [fh_cap] heavy set holding item i's first pair
     unsigned long long fh_cap;
@@ -126,6 +131,9 @@ template <typename M> struct Params {
     // general graphs: sets with more join-pair candidates than this go to the
     // warp-parallel heavy phase (CCC) instead of one thread (light)
     unsigned int light_max;
+    // general graphs on the bitmask memo: the cost array was filled with
+    // kMemoAbsent at staging, so connectivity checks may probe it (reading R20)
+    int memo_conn;
     unsigned long long clique_split_w;     // k_dp_clique: split levels whose sets exceed this many pairs + 1
     double clique_set_cost;                // k_dp_clique: per-set overhead of the group cost model, in pairs
     unsigned long long clique_csize_min;   // k_dp_clique: smallest warp chunk of the split path, in pairs
@@ -153,6 +161,7 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
 template <typename M, int MEMO>
 struct PairSink {
     static constexpr int NP = (MEMO != MEMO_HASH) ? 4 : 2;
+    static constexpr bool kChk = true;     // supports chk (reading R20)
     const MemoPtrs* P;                     // kernel parameter space
     const MemoView* v;
     const unsigned int* rtab;
@@ -163,6 +172,10 @@ struct PairSink {
     double cS;
     Key best;
     unsigned long long nprobe;
+    // reading R20: with chk set, a pair (A, B) counts (nvalid) and competes only
+    // when both probes found their set, i.e. both sides are connected
+    bool chk;
+    unsigned long long nvalid;
 
     __device__ __forceinline__ void init(const MemoPtrs* P_, unsigned int gen_, const MemoView* v_,
                                          const unsigned int* rt, const SQ<M>* q_, double card) {
@@ -175,6 +188,8 @@ struct PairSink {
         cS = card;
         best = key_inf();
         nprobe = 0;
+        chk = false;
+        nvalid = 0;
     }
     __device__ __forceinline__ void flush() {
         if (!cnt) return;
@@ -191,6 +206,10 @@ struct PairSink {
 #pragma unroll
         for (int u = 0; u < NP; u++) {
             if (u < cnt) {
+                if (chk) {
+                    if (!memo_present(c[2 * u]) || !memo_present(c[2 * u + 1])) continue;
+                    nvalid++;
+                }
                 const double x = __dadd_rn(__dadd_rn(c[2 * u], c[2 * u + 1]), cS);
                 const Key key{(unsigned long long)__double_as_longlong(x),
                               (unsigned long long)(A[u] < B[u] ? A[u] : B[u])};
@@ -377,6 +396,7 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
         q.n = n;
         q.dpsub = p.q->dpsub;              // set_kind reads it
         q.nbtab = 0;                       // connected() takes the loop (no byte tables here)
+        q.mc = nullptr;                    // and BFS connectivity (reading R20 is MEMO_MASK only)
     }
     const unsigned long long rmask = p.tiles_ring - 1;
     const unsigned long long epoch = lookback_epoch(p, k);
@@ -555,6 +575,48 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
     } else {
         nb = find_blocks(q, S, blk);
     }
+    if constexpr (Sink::kChk) if (nb == 1 && q.mc) {   // one block S: S_left = lb (grow(lb, lb) = lb);
+        const M lo = lowbit(S), R = S ^ lo;    // the sink's probes of lb and rb are the CCP test (R20)
+        M sub = deposit<M>(j0, R);
+        sink.flush();
+        sink.chk = true;
+        for (unsigned long long j = j0; j < j1; j++) {
+            const M lb = lo | sub;
+            sub = (sub - R) & R;
+            sink.add(lb, S ^ lb);
+        }
+        sink.flush();
+        sink.chk = false;
+        nccp += sink.nvalid;
+        sink.nvalid = 0;
+        return;
+    }
+    if constexpr (Sink::kChk) if (q.mc) {  // reading R20: S_left = grow(lb, S \ rb) is connected
+        sink.flush();                          // iff lb is, so the sink's probes are the CCP test
+        sink.chk = true;
+        unsigned long long base = 0;
+        for (int bi = 0; bi < nb && base < j1; bi++) {
+            const M Bm = blk[bi];
+            const unsigned long long wb = (1ull << (popc(Bm) - 1)) - 1;
+            if (base + wb > j0) {
+                const unsigned long long a0 = (j0 > base ? j0 - base : 0), a1 = (j1 - base < wb ? j1 - base : wb);
+                const M lo = lowbit(Bm), R = Bm ^ lo;
+                M sub = deposit<M>(a0, R);
+                for (unsigned long long j = a0; j < a1; j++) {
+                    const M lb = lo | sub;
+                    sub = (sub - R) & R;
+                    const M A = grow(q, lb, S & ~(Bm ^ lb));
+                    sink.add(A, S ^ A);
+                }
+            }
+            base += wb;
+        }
+        sink.flush();
+        sink.chk = false;
+        nccp += sink.nvalid;
+        sink.nvalid = 0;
+        return;
+    }
     unsigned long long base = 0;
     for (int bi = 0; bi < nb && base < j1; bi++) {
         const M Bm = blk[bi];
@@ -571,7 +633,7 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
         for (unsigned long long j = a0; j < a1; j++) {
             const M lb = lo | sub, rb = Bm ^ lb;
             sub = (sub - R) & R;
-            if (!complete && !(connected(q, lb) && connected(q, rb))) continue;   // CCP block
+            if (!complete && !(conn_sub(q, lb) && conn_sub(q, rb))) continue;   // CCP block
             nccp++;
             const M A = grow(q, lb, S & ~rb);
             sink.add(A, S ^ A);                                        // S_right = S \ S_left
@@ -886,7 +948,7 @@ __device__ __forceinline__ void eval_blocks_ccc(const SQ<M>& q, M S, int kind, u
             M A = 0;
             if (j < a1) {
                 const M lb = lo | sub, rb = Bm ^ lb;
-                valid = complete || (connected(q, lb) && connected(q, rb));   // CCP block
+                valid = complete || (conn_sub(q, lb) && conn_sub(q, rb));     // CCP block
                 if (valid) A = grow(q, lb, S & ~rb);
             }
             sub = ((sub | ~R) + D32) & R;
@@ -913,6 +975,64 @@ __device__ __forceinline__ void eval_blocks_ccc(const SQ<M>& q, M S, int kind, u
     __syncwarp();
 }
 
+// Block-decomposed set S (reading R20, one warp, candidates [a, b) in block
+// order).  For a block B of S and v in B let H_v = grow({v}, (S \ B) + v), the
+// part of S that hangs off B at v (H_v = {v} unless v is a cut vertex with
+// neighbours outside B).  The H_v of B partition S and meet only at B's
+// vertices, so for a split (lb, rb) of B
+//     S_left = grow(lb, S \ rb) = OR of H_v over v in lb
+//     S_right = S \ S_left      = OR of H_v over v in rb
+// and S_left is connected iff lb is (a hanging part touches B at one vertex
+// only).  So no per-candidate BFS: lanes take interleaved candidates, OR in
+// the hanging parts of the cut vertices in lb (usually none or one), and the
+// sink's probes of S_left and S_right are the CCP test of (lb, rb)
+// (P:553-560).  hang[] is the warp's scratch (>= MaxN entries).
+// The blocks come from the heavy list's cache (gblk, nb <= kHeavyBlk) or are
+// found again.
+template <typename M, typename Sink>
+__device__ __forceinline__ void eval_blocks_hang(const SQ<M>& q, M S, unsigned long long a, unsigned long long b,
+                                                 Sink& sink, M* hang, M lblk, int nb) {
+    const unsigned int lane = threadIdx.x & 31;
+    M blk[MaxN<M>::value];
+    const bool cached = nb <= kHeavyBlk;   // lane i holds cached block i & 7
+    if (!cached) nb = find_blocks(q, S, blk);
+    sink.chk = true;
+    unsigned long long base = 0;
+    for (int bi = 0; bi < nb && base < b; bi++) {
+        const M Bm = cached ? __shfl_sync(0xffffffffu, lblk, bi) : blk[bi];
+        const int bsz = popc(Bm);
+        const unsigned long long wb = (1ull << (bsz - 1)) - 1;
+        if (base + wb <= a) {
+            base += wb;
+            continue;
+        }
+        const unsigned long long a0 = (a > base ? a - base : 0), a1 = (b - base < wb ? b - base : wb);
+        const M ext = S & ~Bm;
+        M C = 0;                               // vertices of B with neighbours outside B
+        for (M T = Bm; T; T &= T - 1)
+            if (q.adj[ctz(T)] & ext) C |= lowbit(T);
+        __syncwarp();
+        if ((int)lane < popc(C)) {
+            const int v = nth_bit(C, (int)lane);
+            hang[v] = grow(q, bitm<M>(v), ext | bitm<M>(v));
+        }
+        __syncwarp();
+        const M lo = lowbit(Bm), R = Bm ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
+        unsigned long long j = a0 + lane;
+        M sub = j < a1 ? deposit<M>(j, R) : 0;
+        for (; j < a1; j += 32) {
+            const M lb = lo | sub;
+            M A = lb;
+            for (M T = lb & C; T; T &= T - 1) A |= hang[ctz(T)];
+            sink.add(A, S ^ A);
+            sub = ((sub | ~R) + D) & R;
+        }
+        base += wb;
+    }
+    sink.flush();
+    __syncwarp();
+}
+
 template <typename M, int CLS, int MEMO>
 __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, const SQ<M>& q, const MemoView& v,
                             const unsigned int* rtab, unsigned int gen, const LevelDesc& d,
@@ -934,14 +1054,31 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
         if (c1 > d.heavy_pairs) c1 = d.heavy_pairs;
         unsigned long long h = p.first_heavy[g * G];
         for (; h < d.n_heavy; h++) {
-            const unsigned long long W0 = p.wh[h], w = p.wh[h + 1] - W0;
+            // the set's record in one memory round trip: every load is issued
+            // before the first use (general graphs: lane l also fetches cached
+            // block l & 7)
+            const unsigned long long W0 = p.wh[h], W1 = p.wh[h + 1];
+            const M S = p.heavy[h];
+            const double hc = p.hcard[h];
+            unsigned int inf = 0;
+            M lblk = 0;
+            if (CLS == CLS_GENERAL && q.mc) {
+                inf = p.hinfo[h];
+                lblk = p.hblk[h * kHeavyBlk + (lane & (kHeavyBlk - 1))];
+            }
+            const unsigned long long w = W1 - W0;
             if (W0 >= c1) break;
             const unsigned long long a = (c0 > W0 ? c0 - W0 : 0), b = (c1 - W0 < w ? c1 - W0 : w);
-            const M S = p.heavy[h];
             unsigned long long wk;
-            const int kind = set_kind<M, CLS>(q, S, k, wk);
+            int kind, hnb = 0;
+            if (CLS == CLS_GENERAL && q.mc) {
+                kind = (int)(inf & 3u);
+                hnb = (int)(inf >> 2);
+            } else {
+                kind = set_kind<M, CLS>(q, S, k, wk);
+            }
             PairSink<M, MEMO> sink;
-            sink.init(&p.memo, gen, &v, rtab, &q, p.hcard[h]);
+            sink.init(&p.memo, gen, &v, rtab, &q, hc);
             const unsigned long long cnt = b - a;
             if (kind == KIND_COMPLETE) {
                 // lane-interleaved pairs j = a + lane + 32 i: the lanes' left
@@ -957,6 +1094,24 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                     sub = ((sub | ~R) + D) & R;
                     nccp++;
                 }
+            } else if (CLS == CLS_GENERAL && q.mc && (kind == KIND_ONEBLOCK || (q.dpsub && kind == KIND_BLOCKS))) {
+                // one block S (or every set, DPSUB ablation): S_left = lb, and
+                // the probes of lb and rb are the CCP test (reading R20); lanes
+                // interleaved as for complete sets
+                const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
+                unsigned long long j = a + lane;
+                M sub = j < b ? deposit<M>(j, R) : 0;
+                sink.chk = true;
+                for (; j < b; j += 32) {
+                    const M A = lo | sub;
+                    sink.add(A, S ^ A);
+                    sub = ((sub | ~R) + D) & R;
+                }
+                sink.flush();
+                nccp += sink.nvalid;
+            } else if (CLS == CLS_GENERAL && q.mc && kind == KIND_BLOCKS) {
+                eval_blocks_hang<M>(q, S, a, b, sink, s_ccc[threadIdx.x >> 5], lblk, hnb);
+                nccp += sink.nvalid;
             } else if (CLS == CLS_GENERAL && kind >= KIND_BLOCKS && !p.no_ccc) {
                 eval_blocks_ccc<M>(q, S, kind, a, b, sink, nccp, s_ccc[threadIdx.x >> 5]);
             } else {                               // lane-contiguous chunks of [a, b)

@@ -34,7 +34,7 @@ thread_local std::string g_tls_error;
 
 struct DevLayout {
     size_t query = 0, desc = 0, result = 0, gbar = 0, df = 0, segcnt = 0, rank = 0, tiles = 0, light = 0, heavy = 0, wh = 0, bkey = 0, bdone = 0,
-           hcard = 0,
+           hcard = 0, hinfo = 0, hblk = 0,
            fh = 0, arena = 0, cold = 0, dcost = 0, dleft = 0, memo_end = 0, end = 0;
     int memo_kind = MEMO_HASH;
     bool mask_memo = false;               // dense arrays indexed by bitmask (MEMO_MASK)
@@ -158,6 +158,7 @@ struct mpdp_ctx {
     uint32_t batch_cap = 0;
     bool batch_attr = false;
     int star_hub = -1;                    // star queries: the relation adjacent to all others
+    bool memo_conn = false;               // general graph, bitmask memo pre-filled absent (R20)
     int star_occ = 0;                     // k_dp_star CTAs per SM
     int cluster_size = 0;                 // k_dp_tree_cluster: CTAs per cluster (0 = not probed yet)
     int clique_df_occ = 0;                // k_dp_clique_df (ablation) CTAs per SM
@@ -376,11 +377,8 @@ static void fill_query(mpdp_ctx* c, const mpdp_query_graph* g, const std::vector
 
 // general graphs: sets with more CCP-checked candidates than this are heavy
 static unsigned int light_max_general() {
-    static const unsigned int v = [] {
-        const char* e = getenv("MPDP_DEBUG_LIGHT_GENERAL");     // experiments only
-        return e ? (unsigned int)std::max(1, std::min(32, atoi(e))) : kLightGeneral;
-    }();
-    return v;
+    const char* e = getenv("MPDP_DEBUG_LIGHT_GENERAL");         // experiments only
+    return e ? (unsigned int)std::max(1, std::min(32, atoi(e))) : kLightGeneral;
 }
 
 static unsigned long long heavy_pair_bound(int n, int k, int cls) {
@@ -395,6 +393,10 @@ static unsigned long long heavy_pair_bound(int n, int k, int cls) {
 static unsigned long long level_item(int n, int k, int cls, unsigned long long fh_cap) {
     const unsigned long long ub = heavy_pair_bound(n, k, cls);
     unsigned long long item = 256;
+    if (cls == CLS_GENERAL) {
+        const char* e = getenv("MPDP_DEBUG_ITEM_GENERAL");     // experiments only
+        item = e ? std::max(32ull, strtoull(e, nullptr, 10)) : 256ull;
+    }
     if (fh_cap && ub / fh_cap + 1 > item) item = ub / fh_cap + 1;
     return (item + 31) / 32 * 32;
 }
@@ -505,7 +507,7 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     if (L.mask_memo && c->cls == CLS_CLIQUE)
         heavy_cap = std::max<unsigned long long>(heavy_cap, 8ull * kMaxGrid * (kBlock / 32));
     list_cap = std::min<unsigned long long>(list_cap, (avail / 2) / 16);   // fused: two lists of (rank << 32 | mask)
-    heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 40));
+    heavy_cap = std::min<unsigned long long>(heavy_cap, (avail / 2) / (msz + 44 + msz * kHeavyBlk));
     if (L.mask_memo && c->cls == CLS_CLIQUE && heavy_cap < 8ull * kMaxGrid * (kBlock / 32))
         return fail(c, MPDP_ERR_CAPACITY, "workspace too small for the clique merge slots");
     L.tiles = take(sizeof(TileRec) * tiles_cap);
@@ -515,6 +517,8 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.bkey = take(16 * heavy_cap);
     L.bdone = take(8 * heavy_cap);
     L.hcard = take(8 * heavy_cap);
+    L.hinfo = take(4 * heavy_cap);
+    L.hblk = take(msz * kHeavyBlk * heavy_cap);
     L.fh = take(4 * fh_need);
     L.end = off;
     if (L.end > c->ws_bytes) return fail(c, MPDP_ERR_INTERNAL, "layout overflow");
@@ -577,6 +581,8 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.bkey = reinterpret_cast<Key*>(b + L.bkey);
     p.bdone = reinterpret_cast<unsigned long long*>(b + L.bdone);
     p.hcard = reinterpret_cast<double*>(b + L.hcard);
+    p.hinfo = reinterpret_cast<unsigned int*>(b + L.hinfo);
+    p.hblk = reinterpret_cast<M*>(b + L.hblk);
     p.first_heavy = reinterpret_cast<unsigned int*>(b + L.fh);
     p.fh_cap = L.fh_cap;
     p.tiles = reinterpret_cast<TileRec*>(b + L.tiles);
@@ -589,6 +595,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.inv_load = 1.0 / c->load_factor;
     p.no_ccc = (c->flags & MPDP_FLAG_NO_CCC) ? 1 : 0;
     p.light_max = light_max_general();
+    p.memo_conn = c->memo_conn ? 1 : 0;
     p.clique_split_w = getenv("MPDP_DEBUG_CLIQUE_SPLIT") ? strtoull(getenv("MPDP_DEBUG_CLIQUE_SPLIT"), nullptr, 10) : 4096;
     p.clique_set_cost = getenv("MPDP_DEBUG_CLIQUE_SETCOST") ? atof(getenv("MPDP_DEBUG_CLIQUE_SETCOST")) : kCliqueSetCost;
     p.clique_csize_min = getenv("MPDP_DEBUG_CLIQUE_CSIZE") ? strtoull(getenv("MPDP_DEBUG_CLIQUE_CSIZE"), nullptr, 10) : 512;
@@ -1657,6 +1664,11 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
     if (clear) CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.arena, 0, c->lay.cold - c->lay.arena, c->stream));
     c->last_width = width;
     c->last_memo = c->lay.memo_kind;
+    // reading R20: general graphs on the bitmask memo test connectivity of
+    // subsets by probing the cost array, so every slot starts absent
+    c->memo_conn = c->lay.mask_memo && c->cls == CLS_GENERAL && !getenv("MPDP_DEBUG_BFS_CONN");
+    if (c->memo_conn)
+        CUDA_TRY(c, cudaMemsetAsync(c->ws + c->lay.dcost, 0xff, sizeof(double) << n, c->stream));
     if (c->lay.memo_kind == MEMO_DENSE && c->rank_n != n) {       // chunked colex-rank tables
         const RankGeom rg = rank_geom(n);
         std::vector<unsigned int>& tab = c->rank_cache[n];       // built once per n

@@ -31,6 +31,7 @@ __host__ __device__ constexpr size_t small_smem_bytes(int n) {
 }
 
 struct SmallSink {
+    static constexpr bool kChk = false;    // CCP tests by BFS (reading R20 is MEMO_MASK only)
     const double* cost;
     double cS;
     Key best;

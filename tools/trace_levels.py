@@ -12,7 +12,7 @@ PH = ["start", "ticket", "enum", "queued", "evald", "counted", "barrier", "heavy
 L = mpdp.load_library()
 L.mpdp_debug_trace.restype = C.c_int
 L.mpdp_debug_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int]
-with mpdp.Context(device=0, workspace_bytes=4 << 30) as ctx:
+with mpdp.Context(device=0, workspace_bytes=4 << 30, flags=int(os.environ.get("MPDP_FLAGS", "0"))) as ctx:
     for name in sys.argv[1:]:
         topo, n = name.rsplit("-", 1)
         g = W.generate(topo, int(n), 0)
