@@ -198,6 +198,23 @@ typedef struct {
  * per-level ncclAllGather exchange and the counter ncclAllReduce execute on a
  * single GPU (bit-identical results to the single-GPU kernels)            */
 #define MPDP_FLAG_NCCL_SELF 8192u
+/* flags (multi-GPU contexts, star queries): the FUSED PEER EXCHANGE instead of
+ * per-level ncclAllGather (sets of one size are independent,
+ * P:214, and a set reads only its subsets).  One
+ * k_dp_star launch per rank; each chunk of sets stores its costs into every
+ * rank's memo replica (NVLink peer stores) and adds its completion count to
+ * every replica's per-(level, largest element) counters, so a chunk of level k
+ * waits in its own replica for exactly the level-(k-1) sets it reads and no
+ * level ends in a launch or a collective.  With MPDP_FLAG_SIMULATE_WORLD the W
+ * ranks are the CTA groups (blockIdx mod W) of ONE cooperative launch over the
+ * W shards of the workspace; across GPUs call mpdp_ctx_open_peers first.
+ * Results are bit-identical to the single-GPU kernel; every rank extracts the
+ * plan from its own replica.  Other query shapes keep the NCCL path.        */
+#define MPDP_FLAG_FUSED_EXCHANGE 16384u
+
+/* Bytes of one rank's peer record for mpdp_ctx_open_peers: the CUDA IPC
+ * handle of the context's workspace (64 B) and its size (8 B). */
+#define MPDP_PEER_RECORD_BYTES 72
 
 typedef struct mpdp_ctx mpdp_ctx;
 
@@ -207,6 +224,21 @@ typedef struct mpdp_ctx mpdp_ctx;
  * CUDA (no device), OOM, NCCL. */
 mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out);
 mpdp_status mpdp_ctx_destroy(mpdp_ctx* ctx);
+
+/* Fused peer exchange across GPUs (MPDP_FLAG_FUSED_EXCHANGE, world > 1 over
+ * NCCL).  mpdp_ctx_peer_record writes this rank's MPDP_PEER_RECORD_BYTES-byte
+ * record into out (host memory, caller-owned): the IPC handle of the
+ * workspace, which must have been allocated by the library (cfg->workspace ==
+ * NULL), and its size.  The caller gathers the records of all ranks (any host
+ * collective) and passes them, rank-ordered and contiguous (world x
+ * MPDP_PEER_RECORD_BYTES bytes, host memory, read only during the call), to
+ * mpdp_ctx_open_peers, which maps every other rank's workspace into this
+ * process (cudaIpcOpenMemHandle; the mappings are released by
+ * mpdp_ctx_destroy).  All ranks must use equal workspace sizes (identical
+ * layouts).  Errors: INVALID_ARGUMENT (NULL pointers, world == 1, simulated
+ * world, adopted workspace, unequal sizes), CUDA (IPC not available). */
+mpdp_status mpdp_ctx_peer_record(mpdp_ctx* ctx, void* out);
+mpdp_status mpdp_ctx_open_peers(mpdp_ctx* ctx, const void* records);
 
 /* Optimise one query end to end: validate, copy the graph host->device, run
  * every level, extract the plan on the device and copy the result back.

@@ -49,6 +49,80 @@ __device__ __forceinline__ void df_red_add(unsigned int* p, unsigned int v) {
 }
 __device__ __forceinline__ void df_fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
+// The rank view of a CTA (shared memory, written by thread 0 before the first
+// __syncthreads): which rank it works for and that rank's replica.  Without an
+// XrTable there is one rank and the replica is the launch's own state.
+struct DfRank {
+    int W, r;                              // ranks, this CTA's rank
+    unsigned int nctas, cta;               // CTAs of this rank, this CTA's index among them
+    DataflowDev* df;                       // the rank's replica: dataflow state, descriptors, result,
+    ResultDev* result;                     // memo arrays
+    LevelDesc* desc;
+    double* dcost;
+    double* dcard;
+    unsigned int* dleft;
+    const XrTable* xr;
+    // every replica (XR: the fused exchange is compiled in; otherwise W == 1)
+    template <bool XR> __device__ int ranks() const { return XR ? W : 1; }
+    template <bool XR> __device__ DataflowDev* dfs(int s) const { return XR ? xr->df[s] : df; }
+    template <bool XR> __device__ LevelDesc* descs(int s) const { return XR ? xr->desc[s] : desc; }
+    template <bool XR> __device__ double* costs(int s) const { return XR ? xr->cost[s] : dcost; }
+};
+__device__ __forceinline__ void df_rank_init(DfRank& x, const Params<uint32_t>& p) {
+    if (p.xr) {
+        const XrTable& t = *p.xr;
+        x.W = t.W;
+        x.r = t.emulate ? (int)(blockIdx.x % (unsigned int)t.W) : t.rank;
+        x.nctas = t.emulate ? (gridDim.x - (unsigned int)x.r + (unsigned int)t.W - 1) / (unsigned int)t.W : gridDim.x;
+        x.cta = t.emulate ? blockIdx.x / (unsigned int)t.W : blockIdx.x;
+        x.df = t.df[x.r];
+        x.result = t.result[x.r];
+        x.desc = t.desc[x.r];
+        x.dcost = t.cost[x.r];
+        x.dcard = t.card[x.r];
+        x.dleft = t.left[x.r];
+        x.xr = p.xr;
+    } else {
+        x.W = 1;
+        x.r = 0;
+        x.nctas = gridDim.x;
+        x.cta = blockIdx.x;
+        x.df = p.df;
+        x.result = p.result;
+        x.desc = p.desc;
+        x.dcost = p.memo.dcost;
+        x.dcard = p.memo.dcard;
+        x.dleft = p.memo.dleft;
+        x.xr = nullptr;
+    }
+}
+// Across ranks (peer memory) the synchronisation is at system scope.
+template <bool XR>
+__device__ __forceinline__ void df_red_add_x(unsigned int* p, unsigned int v) {
+    if (XR) asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    else asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+template <bool XR>
+__device__ __forceinline__ unsigned int df_ld_relaxed_x(const unsigned int* p) {
+    unsigned int v;
+    if (XR) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <bool XR>
+__device__ __forceinline__ void df_fence_rel_x() {
+    if (XR) __threadfence_system();
+    else __threadfence();
+}
+template <bool XR>
+__device__ __forceinline__ void df_fence_acq_x() {
+    if (XR) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// an abort pushes a rank's ticket counter here: local ticket u maps to the
+// global ticket u * W + r, which then lies past every chunk
+constexpr unsigned int kDfAbortTicket = 0x08000000u;
+
 // largest element of the colex-rank-r j-subset (j >= 1): the largest c with
 // C(c, j) <= r.  bin: 33 x 33 binomials (u32) in shared memory.
 __device__ __forceinline__ int colex_top(const unsigned int* bin, int j, unsigned int r) {
@@ -60,15 +134,21 @@ __device__ __forceinline__ int colex_top(const unsigned int* bin, int j, unsigne
 // One lane (the control warp's, after acquiring the chunk's memo writes and
 // a gpu-scope fence): publish sets [lo, hi) of level k -- colex ranks of
 // j-subsets, j = elements per set in the rank space -- per largest element.
-template <typename P>
-__device__ __forceinline__ void df_publish_colex(const P& p, const unsigned int* bin, int k, int j, unsigned int lo,
-                                                 unsigned int hi) {
+// Every replica's counters (fused exchange: the other ranks' through peer memory).
+// (ldf: the local dataflow state, p.df for one rank -- the constant bank, not
+// the shared-memory view)
+template <bool XR>
+__device__ __forceinline__ void df_publish_colex(const DfRank& x, DataflowDev* ldf, const unsigned int* bin, int k,
+                                                 int j, unsigned int lo, unsigned int hi) {
     const int ma = colex_top(bin, j, lo), mb = colex_top(bin, j, hi - 1);
     for (int m = ma; m <= mb; m++) {
         const unsigned int a = lo > bin[m * 33 + j] ? lo : bin[m * 33 + j];
         const unsigned int e = bin[(m + 1) * 33 + j];
         const unsigned int b = hi < e ? hi : e;
-        df_red_add(&p.df->done[k][m], b - a);
+        if (XR)
+            for (int s = 0; s < x.W; s++) df_red_add_x<XR>(&x.xr->df[s]->done[k][m], b - a);
+        else
+            df_red_add_x<XR>(&ldf->done[k][m], b - a);
     }
 }
 
@@ -82,11 +162,11 @@ __device__ __forceinline__ void df_add_release_cta(unsigned int* p, unsigned int
 }
 // Stop the launch: flag the error, and push the ticket counter past every
 // ticket so that no CTA claims another chunk.
-template <typename P>
-__device__ __forceinline__ void df_abort(const P& p, unsigned int err) {
-    atomicOr(&p.df->error, err);
-    atomicExch(&p.df->abort, 1u);
-    atomicMax(&p.df->ticket, 0x40000000u);
+template <bool XR>
+__device__ __forceinline__ void df_abort(const DfRank& x, unsigned int err) {
+    atomicOr(&x.df->error, err);
+    for (int s = 0; s < x.ranks<XR>(); s++) atomicExch_system(&x.dfs<XR>(s)->abort, 1u);
+    atomicMax(&x.df->ticket, kDfAbortTicket);
 }
 
 // ---------------------------------------------------------------------------
@@ -150,8 +230,8 @@ __device__ __forceinline__ void df_finish(DfShared& sh, unsigned int i) {
 // = sets of level k1 with largest element j, publish(const DfSlot&) (after the
 // chunk's writes are acquired and fenced).  Lane 0 works; the whole warp
 // arrives at the handover barriers.
-template <typename P, typename Sched>
-__device__ void df_control(const P& p, const Sched& S, DfShared& sh) {
+template <bool XR, typename P, typename Sched>
+__device__ void df_control(const P& p, const Sched& S, DfShared& sh, const DfRank& x) {
     const unsigned int lane = threadIdx.x & 31;
     const unsigned long long t0 = globaltimer_ns();   // timeout origin: this CTA's start
     const unsigned int total = S.total();
@@ -160,17 +240,25 @@ __device__ void df_control(const P& p, const Sched& S, DfShared& sh) {
     fly0.t = fly1.t = ~0u;
     unsigned long long w0 = 0;             // watchdog origin of the current wait
     unsigned int t = 0;
-    if (lane == 0) t = atomicAdd(&p.df->ticket, 1u);
+    DataflowDev* const ldf = XR ? x.df : p.df;   // registers, not the shared view
+    ResultDev* const lres = XR ? x.result : p.result;
+    // this rank's chunks: local ticket u is global ticket u * W + r
+    auto claim = [&]() -> unsigned int {
+        const unsigned int u = atomicAdd(&ldf->ticket, 1u);
+        if (!XR) return u;
+        return u >= kDfAbortTicket ? ~0u : u * (unsigned int)x.W + (unsigned int)x.r;
+    };
+    if (lane == 0) t = claim();
     unsigned long long st_slot = 0, st_dep = 0, st_n = 0;   // MPDP_DEBUG_DF_STATS
     // publish a finished chunk in flight (lane 0); true if slot s is free
     auto retire = [&](int s) -> bool {
         DfSlot& f = s ? fly1 : fly0;
         if (f.t == ~0u) return true;
         if (df_ld_acquire_cta(&sh.done[s]) < kWarps) return false;
-        __threadfence();                   // release the CTA's memo writes at gpu scope
+        df_fence_rel_x<XR>();              // release the CTA's memo writes (every replica)
         S.publish(f);
         const unsigned long long now = globaltimer_ns();
-        for (int k = f.k; k <= f.k2; k++) atomicMax(&p.df->t_done[k], now);
+        for (int k = f.k; k <= f.k2; k++) atomicMax(&ldf->t_done[k], now);
         sh.done[s] = 0;
         f.t = ~0u;
         return true;
@@ -180,15 +268,15 @@ __device__ void df_control(const P& p, const Sched& S, DfShared& sh) {
     auto stalled = [&]() -> bool {
         if (++spins > 64) __nanosleep(32);         // spin hot first: most waits are short
         if ((spins & 63u) != 0) return false;
-        if (df_ld_relaxed(&p.df->abort)) return true;
+        if (df_ld_relaxed_x<XR>(&ldf->abort)) return true;
         if (p.timeout_ns && globaltimer_ns() - t0 > p.timeout_ns) {
-            df_abort(p, ERR_TIMEOUT);
+            df_abort<XR>(x, ERR_TIMEOUT);
             return true;
         }
         const unsigned long long now = globaltimer_ns();
         if (!w0) w0 = now;
         if (now - w0 > 2000000000ull) {    // never hang the device
-            df_abort(p, ERR_HANG);
+            df_abort<XR>(x, ERR_HANG);
             return true;
         }
         return false;
@@ -218,7 +306,7 @@ __device__ void df_control(const P& p, const Sched& S, DfShared& sh) {
                     spins = 0;
                     for (int j = sh.ready[k1] + 1; j <= m && go; j++) {
                         const unsigned int want = S.need_count(k1, j);
-                        while (df_ld_relaxed(&p.df->done[k1][j]) < want) {
+                        while (df_ld_relaxed_x<XR>(&ldf->done[k1][j]) < want) {
                             retire(s ^ 1);     // our own previous chunk may be what we wait for
                             if (stalled()) {
                                 go = false;
@@ -227,22 +315,22 @@ __device__ void df_control(const P& p, const Sched& S, DfShared& sh) {
                         }
                     }
                     if (go) {
-                        df_fence_acq_rel();    // acquire (+ L1 invalidation) once per advance
+                        df_fence_acq_x<XR>();  // acquire (+ L1 invalidation) once per advance
                         sh.ready[k1] = m;
                     }
                     if (p.df_stats) st_dep += globaltimer_ns() - ts1;
                 }
                 if (go && p.timeout_ns && globaltimer_ns() - t0 > p.timeout_ns) {
-                    df_abort(p, ERR_TIMEOUT);
+                    df_abort<XR>(x, ERR_TIMEOUT);
                     go = false;
                 }
                 // claim ahead, after the acquire fence (which would wait for
                 // the claim); its latency hides behind this chunk.  An abort
                 // pushes the counter past every ticket, so the claim sees it.
-                if (go) nxt = atomicAdd(&p.df->ticket, 1u);
+                if (go) nxt = claim();
             }
             if (!go) d.t = ~0u;
-            else if (t == p.dfl[d.k].base) p.result->t_level[d.k] = globaltimer_ns();
+            else if (t == p.dfl[d.k].base) lres->t_level[d.k] = globaltimer_ns();
             sh.slot[s] = d;
             (s ? fly1 : fly0) = d;
             t = nxt;
@@ -289,25 +377,44 @@ __device__ __forceinline__ void df_count(DfCounters& sc, int k, unsigned long lo
 // accumulate over the launches of a sharded query); returns true in the last
 // CTA out (after an acquire fence: every chunk of the launch is finished and
 // visible).
-template <typename P>
-__device__ bool df_exit(const P& p, DfCounters& sc) {
+// With several ranks every CTA adds its counters to every replica's
+// descriptors and then counts itself in every replica's `flushed`; the last
+// CTA of a rank waits until all CTAs of all ranks have flushed into its
+// replica -- each flushed after its last chunk was published to every
+// replica, so the replica is then complete -- before it extracts.
+template <bool XR, typename P>
+__device__ bool df_exit(const P& p, DfCounters& sc, const DfRank& x) {
     __syncthreads();
     for (int j = threadIdx.x; j <= p.n; j += blockDim.x) {
         if (!((p.count_levels >> j) & 1ull)) continue;
-        LevelDesc& d = p.desc[j];
-        if (sc.v[j][0]) {
-            atomicAdd(&d.pairs, sc.v[j][0]);
-            atomicAdd(&d.ccp, sc.v[j][0]);
+        for (int s = 0; s < x.ranks<XR>(); s++) {
+            LevelDesc& d = x.descs<XR>(s)[j];
+            if (sc.v[j][0]) {
+                atomicAdd_system(&d.pairs, sc.v[j][0]);
+                atomicAdd_system(&d.ccp, sc.v[j][0]);
+            }
+            if (sc.v[j][1]) atomicAdd_system(&d.probes, sc.v[j][1]);
+            if (sc.v[j][2]) atomicAdd_system(&d.n_light, sc.v[j][2]);
         }
-        if (sc.v[j][1]) atomicAdd(&d.probes, sc.v[j][1]);
-        if (sc.v[j][2]) atomicAdd(&d.n_light, sc.v[j][2]);
     }
     __shared__ int s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&p.df->exited, 1u) == gridDim.x - 1;
-        if (s_last) df_fence_acq_rel();
+        df_fence_rel_x<XR>();
+        if (XR)
+            for (int s = 0; s < x.W; s++) df_red_add_x<XR>(&x.dfs<XR>(s)->flushed, 1u);
+        s_last = atomicAdd(&x.df->exited, 1u) == x.nctas - 1;
+        if (XR && s_last) {
+            const unsigned long long w0 = globaltimer_ns();
+            while (df_ld_relaxed_x<XR>(&x.df->flushed) < x.xr->ctas_total) {
+                if (globaltimer_ns() - w0 > 4000000000ull) {   // never hang the device
+                    atomicOr(&x.df->error, ERR_HANG);
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+        if (s_last) df_fence_acq_x<XR>();
     }
     __syncthreads();
     return s_last;
@@ -319,26 +426,49 @@ __device__ bool df_exit(const P& p, DfCounters& sc) {
 // finish times are kept across the level launches of a sharded query and
 // cleared by the launch that extracts.
 template <typename P>
-__device__ void df_reset(const P& p) {
+__device__ void df_reset(const P& p, const DfRank& x) {
     __syncthreads();
-    DataflowDev& df = *p.df;
+    DataflowDev& df = *x.df;
     if (p.do_extract) {
-        if (threadIdx.x == 0) p.result->error = df.error;
+        if (threadIdx.x == 0) x.result->error = df.error;
         for (int j = threadIdx.x; j < kMaxN + 2; j += blockDim.x) {
-            p.result->t_done[j] = df.t_done[j];
+            x.result->t_done[j] = df.t_done[j];
             df.t_done[j] = 0;
         }
-        for (int j = threadIdx.x; j <= p.n; j += blockDim.x) p.desc[j] = LevelDesc{};
+        for (int j = threadIdx.x; j <= p.n; j += blockDim.x) x.desc[j] = LevelDesc{};
         __syncthreads();
         if (threadIdx.x == 0) df.error = 0;
     }
     for (int i = threadIdx.x; i < (kMaxN + 1) * kDfMaxElem; i += blockDim.x) (&df.done[0][0])[i] = 0;
-    for (unsigned long long i = threadIdx.x; i < p.zero_words; i += blockDim.x) p.bdone[i] = 0;   // merge counts
+    if (!p.xr)
+        for (unsigned long long i = threadIdx.x; i < p.zero_words; i += blockDim.x) p.bdone[i] = 0;   // merge counts
     if (threadIdx.x == 0) {
         df.ticket = 0;
         df.exited = 0;
         df.abort = 0;
+        df.flushed = 0;
     }
+}
+
+// Start of a query with several ranks: no rank may store into a peer's
+// replica before that peer has finished the previous query (its extraction
+// reads the replica, its reset clears the counters).  The first CTA of each
+// rank counts the rank in every replica's `epoch`; every CTA then waits for
+// W * query arrivals in its own replica.  Thread 0.
+template <typename P>
+__device__ void df_start_barrier(const P& p, const DfRank& x) {
+    if (x.cta == 0)
+        for (int s = 0; s < x.W; s++) df_red_add_x<true>(&x.dfs<true>(s)->epoch, 1u);
+    const unsigned int want = (unsigned int)x.W * p.xr_epoch;
+    const unsigned long long w0 = globaltimer_ns();
+    while ((int)(df_ld_relaxed_x<true>(&x.df->epoch) - want) < 0) {
+        if (globaltimer_ns() - w0 > 4000000000ull) {
+            df_abort<true>(x, ERR_HANG);
+            break;
+        }
+        __nanosleep(64);
+    }
+    df_fence_acq_x<true>();
 }
 
 }  // namespace mpdp

@@ -1026,6 +1026,7 @@ __host__ __device__ constexpr size_t clique_smem_bytes() { return sizeof(SQ<uint
 struct CliqueSched {
     const Params<uint32_t>& p;
     const unsigned int* bin;
+    const DfRank& x;
     __device__ unsigned int total() const { return p.dfl[p.k_end + 1].base; }
     __device__ void locate(unsigned int t, DfSlot& d) const {
         int k = p.k_begin;
@@ -1058,8 +1059,8 @@ struct CliqueSched {
     __device__ unsigned int need_count(int k1, int j) const { return bin[j * 33 + k1 - 1]; }
     __device__ void publish(const DfSlot& d) const {
         if (p.dfl[d.k].split) return;                   // split sets are published by their last contributor
-        df_publish_colex(p, bin, d.k, d.k, d.lo, d.hi);
-        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex(p, bin, k, k, p.share_lo[k], p.share_hi[k]);
+        df_publish_colex<false>(x, p.df, bin, d.k, d.k, d.lo, d.hi);
+        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex<false>(x, p.df, bin, k, k, p.share_lo[k], p.share_hi[k]);
     }
 };
 
@@ -1085,6 +1086,8 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
     __shared__ MemoView v;
     __shared__ DfCounters sc;
     __shared__ DfShared sh;
+    __shared__ DfRank xr;
+    if (threadIdx.x == 0) df_rank_init(xr, p);
     if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[0] = globaltimer_ns();   // kernel start
     load_query(q, p.q);
     for (int j = threadIdx.x; j <= kMaxN; j += blockDim.x) {
@@ -1109,7 +1112,7 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
     }
     __syncthreads();
     if (threadIdx.x >= kDfCompute) {
-        df_control(p, CliqueSched{p, bin}, sh);
+        df_control<false>(p, CliqueSched{p, bin, xr}, sh, xr);
     } else {
         int kc = p.k_begin;
         unsigned long long npairs = 0, nsets = 0;      // this thread, level kc
@@ -1157,9 +1160,9 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
         }
         flush();
     }
-    if (!df_exit(p, sc)) return;
+    if (!df_exit<false>(p, sc, xr)) return;
     if (p.do_extract && threadIdx.x < 32) clique_extract(p, q, v, bin);
-    df_reset(p);
+    df_reset(p, xr);
 }
 
 // Whole-query kernel for cliques with the bitmask memo: clique_level per level

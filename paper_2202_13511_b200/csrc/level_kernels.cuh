@@ -56,6 +56,35 @@ struct DataflowDev {
     unsigned int error;                    // ERR_* bits, kept until the extracting launch copies them
     unsigned long long t_done[kMaxN + 2];  // per level: when its last chunk finished (idem)
     unsigned int done[kMaxN + 1][kDfMaxElem];   // finished sets per (level, largest element)
+    // fused peer exchange (XrTable): CTAs of every rank that flushed their
+    // counters into this replica, and the start-of-query arrivals (monotonic,
+    // never reset: W per query)
+    unsigned int flushed;
+    unsigned int epoch;
+};
+
+struct ResultDev;
+// Fused exchange over peer memory: W ranks, each with a full
+// replica of the star memo.  A rank's chunks store their costs into EVERY
+// replica (NVLink peer stores) and add their completion counts to every
+// replica's done counters, so no level ends in a collective: a chunk of level
+// k waits, in its own replica, for exactly the sets of level k-1 it reads,
+// whichever rank wrote them.  In emulation (one GPU) the ranks are the CTA
+// groups blockIdx % W of one cooperative launch and the replicas are shards
+// of one workspace; across GPUs the pointers of the other ranks are peer
+// mappings (cudaIpcOpenMemHandle) and every rank launches its own kernel.
+constexpr int kMaxXr = 8;
+struct XrTable {
+    int W;                                 // ranks
+    int emulate;                           // 1: rank of a CTA = blockIdx.x % W (one launch)
+    int rank;                              // (emulate = 0) this process's rank
+    unsigned int ctas_total;               // CTAs over all ranks (counter flushes per replica)
+    double* cost[kMaxXr];                  // every replica's arrays (peer pointers but [rank])
+    double* card[kMaxXr];
+    unsigned int* left[kMaxXr];
+    DataflowDev* df[kMaxXr];
+    LevelDesc* desc[kMaxXr];
+    ResultDev* result[kMaxXr];
 };
 struct DfLevel {
     unsigned int base;                     // first ticket of the level (dfl[k_end + 1].base = total)
@@ -119,6 +148,8 @@ template <typename M> struct Params {
     // dataflow scheduling (k_dp_star, k_dp_clique): per level its tickets and
     // chunk geometry, the shared state, and the timeout (0 = none)
     DataflowDev* df;
+    const XrTable* xr;                     // k_dp_star: fused peer exchange (null: one rank)
+    unsigned int xr_epoch;                 // this query's index (start-of-query barrier of the ranks)
     DfLevel dfl[kMaxN + 2];
     unsigned long long timeout_ns;
     unsigned long long zero_words;         // k_init: bdone[0 .. zero_words) cleared (clique merge counts)
@@ -243,9 +274,9 @@ __global__ void k_init(const __grid_constant__ Params<M> p) {
     }
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) p.result->t_level[i] = p.result->t_done[i] = 0;
     for (int i = threadIdx.x; i < kTraceCap; i += blockDim.x) p.result->trace[i] = 0;
-    if (p.df) {                            // dataflow state of the next launch
-        unsigned int* w = reinterpret_cast<unsigned int*>(p.df);
-        for (unsigned int i = threadIdx.x; i < sizeof(DataflowDev) / 4; i += blockDim.x) w[i] = 0;
+    if (p.df) {                            // dataflow state of the next launch (not the
+        unsigned int* w = reinterpret_cast<unsigned int*>(p.df);   // monotonic start-barrier epoch)
+        for (unsigned int i = threadIdx.x; i < offsetof(DataflowDev, epoch) / 4; i += blockDim.x) w[i] = 0;
         __syncthreads();
         if (threadIdx.x == 0) p.result->t_done[0] = globaltimer_ns();   // (t_done[0]: k_init ran)
     }
@@ -1168,8 +1199,9 @@ __global__ void __launch_bounds__(kBlock, 2) k_eval_heavy(const __grid_constant_
 // level, ~15 us at n = 25).  Bit 1 of count_levels: this rank counts the n
 // singletons (level 1).
 template <typename M>
-__device__ void level_counters_warp(const Params<M>& p, ResultDev* r) {
+__device__ void level_counters_warp(const Params<M>& p, ResultDev* r, const LevelDesc* desc = nullptr) {
     const int n = p.n;
+    if (!desc) desc = p.desc;
     const unsigned int lane = threadIdx.x & 31;
     unsigned long long csg = 0, ccp = 0, pairs = 0, probes = 0;
     for (int j = (int)lane; j <= n; j += 32) {
@@ -1177,7 +1209,7 @@ __device__ void level_counters_warp(const Params<M>& p, ResultDev* r) {
         if (j == 1) {
             a = ((p.count_levels >> 1) & 1ull) ? (unsigned long long)n : 0ull;
         } else if (j >= 2 && ((p.count_levels >> j) & 1ull)) {
-            const LevelDesc& ds = p.desc[j];
+            const LevelDesc& ds = desc[j];
             a = ds.n_light + ds.n_heavy;
             b = ds.ccp;
             c = ds.pairs;

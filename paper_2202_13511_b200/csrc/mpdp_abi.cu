@@ -42,7 +42,8 @@ struct DevLayout {
     // perfect-hash memo replica (shard 0 = the fields above)
     int nshards = 1;
     size_t sh_desc[kMaxShards] = {}, sh_result[kMaxShards] = {}, sh_dcost[kMaxShards] = {}, sh_dleft[kMaxShards] = {},
-           sh_dcard[kMaxShards] = {};
+           sh_dcard[kMaxShards] = {}, sh_df[kMaxShards] = {};
+    size_t xr = 0;                        // XrTable of the fused peer exchange
     unsigned long long list_cap = 0, heavy_cap = 0, tiles_cap = 0, fh_cap = 0, arena_buckets = 0;
 };
 
@@ -112,6 +113,14 @@ struct mpdp_ctx {
     // communicator, every query on the sharded path with every level sharded
     bool nccl_self = false;
     bool multi = false;                   // the sharded path: world > 1 || nccl_self
+    // fused peer exchange (MPDP_FLAG_FUSED_EXCHANGE, star queries): every
+    // rank's workspace (IPC-mapped peers, [rank] = ws), the staging of the
+    // XrTable, and the number of fused-exchange queries run (start barrier)
+    unsigned char* peer_ws[kMaxXr] = {};
+    bool peers_open = false;
+    void* h_xr = nullptr;
+    unsigned int xr_epoch = 0;
+    bool xr_run = false;                  // the last run used the fused exchange
     NcclApi* nccl = nullptr;
     ncclComm_t comm = nullptr;
     ResultDev* h_results = nullptr;       // pinned, one per local shard
@@ -160,6 +169,7 @@ struct mpdp_ctx {
     int star_hub = -1;                    // star queries: the relation adjacent to all others
     bool memo_conn = false;               // general graph, bitmask memo pre-filled absent (R20)
     int star_occ = 0;                     // k_dp_star CTAs per SM
+    int star_occ_xr = 0;                  // k_dp_star<true> (fused peer exchange)
     int cluster_size = 0;                 // k_dp_tree_cluster: CTAs per cluster (0 = not probed yet)
     int clique_df_occ = 0;                // k_dp_clique_df (ablation) CTAs per SM
     bool clique_df_attr = false;
@@ -438,7 +448,9 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     L.desc = L.sh_desc[0];
     L.result = L.sh_result[0];
     L.gbar = take(64);
-    L.df = take(sizeof(DataflowDev));
+    for (int sh = 0; sh < nsh; sh++) L.sh_df[sh] = take(sizeof(DataflowDev));
+    L.df = L.sh_df[0];
+    L.xr = take(sizeof(XrTable));
     L.segcnt = take(4 * 2 * kMaxGrid);
     L.rank = take(sizeof(unsigned int) * 256 * (1 + 9 + 17 + 25));
     off = align_up(off, 256);
@@ -550,7 +562,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.memo.error = &reinterpret_cast<ResultDev*>(b + L.sh_result[shard])->error;
     p.memo_kind = L.memo_kind;
     p.gbar = reinterpret_cast<unsigned int*>(b + L.gbar);
-    p.df = reinterpret_cast<DataflowDev*>(b + L.df);
+    p.df = reinterpret_cast<DataflowDev*>(b + L.sh_df[shard]);
     // debug: per-CTA timing words of the dataflow kernels in the (unused by
     // them) level-list scratch
     p.df_stats = getenv("MPDP_DEBUG_DF_STATS") ? reinterpret_cast<unsigned long long*>(b + L.light) : nullptr;
@@ -1048,8 +1060,8 @@ static mpdp_status run_star(mpdp_ctx* c, Params<uint32_t> p) {
     }
     const size_t smem = star_smem_bytes();
     if (!c->star_occ) {
-        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_star, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->star_occ, k_dp_star, kDfThreads, smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_star<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->star_occ, k_dp_star<false>, kDfThreads, smem));
         if (c->star_occ < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
     }
     unsigned long long want = 1;
@@ -1069,7 +1081,7 @@ static mpdp_status run_star(mpdp_ctx* c, Params<uint32_t> p) {
     c->desc_clean = true;
     void* args[] = {const_cast<Params<uint32_t>*>(&p)};
     CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_star, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_star<false>, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
@@ -1155,6 +1167,90 @@ static mpdp_status exchange_level(mpdp_ctx* c, const Params<uint32_t>* P, int k,
     return MPDP_OK;
 }
 
+// Fused peer exchange (MPDP_FLAG_FUSED_EXCHANGE): one launch of
+// k_dp_star per rank whose chunks store their costs into every rank's replica
+// and count themselves in every replica's dataflow counters (XrTable,
+// level_kernels.cuh) -- the exchange overlaps the computation chunk by chunk
+// and no level ends in a launch or a collective.  Simulated world: the W ranks
+// are the CTA groups blockIdx % W of ONE cooperative launch over the W shards
+// of this workspace (ranks that wait on one another must be co-resident);
+// across GPUs the replicas are the IPC-mapped workspaces of
+// mpdp_ctx_open_peers, every rank extracts the plan from its own replica.
+static mpdp_status run_star_xr(mpdp_ctx* c) {
+    const int n = c->n, W = c->world;
+    if (W > kMaxXr) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "fused exchange: world > 8");
+    if (!c->simulate && !c->peers_open)
+        return fail(c, MPDP_ERR_INVALID_ARGUMENT, "fused exchange across GPUs needs mpdp_ctx_open_peers first");
+    const DevLayout& L = c->lay;
+    Params<uint32_t> p = make_params<uint32_t>(c, 0);
+    for (int k = 2; k <= n; k++) {                      // every level: all C(n-1, k-1) sets
+        p.share_lo[k] = 0;
+        p.share_hi[k] = (unsigned int)binom_u64(n - 1, k - 1);
+    }
+    const size_t smem = star_smem_bytes();
+    if (!c->star_occ_xr) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_star<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->star_occ_xr, k_dp_star<true>, kDfThreads, smem));
+        if (c->star_occ_xr < 1) return fail(c, MPDP_ERR_CUDA, "star kernel does not fit on an SM");
+    }
+    const unsigned int full = (unsigned int)std::min<unsigned long long>((unsigned long long)c->num_sms * c->star_occ_xr,
+                                                                         (unsigned long long)kMaxGrid);
+    const unsigned int grid = c->simulate ? full / (unsigned int)W * (unsigned int)W : full;
+    const unsigned int ctas_total = c->simulate ? grid : grid * (unsigned int)W;
+    plan_star_df(p, ctas_total);           // chunks sized for every CTA of every rank
+    p.shard_local = 1;                     // costs only cross ranks: card(S) local, splits re-derived
+    p.do_extract = 1;
+    XrTable t;
+    memset(&t, 0, sizeof(t));
+    t.W = W;
+    t.emulate = c->simulate ? 1 : 0;
+    t.rank = c->simulate ? 0 : c->rank;
+    t.ctas_total = ctas_total;
+    for (int s = 0; s < W; s++) {
+        unsigned char* base = c->simulate ? c->ws : c->peer_ws[s];
+        const int sh = c->simulate ? s : 0;
+        t.cost[s] = reinterpret_cast<double*>(base + L.sh_dcost[sh]);
+        t.card[s] = reinterpret_cast<double*>(base + L.sh_dcard[sh]);
+        t.left[s] = reinterpret_cast<unsigned int*>(base + L.sh_dleft[sh]);
+        t.df[s] = reinterpret_cast<DataflowDev*>(base + L.sh_df[sh]);
+        t.desc[s] = reinterpret_cast<LevelDesc*>(base + L.sh_desc[sh]);
+        t.result[s] = reinterpret_cast<ResultDev*>(base + L.sh_result[sh]);
+    }
+    if (!c->h_xr && cudaMallocHost(&c->h_xr, sizeof(XrTable)) != cudaSuccess)
+        return fail(c, MPDP_ERR_OOM, "pinned host allocation failed");
+    memcpy(c->h_xr, &t, sizeof(t));
+    CUDA_TRY(c, cudaMemcpyAsync(c->ws + L.xr, c->h_xr, sizeof(XrTable), cudaMemcpyHostToDevice, c->stream));
+    p.xr = reinterpret_cast<const XrTable*>(c->ws + L.xr);
+    p.xr_epoch = ++c->xr_epoch;
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    unsigned int nl = 1;
+    if (!c->desc_clean) {                  // the local replicas' dataflow state and descriptors
+        for (int sh = 0; sh < L.nshards; sh++) {
+            k_init<uint32_t><<<1, 256, 0, c->stream>>>(make_params<uint32_t>(c, sh));
+            nl++;
+        }
+    }
+    c->desc_clean = true;
+    void* args[] = {&p};
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_star<true>, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    for (int sh = 0; sh < L.nshards; sh++)
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_results + sh, c->ws + L.sh_result[sh], sizeof(ResultDev),
+                                    cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = nl;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->star = true;
+    c->sharded = false;
+    c->xr_run = true;
+    c->d2h_bytes = sizeof(ResultDev) * L.nshards;
+    return MPDP_OK;
+}
+
 template <int CLS>
 static mpdp_status run_sharded(mpdp_ctx* c) {
     if (c->wide || c->lay.memo_kind != MEMO_DENSE)
@@ -1164,7 +1260,8 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     // whole-query kernel's colex ranks
     const bool star = CLS == CLS_TREE && c->star_hub >= 0 && n >= 3 &&
                       !(c->flags & (MPDP_FLAG_NO_STAR | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS));
-    const void* kern = star ? (const void*)k_dp_star : level_loop_kernel<CLS>();
+    if (star && (c->flags & MPDP_FLAG_FUSED_EXCHANGE) && !c->nccl_self) return run_star_xr(c);
+    const void* kern = star ? (const void*)k_dp_star<false> : level_loop_kernel<CLS>();
     const size_t smem = star ? star_smem_bytes() : level_loop_smem<CLS>(n);
     int occ_star = 0;
     int& occ = star ? occ_star : c->fused_occ[CLS];
@@ -1279,8 +1376,14 @@ static mpdp_status run_query(mpdp_ctx* c) {
     c->small = false;
     c->tree1 = false;
     c->star = false;
+    c->xr_run = false;
     if constexpr (MEMO == MEMO_DENSE && sizeof(M) == 4) {
-        if (c->multi) return run_sharded<CLS>(c);
+        if (c->multi) {
+            c->desc_clean = was_clean;     // (the fused exchange keeps the dataflow state clean)
+            const mpdp_status st = run_sharded<CLS>(c);
+            if (!c->xr_run) c->desc_clean = false;
+            return st;
+        }
     }
     if (c->multi) return fail(c, MPDP_ERR_CAPACITY, "multi-GPU sharding needs n <= 32 and the perfect-hash memo");
     c->fused = false;
@@ -1602,6 +1705,54 @@ mpdp_status mpdp_ctx_create(const mpdp_ctx_config* cfg, mpdp_ctx** out) {
     return MPDP_OK;
 }
 
+mpdp_status mpdp_ctx_peer_record(mpdp_ctx* c, void* out) {
+    if (!c || !out) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "ctx/out is NULL");
+    if (c->world < 2 || c->simulate)
+        return fail(c, MPDP_ERR_INVALID_ARGUMENT, "peer records are for multi-GPU contexts (world > 1, not simulated)");
+    if (!c->own_ws) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "peer records need a library-allocated workspace");
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->ws));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    memcpy(out, &h, 64);
+    const unsigned long long sz = c->ws_bytes;
+    memcpy(static_cast<unsigned char*>(out) + 64, &sz, 8);
+    return MPDP_OK;
+}
+
+mpdp_status mpdp_ctx_open_peers(mpdp_ctx* c, const void* records) {
+    if (!c || !records) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "ctx/records is NULL");
+    if (c->world < 2 || c->simulate || c->world > kMaxXr)
+        return fail(c, MPDP_ERR_INVALID_ARGUMENT, "peers: multi-GPU contexts of 2..8 ranks only");
+    if (c->peers_open) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "peers already open");
+    const unsigned char* rec = static_cast<const unsigned char*>(records);
+    for (int s = 0; s < c->world; s++) {
+        unsigned long long sz;
+        memcpy(&sz, rec + s * MPDP_PEER_RECORD_BYTES + 64, 8);
+        if (sz != c->ws_bytes) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "peers: unequal workspace sizes");
+    }
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    for (int s = 0; s < c->world; s++) {
+        if (s == c->rank) {
+            c->peer_ws[s] = c->ws;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, rec + s * MPDP_PEER_RECORD_BYTES, 64);
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            for (int t = 0; t < s; t++)
+                if (t != c->rank && c->peer_ws[t]) cudaIpcCloseMemHandle(c->peer_ws[t]);
+            for (int t = 0; t < kMaxXr; t++) c->peer_ws[t] = nullptr;
+            return fail(c, MPDP_ERR_CUDA, "cudaIpcOpenMemHandle of rank " + std::to_string(s) + " failed");
+        }
+        c->peer_ws[s] = static_cast<unsigned char*>(ptr);
+    }
+    c->peers_open = true;
+    return MPDP_OK;
+}
+
 mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (!c) return MPDP_OK;
     if (c->stream) cudaStreamSynchronize(c->stream);
@@ -1610,6 +1761,9 @@ mpdp_status mpdp_ctx_destroy(mpdp_ctx* c) {
     if (c->h_rank_pinned) cudaFreeHost(c->h_rank_pinned);
     if (c->comm && c->nccl && c->nccl->CommDestroy) c->nccl->CommDestroy(c->comm);
     if (c->h_results) cudaFreeHost(c->h_results);
+    if (c->h_xr) cudaFreeHost(c->h_xr);
+    for (int s = 0; s < kMaxXr; s++)
+        if (c->peers_open && s != c->rank && c->peer_ws[s]) cudaIpcCloseMemHandle(c->peer_ws[s]);
     if (c->h_bq) cudaFreeHost(c->h_bq);
     if (c->h_br) cudaFreeHost(c->h_br);
     if (c->d_bq) cudaFree(c->d_bq);
@@ -1728,6 +1882,18 @@ mpdp_status mpdp_fetch(mpdp_ctx* c, mpdp_result* out) {
         return fail(c, MPDP_ERR_INVALID_ARGUMENT, "result capacity < 2n-1");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     CUDA_TRY(c, cudaGetLastError());
+    if (c->xr_run && c->simulate) {       // fused exchange: every replica holds the totals and the plan
+        ResultDev* r0 = c->h_results;
+        for (int sh = 1; sh < c->lay.nshards; sh++) {
+            const ResultDev* rs = c->h_results + sh;
+            r0->error |= rs->error;
+            if (!r0->error && (rs->n_nodes != r0->n_nodes || rs->csg != r0->csg || rs->pairs != r0->pairs ||
+                               rs->ccp != r0->ccp ||
+                               memcmp(rs->nodes, r0->nodes, sizeof(mpdp_plan_node) * r0->n_nodes) != 0 ||
+                               memcmp(&rs->cost, &r0->cost, sizeof(double)) != 0))
+                return fail(c, MPDP_ERR_INTERNAL, "fused-exchange replicas extracted different plans or counters");
+        }
+    }
     if (c->sharded && c->simulate) {      // sum the shards' counters; all shards must agree on the plan
         ResultDev* r0 = c->h_results;
         for (int sh = 1; sh < c->lay.nshards; sh++) {

@@ -55,14 +55,15 @@ __device__ __forceinline__ unsigned long long star_slot(const Params<uint32_t>& 
 // lane-consecutive groups, so a warp's probes of the shared high elements
 // coalesce and the CTA's warps share L1 lines.  Counts the join pairs this
 // thread evaluated and the sets it wrote.
-template <int G>
+template <int G, bool XR>
 __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
                                            const uint2* binp, int k, unsigned int lo, unsigned int hi,
-                                           unsigned int RUN, unsigned long long& npairs, unsigned long long& nsets) {
+                                           unsigned int RUN, unsigned long long& npairs, unsigned long long& nsets,
+                                           const DfRank& x) {
     const int hub = p.star_hub, nl = p.n - 1, kl = k - 1;   // kl leaves per set
     const bool leaf_costs = q.pad != 0;
-    const double* lvl = p.memo.dcost + p.star_off[k - 1];
-    const double* lcard = p.memo.dcard + p.star_off[k - 1];
+    const double* lvl = (XR ? x.dcost : p.memo.dcost) + p.star_off[k - 1];   // this rank's replica
+    const double* lcard = (XR ? x.dcard : p.memo.dcard) + p.star_off[k - 1];
     const unsigned long long out = p.star_off[k];
     constexpr unsigned int NG = kDfCompute / G;              // groups per CTA
     const unsigned int grp = threadIdx.x / G, sub = threadIdx.x & (G - 1);
@@ -155,9 +156,18 @@ __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<u
             if (G > 1) best = group_min(best, G);
             if (act && sub == 0) {
                 const unsigned long long idx = out + h;
-                p.memo.dcost[idx] = __longlong_as_double((long long)best.c);
-                __stcs(p.memo.dleft + idx, (unsigned int)best.l);
-                p.memo.dcard[idx] = cS;
+                // the cost into every replica (fused exchange: peer stores;
+                // one rank: the local array); left and card stay local
+                const double bcost = __longlong_as_double((long long)best.c);
+                if constexpr (XR) {
+                    for (int s = 0; s < x.W; s++) x.xr->cost[s][idx] = bcost;
+                    __stcs(x.dleft + idx, (unsigned int)best.l);
+                    x.dcard[idx] = cS;
+                } else {
+                    p.memo.dcost[idx] = bcost;
+                    __stcs(p.memo.dleft + idx, (unsigned int)best.l);
+                    p.memo.dcard[idx] = cS;
+                }
                 nsets++;
             }
         }
@@ -165,16 +175,18 @@ __device__ __forceinline__ void star_chunk(const Params<uint32_t>& p, const SQ<u
 }
 
 __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
-                                          int hub);
+                                          int hub, const DfRank& x);
 __device__ void star_emit_chain(const Params<uint32_t>& p, const SQ<uint32_t>& q, const uint32_t* c_set,
-                                const uint32_t* c_left, const double* c_cost, const double* c_card, int len);
+                                const uint32_t* c_left, const double* c_cost, const double* c_card, int len,
+                                const DfRank& x);
 
 // Sharded extraction (p.shard_local): the ranks exchanged only the memo costs,
 // so every rank re-derives the chain's splits from its complete cost replica:
 // at S the warp evaluates the pairs ({v}, S \ {v}) exactly as the level did
 // (same C_out order of additions, reading R7's key on the real masks) and
 // takes their minimum; card(S) by reading R5's fold.  Lane 0 of warp 0.
-__device__ __noinline__ void star_extract_sharded(const Params<uint32_t>& p, const SQ<uint32_t>& q, int hub) {
+__device__ __noinline__ void star_extract_sharded(const Params<uint32_t>& p, const SQ<uint32_t>& q, int hub,
+                                                  const DfRank& x) {
     const unsigned int lane = threadIdx.x & 31;
     __shared__ uint32_t x_set[32], x_left[32];
     __shared__ double x_cost[32], x_card[32];
@@ -204,7 +216,7 @@ __device__ __noinline__ void star_extract_sharded(const Params<uint32_t>& p, con
                     for (int t = 0; t < i; t++) b = b * (unsigned long long)(e - t) / (unsigned long long)(t + 1);
                     r += e >= i ? (unsigned int)b : 0u;
                 }
-                const double dv = __ldcg(p.memo.dcost + p.star_off[kl] + r);
+                const double dv = __ldcg(x.dcost + p.star_off[kl] + r);
                 const double a = leaf_costs ? __dadd_rn(q.leaf[v], dv) : dv;
                 c = __dadd_rn(a, cS);
             }
@@ -225,15 +237,17 @@ __device__ __noinline__ void star_extract_sharded(const Params<uint32_t>& p, con
         if ((S & (S - 1)) == 0) break;
     }
     __syncwarp();
-    if (lane == 0) star_emit_chain(p, q, x_set, x_left, x_cost, x_card, len);
+    if (lane == 0) star_emit_chain(p, q, x_set, x_left, x_cost, x_card, len, x);
 }
 
 // Star levels as dataflow chunks (dataflow.cuh): level k's sets are the
 // colex ranks of its (k-1)-leaf sets; a chunk needs level k-1 up to the
 // largest leaf of its last set.
+template <bool XR>
 struct StarSched {
     const Params<uint32_t>& p;
     const unsigned int* bin;
+    const DfRank& x;
     __device__ unsigned int total() const { return p.dfl[p.k_end + 1].base; }
     __device__ void locate(unsigned int t, DfSlot& d) const {
         int k = p.k_begin;
@@ -251,18 +265,25 @@ struct StarSched {
     // sets of level k1 (k1 - 1 leaves) whose largest leaf is j
     __device__ unsigned int need_count(int k1, int j) const { return bin[j * 33 + k1 - 2]; }
     __device__ void publish(const DfSlot& d) const {
-        df_publish_colex(p, bin, d.k, d.k - 1, d.lo, d.hi);
-        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex(p, bin, k, k - 1, p.share_lo[k], p.share_hi[k]);
+        DataflowDev* const ldf = XR ? x.df : p.df;
+        df_publish_colex<XR>(x, ldf, bin, d.k, d.k - 1, d.lo, d.hi);
+        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex<XR>(x, ldf, bin, k, k - 1, p.share_lo[k], p.share_hi[k]);
     }
 };
 
+template <bool XR>
 __global__ void __launch_bounds__(kDfThreads, kStarMinBlocks) k_dp_star(const __grid_constant__ Params<uint32_t> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
     unsigned int* bin = reinterpret_cast<unsigned int*>(smem_raw + sizeof(SQ<uint32_t>));   // 33 x 33
     __shared__ DfCounters sc;
     __shared__ DfShared sh;
+    __shared__ DfRank xr;                  // this CTA's rank and replica (fused exchange)
     if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[0] = globaltimer_ns();   // kernel start
+    if (threadIdx.x == 0) {
+        df_rank_init(xr, p);
+        if (XR) df_start_barrier(p, xr);
+    }
     load_query(q, p.q);
     constexpr int NB = MaxN<uint32_t>::value + 1;
     for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) {
@@ -282,7 +303,7 @@ __global__ void __launch_bounds__(kDfThreads, kStarMinBlocks) k_dp_star(const __
     __syncthreads();
     const int hub = p.star_hub;
     if (threadIdx.x >= kDfCompute) {
-        df_control(p, StarSched{p, bin}, sh);
+        df_control<XR>(p, StarSched<XR>{p, bin, xr}, sh, xr);
     } else {
         int kc = p.k_begin;
         unsigned long long npairs = 0, nsets = 0;      // this thread, level kc
@@ -301,14 +322,14 @@ __global__ void __launch_bounds__(kDfThreads, kStarMinBlocks) k_dp_star(const __
                 }
                 if (k > d.k) {
                     asm volatile("bar.sync 3, %0;" ::"r"(kDfCompute) : "memory");
-                    if (threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+                    if (threadIdx.x == 0) xr.result->t_level[k] = globaltimer_ns();
                 }
                 const DfLevel& L = p.dfl[k];
                 const unsigned int lo = k == d.k ? d.lo : p.share_lo[k], hi = k == d.k ? d.hi : p.share_hi[k];
                 switch (L.G) {
-                    case 1: star_chunk<1>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets); break;
-                    case 2: star_chunk<2>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets); break;
-                    default: star_chunk<4>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets); break;
+                    case 1: star_chunk<1, XR>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets, xr); break;
+                    case 2: star_chunk<2, XR>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets, xr); break;
+                    default: star_chunk<4, XR>(p, q, bin, binp, k, lo, hi, L.run, npairs, nsets, xr); break;
                 }
             }
             df_finish(sh, i);
@@ -320,25 +341,25 @@ __global__ void __launch_bounds__(kDfThreads, kStarMinBlocks) k_dp_star(const __
         // every pair of a set of level >= 3 probes one memo entry (S \ {v}, >= 2 relations)
         df_count(sc, kc, npairs, kc >= 3 ? npairs : 0ull, nsets);
     }
-    if (!df_exit(p, sc)) return;
-    if (p.do_extract && threadIdx.x < 32) star_extract(p, q, bin, hub);
-    df_reset(p);
+    if (!df_exit<XR>(p, sc, xr)) return;
+    if (p.do_extract && threadIdx.x < 32) star_extract(p, q, bin, hub, xr);
+    df_reset(p, xr);
 }
 
 // Counters and plan extraction, warp 0 of the last CTA out.
 __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<uint32_t>& q, const unsigned int* bin,
-                                          int hub) {
+                                          int hub, const DfRank& x) {
     const int n = p.n;
-    ResultDev* r = p.result;
+    ResultDev* r = x.result;
     const unsigned int lane = threadIdx.x;             // warp 0
     if (lane == 0) r->t_level[n + 1] = globaltimer_ns();
-    level_counters_warp(p, r);
-    if (ld_relaxed_u32(&p.df->error)) {
+    level_counters_warp(p, r, x.desc);
+    if (ld_relaxed_u32(&x.df->error)) {
         if (lane == 0) r->n_nodes = 0;
         return;
     }
     if (p.shard_local) {
-        star_extract_sharded(p, q, hub);
+        star_extract_sharded(p, q, hub, x);
         return;
     }
     // The optimal plan of a star set is a caterpillar: every join splits one
@@ -381,9 +402,9 @@ __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<ui
         uint32_t e_left = 0;
         double e_cost = 0.0, e_card = 0.0;
         if (load) {
-            e_left = __ldcg(p.memo.dleft + idx);
-            e_cost = __ldcg(p.memo.dcost + idx);
-            e_card = __ldcg(p.memo.dcard + idx);
+            e_left = __ldcg(x.dleft + idx);
+            e_cost = __ldcg(x.dcost + idx);
+            e_card = __ldcg(x.dcard + idx);
         }
         const uint32_t left = __shfl_sync(0xffffffffu, e_left, 31);
         const double cS = __shfl_sync(0xffffffffu, e_cost, 31), kS = __shfl_sync(0xffffffffu, e_card, 31);
@@ -414,14 +435,15 @@ __device__ __noinline__ void star_extract(const Params<uint32_t>& p, const SQ<ui
         if ((S & (S - 1)) == 0) break;
     }
     __syncwarp();
-    if (lane == 0) star_emit_chain(p, q, c_set, c_left, c_cost, c_card, len);
+    if (lane == 0) star_emit_chain(p, q, c_set, c_left, c_cost, c_card, len, x);
 }
 
 
 // Post-order plan nodes of a recorded caterpillar chain (one thread).
 __device__ void star_emit_chain(const Params<uint32_t>& p, const SQ<uint32_t>& q, const uint32_t* c_set,
-                                const uint32_t* c_left, const double* c_cost, const double* c_card, int len) {
-    ResultDev* r = p.result;
+                                const uint32_t* c_left, const double* c_cost, const double* c_card, int len,
+                                const DfRank& x) {
+    ResultDev* r = x.result;
     const int n = p.n;
     // post-order (left subtree, right subtree, node): with prefix_i = [v_i] when
     // the leaf is the left child and suffix_i = [v_i if it is the right child,
@@ -475,7 +497,7 @@ __device__ void star_emit_chain(const Params<uint32_t>& p, const SQ<uint32_t>& q
         inner = nn++;
     }
     r->n_nodes = (unsigned int)nn;
-    atomicMax(&p.df->t_done[n + 1], globaltimer_ns());     // extraction end
+    atomicMax(&x.df->t_done[n + 1], globaltimer_ns());     // extraction end
     r->cost = r->nodes[nn - 1].cost;
 }
 

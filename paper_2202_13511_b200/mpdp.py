@@ -71,13 +71,16 @@ FLAG_NO_SMALL = 1024
 FLAG_NO_CCC = 2048
 FLAG_NO_STAR = 4096
 FLAG_NCCL_SELF = 8192
+FLAG_FUSED_EXCHANGE = 16384
+PEER_RECORD_BYTES = 72
 
 
 EXPORTS = ["mpdp_ctx_create", "mpdp_ctx_destroy", "mpdp_optimize", "mpdp_optimize_batch", "mpdp_stage",
            "mpdp_run", "mpdp_fetch", "mpdp_last_error", "mpdp_status_string", "mpdp_abi_version",
            "mpdp_nccl_get_unique_id", "mpdp_share", "mpdp_debug_trace", "mpdp_subproblem_count",
            "mpdp_subproblem_get", "mpdp_heuristic_optimize", "mpdp_debug_level_span",
-           "mpdp_debug_df_stats", "mpdp_heuristic_optimize_t", "mpdp_optimize_uniondp"]
+           "mpdp_debug_df_stats", "mpdp_heuristic_optimize_t", "mpdp_optimize_uniondp",
+           "mpdp_ctx_peer_record", "mpdp_ctx_open_peers"]
 
 _lib = None
 
@@ -110,8 +113,12 @@ def load_library(path: str = LIB_PATH):
         "mpdp_debug_df_stats": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
         "mpdp_optimize_uniondp": (C.c_int, [P, C.POINTER(mpdp_query_graph), C.c_uint32, C.c_uint32,
                                             C.POINTER(mpdp_result)]),
+        "mpdp_ctx_peer_record": (C.c_int, [P, P]),
+        "mpdp_ctx_open_peers": (C.c_int, [P, P]),
     }
     for name, (res, args) in sig.items():
+        if not hasattr(L, name):           # an older build (A/B timing via MPDP_LIBRARY)
+            continue
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args
@@ -221,14 +228,18 @@ class Context:
         self._ws = None
         self.stream = None
         ws_ptr, stream_ptr = None, stream
+        # the fused peer exchange across GPUs maps the workspace of every rank
+        # through CUDA IPC, which needs a library-allocated workspace
+        peers = world > 1 and (flags & FLAG_FUSED_EXCHANGE) and not (flags & FLAG_SIMULATE_WORLD)
         if use_torch:
             import torch
             if not torch.cuda.is_available():
                 raise MPDPError(ERR_CUDA, "no CUDA device (this library has no CPU path)")
             torch.cuda.set_device(device)
-            self._ws = torch.empty(workspace_bytes, dtype=torch.uint8, device=f"cuda:{device}")
-            torch.cuda.synchronize(device)
-            ws_ptr = self._ws.data_ptr()
+            if not peers:
+                self._ws = torch.empty(workspace_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+                torch.cuda.synchronize(device)
+                ws_ptr = self._ws.data_ptr()
             if stream_ptr is None:
                 # a dedicated torch stream (the legacy default stream's handle is 0,
                 # which the C ABI reads as "create your own")
@@ -244,6 +255,25 @@ class Context:
             raise MPDPError(st, L.mpdp_last_error(None).decode())
         self.h = h
         self.L = L
+        if peers:
+            self.connect_peers()
+
+    def peer_record(self) -> bytes:
+        """This rank's MPDP_PEER_RECORD_BYTES record (IPC handle + workspace size)."""
+        buf = (C.c_char * PEER_RECORD_BYTES)()
+        self._check(self.L.mpdp_ctx_peer_record(self.h, C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def open_peers(self, records: List[bytes]):
+        """Map the other ranks' workspaces (records in rank order)."""
+        blob = b"".join(records)
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        self._check(self.L.mpdp_ctx_open_peers(self.h, C.cast(buf, C.c_void_p)))
+
+    def connect_peers(self, group=None):
+        """Exchange the peer records over torch.distributed (host plumbing) and
+        open the peers."""
+        self.open_peers(gather_peer_records(self.peer_record(), group))
 
     def _check(self, st):
         if st != OK:
@@ -304,6 +334,18 @@ class Context:
 
     def __exit__(self, *a):
         self.close()
+
+
+def gather_peer_records(record: bytes, group=None) -> List[bytes]:
+    """All ranks' peer records in rank order (torch.distributed object
+    allgather: any backend, e.g. gloo on the host)."""
+    import torch.distributed as dist
+    out: List[Optional[bytes]] = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(record), group=group)
+    for r in out:
+        if not isinstance(r, (bytes, bytearray)) or len(r) != PEER_RECORD_BYTES:
+            raise MPDPError(ERR_INVALID_ARGUMENT, "malformed peer record")
+    return [bytes(r) for r in out]
 
 
 def mpdp_nccl_get_unique_id() -> bytes:

@@ -112,3 +112,48 @@ def test_sharded_host_logic_gloo(n, world, shard_min):
                 assert a[1] == b[0]                         # contiguous, disjoint
         else:
             assert all(lo == 0 and hi == C for lo, hi, _ in parts)   # redundant small level
+
+
+def _peer_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2202_13511_b200 import mpdp
+        # a stand-in record (the real one holds this rank's CUDA IPC handle and
+        # workspace size, mpdp_ctx_peer_record): 64 handle bytes + the size
+        rec = bytes([rank + 1] * 64) + (1 << 30).to_bytes(8, "little")
+        recs = mpdp.gather_peer_records(rec)
+        bad = None
+        try:
+            mpdp.gather_peer_records(b"short")
+        except mpdp.MPDPError as e:
+            bad = e.status
+        q.put((rank, recs, bad))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_peer_records_gloo(world):
+    """Host logic of the fused peer exchange (MPDP_FLAG_FUSED_EXCHANGE across
+    GPUs): every rank gathers every rank's peer record, in rank order, before
+    mpdp_ctx_open_peers maps the peers' workspaces; malformed records are
+    rejected on every rank."""
+    from paper_2202_13511_b200 import mpdp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    want = [bytes([r + 1] * 64) + (1 << 30).to_bytes(8, "little") for r in range(world)]
+    for rank, recs, bad in res:
+        assert recs == want
+        assert all(len(r) == mpdp.PEER_RECORD_BYTES for r in recs)
+        assert bad == mpdp.ERR_INVALID_ARGUMENT
