@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config sub-results")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1, star workloads: fused peer exchange inside k_dp_star (default) "
+                         "or per-level ncclAllGather")
     return ap.parse_args()
 
 
@@ -294,8 +297,12 @@ def run_ours(args):
         if rank == 0:
             uid.copy_(torch.tensor(list(mpdp.mpdp_nccl_get_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
+        # star queries: the fused peer exchange (every chunk's costs stored into
+        # every rank's replica over NVLink); --exchange nccl keeps
+        # the per-level ncclAllGather path
+        xflags = mpdp.FLAG_FUSED_EXCHANGE if args.exchange == "fused" else 0
         ctx = mpdp.Context(device=local, workspace_bytes=ws, rank=rank, world=world,
-                           nccl_unique_id=bytes(uid.cpu().tolist()))
+                           nccl_unique_id=bytes(uid.cpu().tolist()), flags=xflags)
     else:
         ctx = mpdp.Context(device=local, workspace_bytes=ws)      # production path: fused kernel
     stream = ctx.stream                       # the stream every library kernel runs on
@@ -431,7 +438,10 @@ def run_ours(args):
                        "pairs_per_query": pairs_total / args.steps,
                        "l2": "flushed between steps (256 MiB write)",
                        "pairs_convention": "unordered join pairs (reading R3; SPEC's ordered count is 2x)",
-                       "parallelism": f"level-sharded x{world} (NCCL allgather per level)" if world > 1 else "single-gpu",
+                       "parallelism": ("single-gpu" if world == 1 else
+                                       f"x{world}: fused peer exchange in k_dp_star" if args.exchange == "fused"
+                                       and args.workload.startswith("star") else
+                                       f"level-sharded x{world} (NCCL allgather per level)"),
                        "opt_time_ms_median": statistics.median(step_ms)},
             "clocks": clk_now, "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
