@@ -202,7 +202,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
-SUB_CONFIGS = ["star-10", "snowflake-20", "clique-18", "chain-20", "cycle-20"]
+SUB_CONFIGS = ["star-10", "snowflake-20", "clique-18", "chain-20", "cycle-20", "random-20"]
 
 
 def l2_copy_gbs(torch, dev, mb=24, reps=50):
