@@ -425,8 +425,8 @@ __device__ __forceinline__ void clique_write(const MemoPtrs& P, uint32_t S, cons
 constexpr double kCliqueSetCost = 64.0;
 __host__ __device__ inline unsigned int clique_group(unsigned long long w, unsigned long long C, unsigned long long T,
                                                      unsigned long long split_w = 8192,
-                                                     double set_cost = kCliqueSetCost) {
-    if (w + 1 > split_w && 32ull * C < T) return 0;
+                                                     double set_cost = kCliqueSetCost, double split_fac = 1.0) {
+    if (w + 1 > split_w && 32.0 * (double)C < (double)T * split_fac) return 0;
     unsigned int best_g = 1;
     double best = 1e300;
     for (unsigned int G = 1; G <= 32 && G <= w + 1; G <<= 1) {
@@ -935,7 +935,7 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
         p.memo.dcard[1u << gtid] = q.card[gtid];
     }
     // whole sets per group of G lanes (clique_group), or pair chunks per warp
-    const unsigned int G = clique_group(w, C, nthreads, p.clique_split_w, p.clique_set_cost);
+    const unsigned int G = clique_group(w, C, nthreads, p.clique_split_w, p.clique_set_cost, p.clique_split_fac);
     (void)nccp;                            // every evaluated pair is a ccp (Lemma 8): counted as pairs
     if (G) {
         switch (G) {

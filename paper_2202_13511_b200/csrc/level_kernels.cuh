@@ -162,11 +162,16 @@ template <typename M> struct Params {
     // general graphs: sets with more join-pair candidates than this go to the
     // warp-parallel heavy phase (CCC) instead of one thread (light)
     unsigned int light_max;
+    // heavy phase: sets of at most this many pairs are evaluated whole by the
+    // warp whose claim holds their first pair (no cross-warp merge); larger
+    // sets are cut at the claim boundaries and merged
+    unsigned long long heavy_whole;
     // general graphs on the bitmask memo: the cost array was filled with
     // kMemoAbsent at staging, so connectivity checks may probe it (reading R20)
     int memo_conn;
     unsigned long long clique_split_w;     // k_dp_clique: split levels whose sets exceed this many pairs + 1
     double clique_set_cost;                // k_dp_clique: per-set overhead of the group cost model, in pairs
+    double clique_split_fac;               // k_dp_clique: split levels of fewer than fac x (warps) sets
     unsigned long long clique_csize_min;   // k_dp_clique: smallest warp chunk of the split path, in pairs
 };
 
@@ -540,6 +545,56 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
     }
 }
 
+// The candidates j, j + step, j + 2 step, ... < b of one block of S with memo
+// connectivity (reading R20): lb = lo | deposit(j, R) advanced by a masked add
+// of D = deposit(step, R); S_left = lb, or with HANG lb plus the hanging parts
+// of its cut vertices C (eval_blocks_hang).  Four pairs (eight probes) in
+// flight per lane; a pair competes iff both probes found their set (the CCP
+// test of the block); the min is kept in f64 / mask registers (costs >= 0, so
+// the f64 order is the bit order of the Key, reading R7).  Singletons read the
+// leaf cost.  Counts valid pairs and non-singleton probes.
+template <bool HANG, typename M>
+__device__ __forceinline__ void mc_span(const SQ<M>& q, M S, M lo, M R, M D, M sub, unsigned long long j,
+                                        unsigned long long b, unsigned int step, double cS, M C, const M* hang,
+                                        Key& best, unsigned long long& nvalid, unsigned long long& nprobe) {
+    const double* __restrict__ mc = q.mc;
+    double bc = __longlong_as_double((long long)best.c);
+    M bl = (M)best.l;
+    unsigned int nv = 0, np = 0;
+    for (; j < b; j += 4ull * step) {
+        M A[4];
+        double ca[4], cb[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            ok[u] = j + (unsigned long long)step * u < b;
+            M X = lo | sub;
+            if (HANG)
+                for (M T = X & C; T; T &= T - 1) X |= hang[ctz(T)];
+            A[u] = X;
+            const M Y = S ^ X;
+            const bool xs = (X & (X - 1)) != 0, ys = (Y & (Y - 1)) != 0;
+            ca[u] = ok[u] ? (xs ? mc[X] : q.leaf[ctz(X)]) : 0.0;
+            cb[u] = ok[u] ? (ys ? mc[Y] : q.leaf[ctz(Y)]) : 0.0;
+            np += ok[u] ? (unsigned int)xs + (unsigned int)ys : 0u;
+            sub = ((sub | ~R) + D) & R;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const bool valid = ok[u] && memo_present(ca[u]) && memo_present(cb[u]);
+            const double c = __dadd_rn(__dadd_rn(ca[u], cb[u]), cS);
+            const M Y = S ^ A[u], l = A[u] < Y ? A[u] : Y;
+            const bool better = valid && (c < bc || (c == bc && l < bl));
+            bc = better ? c : bc;
+            bl = better ? l : bl;
+            nv += valid;
+        }
+    }
+    nvalid += nv;
+    nprobe += np;
+    best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
+}
+
 // ------------------------------------------------------------ k_eval
 template <typename M, int CLS, typename Sink>
 __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long long j0, unsigned long long j1,
@@ -607,19 +662,12 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
         nb = find_blocks(q, S, blk);
     }
     if constexpr (Sink::kChk) if (nb == 1 && q.mc) {   // one block S: S_left = lb (grow(lb, lb) = lb);
-        const M lo = lowbit(S), R = S ^ lo;    // the sink's probes of lb and rb are the CCP test (R20)
-        M sub = deposit<M>(j0, R);
+        const M lo = lowbit(S), R = S ^ lo;    // the probes of lb and rb are the CCP test (R20)
         sink.flush();
-        sink.chk = true;
-        for (unsigned long long j = j0; j < j1; j++) {
-            const M lb = lo | sub;
-            sub = (sub - R) & R;
-            sink.add(lb, S ^ lb);
-        }
-        sink.flush();
-        sink.chk = false;
-        nccp += sink.nvalid;
-        sink.nvalid = 0;
+        unsigned long long nv = 0;
+        mc_span<false, M>(q, S, lo, R, lowbit(R), deposit<M>(j0, R), j0, j1, 1u, sink.cS, (M)0, nullptr, sink.best, nv,
+                          sink.nprobe);
+        nccp += nv;
         return;
     }
     if constexpr (Sink::kChk) if (q.mc) {  // reading R20: S_left = grow(lb, S \ rb) is connected
@@ -1049,18 +1097,15 @@ __device__ __forceinline__ void eval_blocks_hang(const SQ<M>& q, M S, unsigned l
         }
         __syncwarp();
         const M lo = lowbit(Bm), R = Bm ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
-        unsigned long long j = a0 + lane;
-        M sub = j < a1 ? deposit<M>(j, R) : 0;
-        for (; j < a1; j += 32) {
-            const M lb = lo | sub;
-            M A = lb;
-            for (M T = lb & C; T; T &= T - 1) A |= hang[ctz(T)];
-            sink.add(A, S ^ A);
-            sub = ((sub | ~R) + D) & R;
+        const unsigned long long j = a0 + lane;
+        if (j < a1) {
+            // deposit(a0 + lane) = deposit(a0) (+) deposit(lane) in R's domain
+            const M da = a0 ? deposit<M>(a0, R) : (M)0;
+            const M sub = ((da | ~R) + deposit<M>(lane, R)) & R;
+            mc_span<true, M>(q, S, lo, R, D, sub, j, a1, 32u, sink.cS, C, hang, sink.best, sink.nvalid, sink.nprobe);
         }
         base += wb;
     }
-    sink.flush();
     __syncwarp();
 }
 
@@ -1099,7 +1144,10 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
             }
             const unsigned long long w = W1 - W0;
             if (W0 >= c1) break;
-            const unsigned long long a = (c0 > W0 ? c0 - W0 : 0), b = (c1 - W0 < w ? c1 - W0 : w);
+            const bool whole = w <= p.heavy_whole;
+            if (whole && W0 < c0) continue;    // owned by the claim holding its first pair
+            const unsigned long long a = whole ? 0 : (c0 > W0 ? c0 - W0 : 0),
+                                     b = whole ? w : (c1 - W0 < w ? c1 - W0 : w);
             unsigned long long wk;
             int kind, hnb = 0;
             if (CLS == CLS_GENERAL && q.mc) {
@@ -1130,15 +1178,13 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                 // the probes of lb and rb are the CCP test (reading R20); lanes
                 // interleaved as for complete sets
                 const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
-                unsigned long long j = a + lane;
-                M sub = j < b ? deposit<M>(j, R) : 0;
-                sink.chk = true;
-                for (; j < b; j += 32) {
-                    const M A = lo | sub;
-                    sink.add(A, S ^ A);
-                    sub = ((sub | ~R) + D) & R;
+                const unsigned long long j = a + lane;
+                if (j < b) {
+                    const M da = a ? deposit<M>(a, R) : (M)0;      // deposit(a + lane), as a masked add
+                    const M sub = ((da | ~R) + deposit<M>(lane, R)) & R;
+                    mc_span<false, M>(q, S, lo, R, D, sub, j, b, 32u, sink.cS, (M)0, nullptr, sink.best, sink.nvalid,
+                                      sink.nprobe);
                 }
-                sink.flush();
                 nccp += sink.nvalid;
             } else if (CLS == CLS_GENERAL && q.mc && kind == KIND_BLOCKS) {
                 eval_blocks_hang<M>(q, S, a, b, sink, s_ccc[threadIdx.x >> 5], lblk, hnb);

@@ -608,8 +608,10 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.no_ccc = (c->flags & MPDP_FLAG_NO_CCC) ? 1 : 0;
     p.light_max = light_max_general();
     p.memo_conn = c->memo_conn ? 1 : 0;
+    p.heavy_whole = getenv("MPDP_DEBUG_HEAVY_WHOLE") ? strtoull(getenv("MPDP_DEBUG_HEAVY_WHOLE"), nullptr, 10) : 2048;
     p.clique_split_w = getenv("MPDP_DEBUG_CLIQUE_SPLIT") ? strtoull(getenv("MPDP_DEBUG_CLIQUE_SPLIT"), nullptr, 10) : 4096;
     p.clique_set_cost = getenv("MPDP_DEBUG_CLIQUE_SETCOST") ? atof(getenv("MPDP_DEBUG_CLIQUE_SETCOST")) : kCliqueSetCost;
+    p.clique_split_fac = getenv("MPDP_DEBUG_CLIQUE_SPLITFAC") ? atof(getenv("MPDP_DEBUG_CLIQUE_SPLITFAC")) : 1.0;
     p.clique_csize_min = getenv("MPDP_DEBUG_CLIQUE_CSIZE") ? strtoull(getenv("MPDP_DEBUG_CLIQUE_CSIZE"), nullptr, 10) : 512;
     p.star_hub = c->star_hub;
     {   // star levels: C(n-1, k-1) entries + `world` padding (equal rank segments, as dense_off)
