@@ -1068,20 +1068,53 @@ __device__ __forceinline__ void eval_blocks_ccc(const SQ<M>& q, M S, int kind, u
 // (P:553-560).  hang[] is the warp's scratch (>= MaxN entries).
 // The blocks come from the heavy list's cache (gblk, nb <= kHeavyBlk) or are
 // found again.
+//
+// A set evaluated whole (whole: [a, b) = [0, w)) first takes the candidates of
+// all its small blocks (at most kSmallBlockPairs each: bridges, triangles)
+// together, one lane per candidate with S_left = grow(lb, S \ rb) --
+// otherwise every bridge would cost the warp a memory round trip for one pair.
+constexpr unsigned long long kSmallBlockPairs = 7;
 template <typename M, typename Sink>
 __device__ __forceinline__ void eval_blocks_hang(const SQ<M>& q, M S, unsigned long long a, unsigned long long b,
-                                                 Sink& sink, M* hang, M lblk, int nb) {
+                                                 bool whole, Sink& sink, M* hang, M lblk, int nb) {
     const unsigned int lane = threadIdx.x & 31;
     M blk[MaxN<M>::value];
     const bool cached = nb <= kHeavyBlk;   // lane i holds cached block i & 7
     if (!cached) nb = find_blocks(q, S, blk);
     sink.chk = true;
+    if (whole) {
+        unsigned int nsmall = 0;           // candidates of the small blocks
+        for (int bi = 0; bi < nb; bi++) {
+            const M Bm = cached ? __shfl_sync(0xffffffffu, lblk, bi) : blk[bi];
+            const unsigned long long wb = (1ull << (popc(Bm) - 1)) - 1;
+            if (wb <= kSmallBlockPairs) nsmall += (unsigned int)wb;
+        }
+        for (unsigned int r = 0; r < nsmall; r += 32) {
+            const unsigned int idx = r + lane;
+            M Bm = 0;
+            unsigned int j = idx;
+            for (int bi = 0; bi < nb; bi++) {      // (uniform trip count: shuffles inside)
+                const M X = cached ? __shfl_sync(0xffffffffu, lblk, bi) : blk[bi];
+                const unsigned int wb = (1u << (popc(X) - 1)) - 1u;
+                if (wb <= kSmallBlockPairs && !Bm) {
+                    if (j < wb) Bm = X;
+                    else j -= wb;
+                }
+            }
+            if (idx < nsmall) {
+                const M lo = lowbit(Bm), lb = lo | deposit<M>(j, Bm ^ lo), rb = Bm ^ lb;
+                const M A = grow(q, lb, S & ~rb);
+                mc_span<false, M>(q, S, A, (M)0, (M)0, (M)0, 0, 1, 1u, sink.cS, (M)0, nullptr, sink.best,
+                                  sink.nvalid, sink.nprobe);
+            }
+        }
+    }
     unsigned long long base = 0;
     for (int bi = 0; bi < nb && base < b; bi++) {
         const M Bm = cached ? __shfl_sync(0xffffffffu, lblk, bi) : blk[bi];
         const int bsz = popc(Bm);
         const unsigned long long wb = (1ull << (bsz - 1)) - 1;
-        if (base + wb <= a) {
+        if (base + wb <= a || (whole && wb <= kSmallBlockPairs)) {
             base += wb;
             continue;
         }
@@ -1187,7 +1220,7 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                 }
                 nccp += sink.nvalid;
             } else if (CLS == CLS_GENERAL && q.mc && kind == KIND_BLOCKS) {
-                eval_blocks_hang<M>(q, S, a, b, sink, s_ccc[threadIdx.x >> 5], lblk, hnb);
+                eval_blocks_hang<M>(q, S, a, b, a == 0 && b == w, sink, s_ccc[threadIdx.x >> 5], lblk, hnb);
                 nccp += sink.nvalid;
             } else if (CLS == CLS_GENERAL && kind >= KIND_BLOCKS && !p.no_ccc) {
                 eval_blocks_ccc<M>(q, S, kind, a, b, sink, nccp, s_ccc[threadIdx.x >> 5]);
