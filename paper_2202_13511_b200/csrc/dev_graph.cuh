@@ -352,7 +352,7 @@ __device__ __forceinline__ bool biconnected(const SQ<M>& q, M S) {
 constexpr int kHeavyBlk = 8;
 template <typename M, int CLS>
 __device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned long long& w, M* blk_out = nullptr,
-                                        int* nb_out = nullptr) {
+                                        int* nb_out = nullptr, M* cut_out = nullptr) {
     if (CLS == CLS_TREE) {
         w = (unsigned long long)(k - 1);
         return KIND_TREE;
@@ -378,6 +378,7 @@ __device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned lon
     int nb;
     if (q.mc) {                            // reading R21: cut vertices by probes, blocks from them
         const M cut = cut_vertices_memo(q, S);
+        if (cut_out) *cut_out = cut;
         if (!cut) {                        // one (non-complete) block: S
             w = (1ull << (k - 1)) - 1;
             return KIND_ONEBLOCK;
@@ -403,13 +404,15 @@ __device__ __forceinline__ int set_kind(const SQ<M>& q, M S, int k, unsigned lon
 // Pair count of a set whose kind is already known (set_kind's w without its
 // tests): closed forms, or Find-Blocks for KIND_BLOCKS (blocks cached as in
 // set_kind).
+// (cut: the cut vertices of a KIND_BLOCKS set when set_kind found them by
+// probes, reading R21; 0 = not known)
 template <typename M, int CLS>
 __device__ __forceinline__ unsigned long long kind_pairs(const SQ<M>& q, M S, int k, int kind, M* blk_out = nullptr,
-                                                         int* nb_out = nullptr) {
+                                                         int* nb_out = nullptr, M cut = 0) {
     if (kind == KIND_TREE) return (unsigned long long)(k - 1);
     if (kind != KIND_BLOCKS || q.dpsub) return (1ull << (k - 1)) - 1;
     M blk[MaxN<M>::value];
-    const int nb = find_blocks(q, S, blk);
+    const int nb = (q.mc && cut) ? blocks_from_cut(q, S, cut, blk) : find_blocks(q, S, blk);
     unsigned long long s = 0;
     for (int i = 0; i < nb; i++) s += (1ull << (popc(blk[i]) - 1)) - 1;
     if (blk_out) {

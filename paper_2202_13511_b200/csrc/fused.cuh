@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             const unsigned int r0 = lo + (unsigned int)t0 + threadIdx.x * rpt;
             M S0 = 0;
             unsigned int lflag = 0, hflag = 0, kinds = 0;   // kinds: 2 bits per rank (set_kind once)
+            M cuts[kFusedRanksPerThread];      // general graphs: cut vertices of each rank's set (R21)
             Tri mine = {0, 0, 0};
             if (r0 < r_hi) {
                 S0 = unrank_colex32(bin, n, k, r0);
@@ -652,7 +653,8 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                     if (i < (int)rpt && r0 + i < r_hi) {
                         if (connected_cls<M, CLS>(q, S, k)) {
                             unsigned long long w;
-                            const int kind = set_kind<M, CLS>(q, S, k, w);
+                            cuts[i] = 0;
+                            const int kind = set_kind<M, CLS>(q, S, k, w, nullptr, nullptr, &cuts[i]);
                             kinds |= (unsigned int)kind << (2 * i);
                             // (general graphs: only sets without CCP checks,
                             // or with few candidates, are evaluated by one thread)
@@ -740,7 +742,7 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                             M blk[kHeavyBlk];
                             int nb = 0;
                             const int kind = (int)((kinds >> (2 * i)) & 3u);
-                            w = kind_pairs<M, CLS>(q, S, k, kind, blk, &nb);
+                            w = kind_pairs<M, CLS>(q, S, k, kind, blk, &nb, cuts[i]);
                             if (hi < p.heavy_cap) {
                                 p.hinfo[hi] = (unsigned int)kind | ((unsigned int)nb << 2);
                                 for (int b = 0; b < nb && b < kHeavyBlk; b++) p.hblk[hi * kHeavyBlk + b] = blk[b];
