@@ -516,3 +516,60 @@ def test_batch_invalidates_staged_query(ctx):
     ctx.mpdp_stage(big)
     ctx.mpdp_run()
     check(ctx.mpdp_fetch(), O.optimize(big), big)
+
+
+def _structured(name, n, edges, seed):
+    """A fixed topology with the recipe's numbers (cards log-uniform, factors)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    card = [float(x) for x in 10.0 ** rng.uniform(1.0, 6.0, size=n)]
+    edges = sorted({(min(a, b), max(a, b)) for a, b in edges})
+    sel = [float(x) for x in 10.0 ** rng.uniform(-1.0, 0.0, size=len(edges))]
+    return W.QueryGraph(n, card, edges, sel, name=name)
+
+
+def _sun(k, pend):
+    """A k-cycle whose every vertex carries `pend` pendant vertices: its large
+    connected sets have many blocks (the cycle plus one bridge per pendant)."""
+    edges = [(i, (i + 1) % k) for i in range(k)]
+    v = k
+    for i in range(k):
+        for _ in range(pend):
+            edges.append((i, v))
+            v += 1
+    return v, edges
+
+
+def _cut_triangle():
+    """A triangle of cut vertices (a block made only of cut vertices) whose
+    corners carry pendant paths and a chorded square."""
+    edges = [(0, 1), (1, 2), (0, 2),                  # the triangle
+             (0, 3), (3, 4), (1, 5), (5, 6), (2, 7),  # pendant paths
+             (7, 8), (8, 9), (9, 10), (10, 7), (7, 9)]   # a chorded square at vertex 7
+    return 11, edges
+
+
+@pytest.mark.parametrize("shape", ["sun6x2", "sun5x3", "sun8x1", "sun7x2", "cut_triangle", "barbell"])
+def test_block_structures_parity(ctx, shape):
+    """Readings R20/R21 on shapes the random graphs rarely produce: sets with
+    more blocks than the heavy list caches (kHeavyBlk = 8, the Find-Blocks
+    fallback), blocks made only of cut vertices (found from an edge), bridges
+    (small blocks evaluated lane-parallel) and hanging parts of several cut
+    vertices of one block."""
+    if shape.startswith("sun"):
+        k, p = (int(x) for x in shape[3:].split("x"))
+        n, edges = _sun(k, p)
+    elif shape == "cut_triangle":
+        n, edges = _cut_triangle()
+    else:                                          # two 5-cliques joined by a 3-path
+        edges = [(a, b) for a in range(5) for b in range(a + 1, 5)]
+        edges += [(a + 8, b + 8) for a in range(5) for b in range(a + 1, 5)]
+        edges += [(4, 5), (5, 6), (6, 7), (7, 8)]
+        n = 13
+    g = _structured(shape, n, edges, 11)
+    r = ctx.mpdp_optimize(g)
+    check(r, O.optimize(g), g)
+    from paper_2202_13511_b200 import mpdp
+    with mpdp.Context(device=0, workspace_bytes=1 << 30, flags=mpdp.FLAG_DPSUB_ENUM) as c:   # (ablation)
+        r2 = c.mpdp_optimize(g)
+        assert r2.cost == r.cost and r2.tree() == r.tree() and r2.ccp_pairs == r.ccp_pairs
