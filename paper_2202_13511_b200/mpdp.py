@@ -8,7 +8,9 @@ stream.
 """
 from __future__ import annotations
 
+import array
 import ctypes as C
+import itertools
 import os
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -143,28 +145,51 @@ class PlanNode:
     cost: float
 
 
-@dataclass
 class Result:
-    cost: float
-    nodes: List[PlanNode]
-    pairs_evaluated: int
-    ccp_pairs: int
-    csg_count: int
-    level_csg: List[int]
-    level_ccp: List[int]
-    level_pairs: List[int]
-    time_ms: float
-    gpu_launches: int
-    probes: int = 0
-    h2d_bytes: int = 0
-    d2h_bytes: int = 0
-    enum_ms: float = 0.0
-    eval_ms: float = 0.0
-    enum_launches: int = 0
-    eval_launches: int = 0
-    memo_kind: int = 0
-    level_ms: List[float] = field(default_factory=list)
-    inner_calls: int = 0
+    """One optimisation result (mpdp_result).  The plan nodes are converted
+    from the C array on first access (`nodes`): building 2n-1 Python objects
+    per call was most of the binding's per-query cost."""
+    _FIELDS = ("cost", "pairs_evaluated", "ccp_pairs", "csg_count", "level_csg", "level_ccp", "level_pairs",
+               "time_ms", "gpu_launches", "probes", "h2d_bytes", "d2h_bytes", "enum_ms", "eval_ms",
+               "enum_launches", "eval_launches", "memo_kind", "level_ms", "inner_calls")
+
+    def __init__(self, cost, nodes, pairs_evaluated, ccp_pairs, csg_count, level_csg, level_ccp, level_pairs,
+                 time_ms, gpu_launches, probes=0, h2d_bytes=0, d2h_bytes=0, enum_ms=0.0, eval_ms=0.0,
+                 enum_launches=0, eval_launches=0, memo_kind=0, level_ms=None, inner_calls=0):
+        self.cost, self.pairs_evaluated, self.ccp_pairs, self.csg_count = cost, pairs_evaluated, ccp_pairs, csg_count
+        self._lv = [level_csg, level_ccp, level_pairs]   # lists, or ctypes arrays converted lazily
+        self.time_ms, self.gpu_launches, self.probes = time_ms, gpu_launches, probes
+        self.h2d_bytes, self.d2h_bytes, self.enum_ms, self.eval_ms = h2d_bytes, d2h_bytes, enum_ms, eval_ms
+        self.enum_launches, self.eval_launches, self.memo_kind = enum_launches, eval_launches, memo_kind
+        self._lv.append(level_ms if level_ms is not None else [])
+        self.inner_calls = inner_calls
+        self._nodes = nodes                # a list, or (ctypes node array, count) converted lazily
+
+    @property
+    def nodes(self) -> List[PlanNode]:
+        if isinstance(self._nodes, tuple):
+            arr, cnt = self._nodes
+            self._nodes = [PlanNode(x.left, x.right, x.relation, x.set, x.cardinality, x.cost) for x in arr[:cnt]]
+        return self._nodes
+
+    @nodes.setter
+    def nodes(self, v):
+        self._nodes = v
+
+    def _level(self, i):
+        x = self._lv[i]
+        if x is not None and not isinstance(x, list):
+            x = self._lv[i] = list(x)
+        return x
+
+    level_csg = property(lambda self: self._level(0), lambda self, v: self._lv.__setitem__(0, v))
+    level_ccp = property(lambda self: self._level(1), lambda self, v: self._lv.__setitem__(1, v))
+    level_pairs = property(lambda self: self._level(2), lambda self, v: self._lv.__setitem__(2, v))
+    level_ms = property(lambda self: self._level(3), lambda self, v: self._lv.__setitem__(3, v))
+
+    def __repr__(self):
+        return "Result(" + ", ".join(f"{f}={getattr(self, f)!r}" for f in ("cost", "pairs_evaluated", "csg_count",
+                                                                          "memo_kind", "time_ms")) + ")"
 
     def tree(self):
         """Nested tuples: leaves are relation ids, internal nodes (left, right)."""
@@ -178,12 +203,19 @@ class GraphArgs:
     """Marshals a workload.QueryGraph-like object (n, card, edges, sel, leaf_cost)."""
 
     def __init__(self, g):
+        # array.array buffers (C-speed conversion of the Python lists), viewed
+        # as ctypes arrays without a copy
         n, m = g.n, len(g.edges)
-        self.card = (C.c_double * n)(*g.card)
-        self.edges = (C.c_uint32 * max(1, 2 * m))(*[x for e in g.edges for x in e])
-        self.sel = (C.c_double * max(1, m))(*g.sel)
+        self._a = [array.array("d", g.card), array.array("I", itertools.chain.from_iterable(g.edges) if m else (0, 0)),
+                   array.array("d", g.sel if m else (0.0,))]
+        self.card = (C.c_double * n).from_buffer(self._a[0])
+        self.edges = (C.c_uint32 * max(1, 2 * m)).from_buffer(self._a[1])
+        self.sel = (C.c_double * max(1, m)).from_buffer(self._a[2])
         lc = getattr(g, "leaf_cost", None)
-        self.leaf = (C.c_double * n)(*lc) if lc is not None else None
+        self.leaf = None
+        if lc is not None:
+            self._a.append(array.array("d", lc))
+            self.leaf = (C.c_double * n).from_buffer(self._a[3])
         self.s = mpdp_query_graph(n, self.card, m, self.edges, self.sel, self.leaf)
         self.n = n
 
@@ -208,12 +240,11 @@ class ResultBuf:
 
     def to_result(self) -> Result:
         r = self.s
-        nodes = [PlanNode(x.left, x.right, x.relation, x.set, x.cardinality, x.cost)
-                 for x in self.nodes[:r.n_nodes]]
+        nodes = (self.nodes, r.n_nodes)   # converted on first access (Result.nodes)
         return Result(r.cost, nodes, r.pairs_evaluated, r.ccp_pairs, r.csg_count,
-                      list(self.lc), list(self.lx), list(self.lp), r.time_ms, r.gpu_launches,
+                      self.lc, self.lx, self.lp, r.time_ms, r.gpu_launches,
                       r.probes, r.h2d_bytes, r.d2h_bytes, r.enum_ms, r.eval_ms,
-                      r.enum_launches, r.eval_launches, r.memo_kind, list(self.lt), r.inner_calls)
+                      r.enum_launches, r.eval_launches, r.memo_kind, self.lt, r.inner_calls)
 
 
 class Context:
