@@ -42,6 +42,7 @@ struct HNode {
     int nleaves = 1;             // leaves of the CURRENT tree (a temp table counts 1)
     int temp = -1;               // IDP2: this leaf is a temp table whose subplan is pool[temp]
     int parent = -1;
+    int minrel = -1;             // lowest base relation under this node (IDP2's last tie-break)
 };
 
 struct Query {
@@ -69,6 +70,7 @@ struct Driver {
     int leaf(int r) {
         HNode h;
         h.relation = r;
+        h.minrel = r;
         h.card = Q.card[r];
         h.cost = Q.leaf[r];
         pool.push_back(h);
@@ -138,6 +140,7 @@ struct Driver {
             h.left = map[nd.left];
             h.right = map[nd.right];
             h.nleaves = pool[h.left].nleaves + pool[h.right].nleaves;
+            h.minrel = std::min(pool[h.left].minrel, pool[h.right].minrel);
             pool.push_back(h);
             const int id = (int)pool.size() - 1;
             join_card_cost(id);
@@ -282,6 +285,7 @@ static int goo(Driver& D) {
         h.left = root[swap ? bb : ba];
         h.right = root[swap ? ba : bb];
         h.nleaves = D.pool[h.left].nleaves + D.pool[h.right].nleaves;
+        h.minrel = std::min(D.pool[h.left].minrel, D.pool[h.right].minrel);
         D.pool.push_back(h);
         const int id = (int)D.pool.size() - 1;
         D.join_card_cost(id);
@@ -341,9 +345,7 @@ static int idp2(Driver& D, int k) {
             HNode& h = D.pool[x];
             if (h.relation >= 0 || h.temp >= 0) {
                 h.nleaves = 1;
-                std::vector<int> r;
-                D.collect(h.temp >= 0 ? h.temp : x, r);
-                minrel[x] = *std::min_element(r.begin(), r.end());
+                minrel[x] = h.minrel;          // cached when the node / temp table was made
                 continue;
             }
             h.nleaves = D.pool[h.left].nleaves + D.pool[h.right].nleaves;
@@ -391,6 +393,7 @@ static int idp2(Driver& D, int k) {
         // replace the subtree `best` by a temp table leaf
         HNode t;
         t.temp = sub;
+        t.minrel = D.pool[sub].minrel;
         t.card = D.pool[sub].card;
         t.cost = D.pool[sub].cost;
         D.pool[best] = t;
