@@ -67,14 +67,37 @@ struct Driver {
 
     Driver(const Query& q, InnerSolver s, void* u) : Q(q), solve(s), user(u) {}
 
+    // relation set of every pool node as a bitset of W words (a leaf: its bit;
+    // a join: the OR of its children), and its relation count, so a join's
+    // cross edges are found from the smaller side alone (join_card_cost)
+    int W = 0;
+    std::vector<uint64_t> bits;
+    std::vector<int> nrel;
+    int add_node(const HNode& h) {
+        if (!W) W = (Q.n + 63) / 64;
+        pool.push_back(h);
+        const int id = (int)pool.size() - 1;
+        bits.resize((size_t)(id + 1) * W, 0);
+        nrel.resize(id + 1, 0);
+        uint64_t* b = &bits[(size_t)id * W];
+        if (h.relation >= 0) {
+            b[h.relation >> 6] |= 1ull << (h.relation & 63);
+            nrel[id] = 1;
+        } else {
+            const uint64_t* l = &bits[(size_t)h.left * W];
+            const uint64_t* r = &bits[(size_t)h.right * W];
+            for (int w = 0; w < W; w++) b[w] = l[w] | r[w];
+            nrel[id] = nrel[h.left] + nrel[h.right];
+        }
+        return id;
+    }
     int leaf(int r) {
         HNode h;
         h.relation = r;
         h.minrel = r;
         h.card = Q.card[r];
         h.cost = Q.leaf[r];
-        pool.push_back(h);
-        return (int)pool.size() - 1;
+        return add_node(h);
     }
 
     // A sub-problem over the composites `nodes` (pool roots covering disjoint
@@ -141,8 +164,7 @@ struct Driver {
             h.right = map[nd.right];
             h.nleaves = pool[h.left].nleaves + pool[h.right].nleaves;
             h.minrel = std::min(pool[h.left].minrel, pool[h.right].minrel);
-            pool.push_back(h);
-            const int id = (int)pool.size() - 1;
+            const int id = add_node(h);
             join_card_cost(id);
             map[i] = id;
         }
@@ -176,28 +198,20 @@ struct Driver {
         collect(pool[x].left, rels);
         collect(pool[x].right, rels);
     }
-    // scratch of join_card_cost: relation stamps instead of a fresh n-byte
-    // vector per join
-    std::vector<unsigned> stamp;
-    unsigned cur_stamp = 0;
-    std::vector<int> scratch_l, scratch_r;
+    // the edges between the two sides: the smaller side's relations are
+    // walked, the larger side is a bitset lookup
+    std::vector<int> scratch_s, cross;
     void join_card_cost(int id) {
         HNode& h = pool[id];
-        scratch_l.clear();
-        scratch_r.clear();
-        collect(h.left, scratch_l);
-        collect(h.right, scratch_r);
-        if (stamp.size() != (size_t)Q.n) stamp.assign(Q.n, 0);
-        if (++cur_stamp == 0) {                // wrapped: clear once
-            std::fill(stamp.begin(), stamp.end(), 0u);
-            cur_stamp = 1;
-        }
-        for (int r : scratch_r) stamp[r] = cur_stamp;
-        std::vector<int> cross;
-        for (int r : scratch_l)
+        const bool lsmall = nrel[h.left] <= nrel[h.right];
+        scratch_s.clear();
+        collect(lsmall ? h.left : h.right, scratch_s);
+        const uint64_t* big = &bits[(size_t)(lsmall ? h.right : h.left) * W];
+        cross.clear();
+        for (int r : scratch_s)
             for (auto [u, e] : Q.adj[r])
-                if (stamp[u] == cur_stamp) cross.push_back(e);
-        std::sort(cross.begin(), cross.end());
+                if ((big[u >> 6] >> (u & 63)) & 1ull) cross.push_back(e);
+        std::sort(cross.begin(), cross.end());   // the product in edge-id order (reading R17)
         double c = pool[h.left].card * pool[h.right].card;
         for (int e : cross) c = c * Q.sel[e];
         h.card = c;
@@ -286,8 +300,7 @@ static int goo(Driver& D) {
         h.right = root[swap ? ba : bb];
         h.nleaves = D.pool[h.left].nleaves + D.pool[h.right].nleaves;
         h.minrel = std::min(D.pool[h.left].minrel, D.pool[h.right].minrel);
-        D.pool.push_back(h);
-        const int id = (int)D.pool.size() - 1;
+        const int id = D.add_node(h);
         D.join_card_cost(id);
         // merge component bb into ba
         root[ba] = id;
