@@ -442,10 +442,29 @@ __host__ __device__ inline unsigned int clique_group(unsigned long long w, unsig
 // Group path, one chunk: sets [lo, hi) of clique level k on the CTA's compute
 // threads, G lanes per set, group-consecutive sets (the warp's groups work on
 // colex neighbours, whose probes share lines).
-template <int G>
+// (XR, the fused peer exchange: M is this rank's replica, and every set is
+// written into every replica, cost, card and left -- 20 B per set, 5 MB per
+// replica at clique-18 -- so card(S \ max) and the extraction stay local)
+template <bool XR>
+__device__ __forceinline__ void clique_write_x(const MemoPtrs& M, const DfRank* x, uint32_t S, const Key& best,
+                                               double cS) {
+    if (!XR) {
+        clique_write(M, S, best, cS);
+        return;
+    }
+    const double c = __longlong_as_double((long long)best.c);
+    for (int r = 0; r < x->W; r++) {
+        x->xr->cost[r][S] = c;
+        x->xr->left[r][S] = (unsigned int)best.l;
+        x->xr->card[r][S] = cS;
+    }
+}
+
+template <int G, bool XR = false>
 __device__ void clique_group_chunk(const Params<uint32_t>& p, int k, const SQ<uint32_t>& q, const MemoView& v,
                                    const unsigned int* bin, unsigned int lo, unsigned int hi,
-                                   unsigned long long& npairs, unsigned long long& nsets) {
+                                   unsigned long long& npairs, unsigned long long& nsets, const MemoPtrs& M,
+                                   const DfRank* x = nullptr) {
     constexpr int MEMO = MEMO_MASK;
     constexpr unsigned int NG = kDfCompute / G;
     const unsigned int w = (1u << (k - 1)) - 1u;
@@ -459,14 +478,14 @@ __device__ void clique_group_chunk(const Params<uint32_t>& p, int k, const SQ<ui
         uint32_t S = 0;
         if (act) {
             S = unrank_colex32(bin, q.n, k, h);
-            cS = card_fast<CLS_CLIQUE, MEMO>(p.memo, v, bin, q, S, k, h);
+            cS = card_fast<CLS_CLIQUE, MEMO>(M, v, bin, q, S, k, h);
             const uint32_t lo1 = S & (0u - S), R = S ^ lo1;
-            clique_eval_span<G>(q, p.memo.dcost, S, lo1, R, deposit_small(G, R), deposit_small(sub, R), sub, w, cS,
+            clique_eval_span<G>(q, M.dcost, S, lo1, R, deposit_small(G, R), deposit_small(sub, R), sub, w, cS,
                                 leaves, best, npairs);
         }
         best = group_min(best, G);
         if (act && sub == 0) {
-            clique_write(p.memo, S, best, cS);
+            clique_write_x<XR>(M, x, S, best, cS);
             nsets++;
         }
     }
@@ -1025,6 +1044,7 @@ __device__ void clique_level(const Params<uint32_t>& p, int k, const SQ<uint32_t
 constexpr int kCliqueMinBlocks = 3;
 __host__ __device__ constexpr size_t clique_smem_bytes() { return sizeof(SQ<uint32_t>) + sizeof(unsigned int) * 33 * 33; }
 
+template <bool XR = false>
 struct CliqueSched {
     const Params<uint32_t>& p;
     const unsigned int* bin;
@@ -1061,8 +1081,9 @@ struct CliqueSched {
     __device__ unsigned int need_count(int k1, int j) const { return bin[j * 33 + k1 - 1]; }
     __device__ void publish(const DfSlot& d) const {
         if (p.dfl[d.k].split) return;                   // split sets are published by their last contributor
-        df_publish_colex<false>(x, p.df, bin, d.k, d.k, d.lo, d.hi);
-        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex<false>(x, p.df, bin, k, k, p.share_lo[k], p.share_hi[k]);
+        DataflowDev* const ldf = XR ? x.df : p.df;
+        df_publish_colex<XR>(x, ldf, bin, d.k, d.k, d.lo, d.hi);
+        for (int k = d.k + 1; k <= d.k2; k++) df_publish_colex<XR>(x, ldf, bin, k, k, p.share_lo[k], p.share_hi[k]);
     }
 };
 
@@ -1081,6 +1102,24 @@ __device__ __noinline__ void clique_extract(const Params<uint32_t>& p, const SQ<
     }
 }
 
+// The extraction from this rank's replica (fused exchange): the same code on a
+// copy of the parameters that points at the replica, its descriptors and result.
+__device__ __noinline__ void clique_extract_x(const Params<uint32_t>& p, const SQ<uint32_t>& q, const MemoView& v,
+                                              const unsigned int* bin, const DfRank& x, const MemoPtrs& M) {
+    if (threadIdx.x == 0) x.result->t_level[p.n + 1] = globaltimer_ns();
+    level_counters_warp(p, x.result, x.desc);
+    if (threadIdx.x == 0) {
+        if (ld_relaxed_u32(&x.df->error)) {
+            x.result->n_nodes = 0;
+        } else {
+            x.result->error = 0;
+            extract_phase_m<uint32_t, MEMO_MASK>(M, x.result, p.n, q, v, bin, p.q->gen);
+        }
+        atomicMax(&x.df->t_done[p.n + 1], globaltimer_ns());
+    }
+}
+
+template <bool XR>
 __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(const __grid_constant__ Params<uint32_t> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SQ<uint32_t>& q = *reinterpret_cast<SQ<uint32_t>*>(smem_raw);
@@ -1089,7 +1128,17 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
     __shared__ DfCounters sc;
     __shared__ DfShared sh;
     __shared__ DfRank xr;
-    if (threadIdx.x == 0) df_rank_init(xr, p);
+    __shared__ MemoPtrs xm;                // this rank's replica (XR) or the launch's memo
+    if (threadIdx.x == 0) {
+        df_rank_init(xr, p);
+        xm = p.memo;
+        if (XR) {
+            xm.dcost = xr.dcost;
+            xm.dcard = xr.dcard;
+            xm.dleft = xr.dleft;
+            df_start_barrier(p, xr);
+        }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) p.result->t_level[0] = globaltimer_ns();   // kernel start
     load_query(q, p.q);
     for (int j = threadIdx.x; j <= kMaxN; j += blockDim.x) {
@@ -1109,12 +1158,12 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
     // ordered after its own writes
     __syncthreads();
     for (int u = threadIdx.x; u < q.n; u += blockDim.x) {
-        p.memo.dcost[1u << u] = q.leaf[u];
-        p.memo.dcard[1u << u] = q.card[u];
+        xm.dcost[1u << u] = q.leaf[u];
+        xm.dcard[1u << u] = q.card[u];
     }
     __syncthreads();
     if (threadIdx.x >= kDfCompute) {
-        df_control<false>(p, CliqueSched{p, bin, xr}, sh, xr);
+        df_control<XR>(p, CliqueSched<XR>{p, bin, xr}, sh, xr);
     } else {
         int kc = p.k_begin;
         unsigned long long npairs = 0, nsets = 0;      // this thread, level kc
@@ -1136,22 +1185,22 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
                 }
                 if (k > d.k) {
                     asm volatile("bar.sync 3, %0;" ::"r"(kDfCompute) : "memory");
-                    if (threadIdx.x == 0) p.result->t_level[k] = globaltimer_ns();
+                    if (threadIdx.x == 0) xr.result->t_level[k] = globaltimer_ns();
                 }
                 const DfLevel& L = p.dfl[k];
-                if (L.split) {
+                if (!XR && L.split) {             // (the fused exchange plans no split levels)
                     const unsigned int c = d.lo + (threadIdx.x >> 5);
                     if (c < d.hi) clique_split_chunk(p, k, q, v, bin, L, c, npairs, nsets);
                     continue;
                 }
                 const unsigned int lo = k == d.k ? d.lo : p.share_lo[k], hi = k == d.k ? d.hi : p.share_hi[k];
                 switch (L.G) {
-                    case 1: clique_group_chunk<1>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
-                    case 2: clique_group_chunk<2>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
-                    case 4: clique_group_chunk<4>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
-                    case 8: clique_group_chunk<8>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
-                    case 16: clique_group_chunk<16>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
-                    default: clique_group_chunk<32>(p, k, q, v, bin, lo, hi, npairs, nsets); break;
+                    case 1: clique_group_chunk<1, XR>(p, k, q, v, bin, lo, hi, npairs, nsets, xm, &xr); break;
+                    case 2: clique_group_chunk<2, XR>(p, k, q, v, bin, lo, hi, npairs, nsets, xm, &xr); break;
+                    case 4: clique_group_chunk<4, XR>(p, k, q, v, bin, lo, hi, npairs, nsets, xm, &xr); break;
+                    case 8: clique_group_chunk<8, XR>(p, k, q, v, bin, lo, hi, npairs, nsets, xm, &xr); break;
+                    case 16: clique_group_chunk<16, XR>(p, k, q, v, bin, lo, hi, npairs, nsets, xm, &xr); break;
+                    default: clique_group_chunk<32, XR>(p, k, q, v, bin, lo, hi, npairs, nsets, xm, &xr); break;
                 }
             }
             df_finish(sh, i);
@@ -1162,8 +1211,11 @@ __global__ void __launch_bounds__(kDfThreads, kCliqueMinBlocks) k_dp_clique_df(c
         }
         flush();
     }
-    if (!df_exit<false>(p, sc, xr)) return;
-    if (p.do_extract && threadIdx.x < 32) clique_extract(p, q, v, bin);
+    if (!df_exit<XR>(p, sc, xr)) return;
+    if (p.do_extract && threadIdx.x < 32) {
+        if (XR) clique_extract_x(p, q, v, bin, xr, xm);
+        else clique_extract(p, q, v, bin);
+    }
     df_reset(p, xr);
 }
 

@@ -1316,11 +1316,19 @@ __device__ void level_counters_warp(const Params<M>& p, ResultDev* r, const Leve
 }
 
 template <typename M, int MEMO>
+__device__ void extract_phase_m(const MemoPtrs& PM, ResultDev* r, int n, const SQ<M>& q, const MemoView& v,
+                                const unsigned int* rtab, unsigned int gen);
+template <typename M, int MEMO>
 __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView& v, const unsigned int* rtab,
                               unsigned int gen) {
+    extract_phase_m<M, MEMO>(p.memo, p.result, p.n, q, v, rtab, gen);
+}
+// (the memo, result and n explicitly: the fused exchange extracts from a
+// rank's replica)
+template <typename M, int MEMO>
+__device__ void extract_phase_m(const MemoPtrs& PM, ResultDev* r, int n, const SQ<M>& q, const MemoView& v,
+                                const unsigned int* rtab, unsigned int gen) {
     // (the level counters are written by level_counters_warp before)
-    ResultDev* r = p.result;
-    const int n = p.n;
     if (r->error) {
         r->n_nodes = 0;
         return;
@@ -1354,7 +1362,7 @@ __device__ void extract_phase(const Params<M>& p, const SQ<M>& q, const MemoView
         }
         if (st_state[top] == 0) {
             M L;
-            st_c[top] = memo_get<M, MEMO>(p.memo, gen, v, rtab, S, L, &st_card[top]);
+            st_c[top] = memo_get<M, MEMO>(PM, gen, v, rtab, S, L, &st_card[top]);
             st_L[top] = L;
             st_state[top] = 1;
             st_set[sp] = L;

@@ -170,6 +170,7 @@ struct mpdp_ctx {
     bool memo_conn = false;               // general graph, bitmask memo pre-filled absent (R20)
     int star_occ = 0;                     // k_dp_star CTAs per SM
     int star_occ_xr = 0;                  // k_dp_star<true> (fused peer exchange)
+    int clique_xr_occ = 0;                // k_dp_clique_df<true> (fused peer exchange)
     int cluster_size = 0;                 // k_dp_tree_cluster: CTAs per cluster (0 = not probed yet)
     int clique_df_occ = 0;                // k_dp_clique_df (ablation) CTAs per SM
     bool clique_df_attr = false;
@@ -466,7 +467,10 @@ static mpdp_status plan_layout(mpdp_ctx* c) {
     for (int k = 2; k <= n; k++) dense_entries += binom_u64(n, k) + (unsigned long long)W;
     // MEMO_MASK: clique / general queries on one GPU through the whole-query
     // kernel index the same arrays by bitmask (2^n entries)
-    const bool mask = c->cls != CLS_TREE && !c->multi && !c->wide && n >= 2 && n <= kMaskMaxN &&
+    // (multi-GPU cliques with the fused peer exchange keep the bitmask memo:
+    // every rank holds a full replica of it)
+    const bool xr_clique = c->multi && !c->nccl_self && c->cls == CLS_CLIQUE && (c->flags & MPDP_FLAG_FUSED_EXCHANGE);
+    const bool mask = c->cls != CLS_TREE && (!c->multi || xr_clique) && !c->wide && n >= 2 && n <= kMaskMaxN &&
                       !(c->flags & (MPDP_FLAG_HASH_MEMO | MPDP_FLAG_RANK_MEMO | MPDP_FLAG_NO_FUSED |
                                     MPDP_FLAG_PROFILE_KERNELS)) &&
                       (c->timeout_ms <= 0 || c->cls == CLS_CLIQUE);   // (k_dp_clique checks the deadline)
@@ -716,7 +720,8 @@ static size_t level_loop_smem(int n) {
 // most kCliqueSoloPairs pairs run as one solo chunk.  Returns false when the
 // merge slots exceed the workspace's.
 constexpr unsigned long long kCliqueSoloPairs = 512;
-static bool plan_clique_df(Params<uint32_t>& p, unsigned int grid, unsigned long long slot_cap) {
+static bool plan_clique_df(Params<uint32_t>& p, unsigned int grid, unsigned long long slot_cap,
+                           bool allow_split = true) {
     const unsigned long long T = (unsigned long long)grid * kDfCompute, nwarps = T / 32;
     const int n = p.n;
     unsigned int base = 0;
@@ -728,7 +733,7 @@ static bool plan_clique_df(Params<uint32_t>& p, unsigned int grid, unsigned long
         DfLevel& L = p.dfl[k];
         L = DfLevel{};
         L.base = base;
-        const unsigned int G = clique_group(w, C, T);
+        const unsigned int G = allow_split ? clique_group(w, C, T) : clique_group(w, C, T, ~0ull);
         if (!G) {                                          // split path
             const unsigned long long P = C * w;
             const unsigned long long csize = std::max<unsigned long long>(512, (P + nwarps - 1) / nwarps);
@@ -778,11 +783,11 @@ static mpdp_status run_clique_df(mpdp_ctx* c, Params<uint32_t> p) {
     const size_t smem = clique_smem_bytes();
     int& occ = c->clique_df_occ;
     if (!c->clique_df_attr) {
-        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_clique_df, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_clique_df<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         c->clique_df_attr = true;
     }
     if (!occ) {
-        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_clique_df, kDfThreads, smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dp_clique_df<false>, kDfThreads, smem));
         if (occ < 1) return fail(c, MPDP_ERR_CUDA, "clique kernel does not fit on an SM");
     }
     unsigned long long want = 1;
@@ -802,7 +807,7 @@ static mpdp_status run_clique_df(mpdp_ctx* c, Params<uint32_t> p) {
     c->desc_clean = true;
     void* args[] = {&p};
     CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
-    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_clique_df, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_clique_df<false>, dim3(grid), dim3(kDfThreads), args, smem, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
     CUDA_TRY(c, cudaMemcpyAsync(c->h_result, c->ws + c->lay.result, sizeof(ResultDev), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
@@ -1253,6 +1258,81 @@ static mpdp_status run_star_xr(mpdp_ctx* c) {
     return MPDP_OK;
 }
 
+// Fused peer exchange for cliques (MPDP_FLAG_FUSED_EXCHANGE): k_dp_clique_df
+// with every set written into every rank's bitmask-memo replica (cost, card
+// and left) and counted in every replica's dataflow counters; no split levels
+// (a set is evaluated by one group of one rank, so no cross-rank merges).
+// Simulated world: the ranks are the CTA groups blockIdx % W of one launch.
+static mpdp_status run_clique_xr(mpdp_ctx* c) {
+    const int W = c->world;
+    if (W > kMaxXr) return fail(c, MPDP_ERR_INVALID_ARGUMENT, "fused exchange: world > 8");
+    if (!c->simulate && !c->peers_open)
+        return fail(c, MPDP_ERR_INVALID_ARGUMENT, "fused exchange across GPUs needs mpdp_ctx_open_peers first");
+    const DevLayout& L = c->lay;
+    Params<uint32_t> p = make_params<uint32_t>(c, 0);
+    const size_t smem = clique_smem_bytes();
+    if (!c->clique_xr_occ) {
+        CUDA_TRY(c, cudaFuncSetAttribute(k_dp_clique_df<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->clique_xr_occ, k_dp_clique_df<true>, kDfThreads, smem));
+        if (c->clique_xr_occ < 1) return fail(c, MPDP_ERR_CUDA, "clique kernel does not fit on an SM");
+    }
+    const unsigned int full = (unsigned int)std::min<unsigned long long>((unsigned long long)c->num_sms * c->clique_xr_occ,
+                                                                         (unsigned long long)kMaxGrid);
+    const unsigned int grid = c->simulate ? full / (unsigned int)W * (unsigned int)W : full;
+    const unsigned int ctas_total = c->simulate ? grid : grid * (unsigned int)W;
+    plan_clique_df(p, ctas_total, ~0ull, false);
+    p.do_extract = 1;
+    XrTable t;
+    memset(&t, 0, sizeof(t));
+    t.W = W;
+    t.emulate = c->simulate ? 1 : 0;
+    t.rank = c->simulate ? 0 : c->rank;
+    t.ctas_total = ctas_total;
+    for (int s = 0; s < W; s++) {
+        unsigned char* base = c->simulate ? c->ws : c->peer_ws[s];
+        const int sh = c->simulate ? s : 0;
+        t.cost[s] = reinterpret_cast<double*>(base + L.sh_dcost[sh]);
+        t.card[s] = reinterpret_cast<double*>(base + L.sh_dcard[sh]);
+        t.left[s] = reinterpret_cast<unsigned int*>(base + L.sh_dleft[sh]);
+        t.df[s] = reinterpret_cast<DataflowDev*>(base + L.sh_df[sh]);
+        t.desc[s] = reinterpret_cast<LevelDesc*>(base + L.sh_desc[sh]);
+        t.result[s] = reinterpret_cast<ResultDev*>(base + L.sh_result[sh]);
+    }
+    if (!c->h_xr && cudaMallocHost(&c->h_xr, sizeof(XrTable)) != cudaSuccess)
+        return fail(c, MPDP_ERR_OOM, "pinned host allocation failed");
+    memcpy(c->h_xr, &t, sizeof(t));
+    CUDA_TRY(c, cudaMemcpyAsync(c->ws + L.xr, c->h_xr, sizeof(XrTable), cudaMemcpyHostToDevice, c->stream));
+    p.xr = reinterpret_cast<const XrTable*>(c->ws + L.xr);
+    p.xr_epoch = ++c->xr_epoch;
+    CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+    unsigned int nl = 1;
+    if (!c->desc_clean) {
+        for (int sh = 0; sh < L.nshards; sh++) {
+            k_init<uint32_t><<<1, 256, 0, c->stream>>>(make_params<uint32_t>(c, sh));
+            nl++;
+        }
+    }
+    c->desc_clean = true;
+    void* args[] = {&p};
+    CUDA_TRY(c, cudaEventRecord(c->kev[0], c->stream));
+    CUDA_TRY(c, cudaLaunchCooperativeKernel((const void*)k_dp_clique_df<true>, dim3(grid), dim3(kDfThreads), args, smem,
+                                            c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->kev[1], c->stream));
+    for (int sh = 0; sh < L.nshards; sh++)
+        CUDA_TRY(c, cudaMemcpyAsync(c->h_results + sh, c->ws + L.sh_result[sh], sizeof(ResultDev),
+                                    cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+    c->launches = nl;
+    c->enum_launches = 0;
+    c->eval_launches = 1;
+    c->nkev = 2;
+    c->fused = true;
+    c->sharded = false;
+    c->xr_run = true;
+    c->d2h_bytes = sizeof(ResultDev) * L.nshards;
+    return MPDP_OK;
+}
+
 template <int CLS>
 static mpdp_status run_sharded(mpdp_ctx* c) {
     if (c->wide || c->lay.memo_kind != MEMO_DENSE)
@@ -1263,6 +1343,8 @@ static mpdp_status run_sharded(mpdp_ctx* c) {
     const bool star = CLS == CLS_TREE && c->star_hub >= 0 && n >= 3 &&
                       !(c->flags & (MPDP_FLAG_NO_STAR | MPDP_FLAG_NO_FUSED | MPDP_FLAG_PROFILE_KERNELS));
     if (star && (c->flags & MPDP_FLAG_FUSED_EXCHANGE) && !c->nccl_self) return run_star_xr(c);
+    if (CLS == CLS_CLIQUE && c->lay.mask_memo && (c->flags & MPDP_FLAG_FUSED_EXCHANGE) && !c->nccl_self)
+        return run_clique_xr(c);
     const void* kern = star ? (const void*)k_dp_star<false> : level_loop_kernel<CLS>();
     const size_t smem = star ? star_smem_bytes() : level_loop_smem<CLS>(n);
     int occ_star = 0;

@@ -1,4 +1,4 @@
-"""The fused peer exchange of the star kernel (MPDP_FLAG_FUSED_EXCHANGE,
+"""The fused peer exchange of the star and clique kernels (MPDP_FLAG_FUSED_EXCHANGE,
 SURVEY §8(e)): W ranks, each with a full memo replica, store
 every chunk's costs into every replica and count it in every replica's
 dataflow counters; emulated on one GPU as the CTA groups of one cooperative
@@ -74,3 +74,25 @@ def test_fused_exchange_needs_peers_across_gpus():
         with pytest.raises(mpdp.MPDPError) as e:
             c.peer_record()
         assert e.value.status == mpdp.ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("n,seed,leaf", [(3, 0, False), (5, 1, True), (9, 2, False), (12, 3, True), (14, 4, False)])
+def test_fused_exchange_clique(xr_ctx, n, seed, leaf):
+    """Cliques through k_dp_clique_df with the fused exchange: every set
+    written into every rank's bitmask-memo replica, counted in every replica."""
+    g = W.clique(n, seed)
+    if leaf:
+        g.leaf_cost = [float((5 * i) % 3) for i in range(n)]
+    r = xr_ctx.mpdp_optimize(g)
+    assert r.memo_kind == 2
+    check(r, O.optimize(g), g)
+
+
+def test_fused_exchange_clique18_full_size():
+    """BASELINE config 4 (clique-18) with 4 emulated ranks."""
+    from paper_2202_13511_b200 import mpdp
+    g = W.clique(18, 0)
+    with mpdp.Context(device=0, workspace_bytes=4 << 30, world=4,
+                      flags=mpdp.FLAG_SIMULATE_WORLD | mpdp.FLAG_FUSED_EXCHANGE) as c:
+        r = c.mpdp_optimize(g)
+    check(r, O.optimize(g), g)

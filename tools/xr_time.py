@@ -15,7 +15,7 @@ reps = 10
 if "--reps" in args:
     i = args.index("--reps"); reps = int(args[i + 1]); del args[i:i + 2]
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for name in args or ["star-25"]:
+for name in args or ["star-25", "clique-18"]:
     topo, n = name.rsplit("-", 1)
     g = W.generate(topo, int(n), 0)
     for world in (1, 2, 4, 8):
