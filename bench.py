@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config sub-results")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
-                    help="N > 1, star workloads: fused peer exchange inside k_dp_star (default) "
+                    help="N > 1, star / clique workloads: fused peer exchange inside the dataflow kernel (default) "
                          "or per-level ncclAllGather")
     return ap.parse_args()
 
@@ -439,8 +439,8 @@ def run_ours(args):
                        "l2": "flushed between steps (256 MiB write)",
                        "pairs_convention": "unordered join pairs (reading R3; SPEC's ordered count is 2x)",
                        "parallelism": ("single-gpu" if world == 1 else
-                                       f"x{world}: fused peer exchange in k_dp_star" if args.exchange == "fused"
-                                       and args.workload.startswith("star") else
+                                       f"x{world}: fused peer exchange in the dataflow kernel" if args.exchange == "fused"
+                                       and args.workload.startswith(("star", "clique")) else
                                        f"level-sharded x{world} (NCCL allgather per level)"),
                        "opt_time_ms_median": statistics.median(step_ms)},
             "clocks": clk_now, "roofline": roof,

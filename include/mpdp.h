@@ -198,14 +198,15 @@ typedef struct {
  * per-level ncclAllGather exchange and the counter ncclAllReduce execute on a
  * single GPU (bit-identical results to the single-GPU kernels)            */
 #define MPDP_FLAG_NCCL_SELF 8192u
-/* flags (multi-GPU contexts, star queries): the FUSED PEER EXCHANGE instead of
+/* flags (multi-GPU contexts, star and clique queries): the FUSED PEER EXCHANGE instead of
  * per-level ncclAllGather (sets of one size are independent,
  * P:214, and a set reads only its subsets).  One
  * k_dp_star launch per rank; each chunk of sets stores its costs into every
  * rank's memo replica (NVLink peer stores) and adds its completion count to
  * every replica's per-(level, largest element) counters, so a chunk of level k
  * waits in its own replica for exactly the level-(k-1) sets it reads and no
- * level ends in a launch or a collective.  With MPDP_FLAG_SIMULATE_WORLD the W
+ * level ends in a launch or a collective (cliques: k_dp_clique_df, every set's
+ * cost, card and left into every rank's bitmask-memo replica).  With MPDP_FLAG_SIMULATE_WORLD the W
  * ranks are the CTA groups (blockIdx mod W) of ONE cooperative launch over the
  * W shards of the workspace; across GPUs call mpdp_ctx_open_peers first.
  * Results are bit-identical to the single-GPU kernel; every rank extracts the
