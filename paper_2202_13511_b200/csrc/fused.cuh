@@ -871,7 +871,9 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             o[7] = nsmall;
         }
 #endif
-        if (CLS != CLS_TREE && heavy_level) {
+        // (a heavy level that found no heavy set -- sparse general graphs --
+        // skips the heavy phase and its barrier: d is grid-uniform here)
+        if (CLS != CLS_TREE && heavy_level && d.n_heavy > 0) {
             // card(S) of every heavy set once (one thread per set); general
             // graphs with memo connectivity wrote it with the heavy list
             if (!(CLS == CLS_GENERAL && q.mc)) {
