@@ -594,6 +594,14 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
     __shared__ unsigned int s_small;
     unsigned long long* small_list = reinterpret_cast<unsigned long long*>(p.light);
     __shared__ Tri s_excl, s_agg;
+    // heavy sets spanning many work items: their first_heavy ranges are filled
+    // by the whole CTA after the queue barrier instead of by one thread (the
+    // full cycle at cycle-20's top level spans 2048 items: 47 us of one thread)
+    constexpr int kFhDefer = 32;
+    __shared__ unsigned int s_fh_n;
+    __shared__ unsigned long long s_fh_lo[kFhDefer], s_fh_hi[kFhDefer];
+    __shared__ unsigned int s_fh_h[kFhDefer];
+    if (threadIdx.x == 0) s_fh_n = 0;
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
     if constexpr (CLS == CLS_GENERAL && sizeof(M) == 4) build_nbtab(q, p.q);   // byte-table BFS steps
@@ -776,8 +784,16 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                             p.bkey[hi] = key_inf();
                             p.bdone[hi] = 0;
                             const unsigned long long it0 = (wi + item - 1) / item, it1 = (wi + w - 1) / item;
-                            for (unsigned long long it = it0; it <= it1; it++)
-                                if (it < p.fh_cap) p.first_heavy[it] = (unsigned int)hi;
+                            unsigned int slot = kFhDefer;
+                            if (it1 >= it0 + 16) slot = atomicAdd(&s_fh_n, 1u);
+                            if (slot < kFhDefer) {
+                                s_fh_lo[slot] = it0;
+                                s_fh_hi[slot] = it1;
+                                s_fh_h[slot] = (unsigned int)hi;
+                            } else {
+                                for (unsigned long long it = it0; it <= it1; it++)
+                                    if (it < p.fh_cap) p.first_heavy[it] = (unsigned int)hi;
+                            }
                         }
                         wi += w;
                         hi++;
@@ -786,6 +802,14 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                 }
             }
             __syncthreads();
+            if (s_fh_n) {                      // the deferred first_heavy ranges, CTA-wide
+                const unsigned int nd = s_fh_n < kFhDefer ? s_fh_n : kFhDefer;
+                for (unsigned int e = 0; e < nd; e++)
+                    for (unsigned long long it = s_fh_lo[e] + threadIdx.x; it <= s_fh_hi[e]; it += blockDim.x)
+                        if (it < p.fh_cap) p.first_heavy[it] = s_fh_h[e];
+                __syncthreads();
+                if (threadIdx.x == 0) s_fh_n = 0;
+            }
 
             TRACE(3);
 #ifdef MPDP_TRACE
