@@ -12,6 +12,8 @@ F = mpdp
 ctxs = [mpdp.Context(device=0, workspace_bytes=2 << 30, flags=f) for f in
         (0, F.FLAG_HASH_MEMO, F.FLAG_RANK_MEMO, F.FLAG_NO_FUSED, F.FLAG_NO_SMALL | F.FLAG_NO_STAR, F.FLAG_NO_CCC)]
 ctxs.append(mpdp.Context(device=0, workspace_bytes=2 << 30, world=2, flags=F.FLAG_SIMULATE_WORLD))
+ctxs.append(mpdp.Context(device=0, workspace_bytes=2 << 30, world=3,
+                         flags=F.FLAG_SIMULATE_WORLD | F.FLAG_FUSED_EXCHANGE))   # fused peer exchange
 bad = 0
 batch = []
 for i in range(200):
