@@ -605,8 +605,14 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
 
     memo_prologue<M, MEMO>(p, p.n, q, v, rtab);
     if constexpr (CLS == CLS_GENERAL && sizeof(M) == 4) build_nbtab(q, p.q);   // byte-table BFS steps
-    if constexpr (CLS == CLS_GENERAL && MEMO == MEMO_MASK)
+    if constexpr (CLS == CLS_GENERAL && MEMO == MEMO_MASK) {
         if (threadIdx.x == 0 && p.memo_conn) q.mc = p.memo.dcost;               // reading R20
+        // the singletons' slots hold their leaf costs, so the probe loops need
+        // no singleton branch; written by every CTA before its first level (the
+        // same values everywhere; a CTA's own probes follow its own writes)
+        if (p.memo_conn)
+            for (int u = threadIdx.x; u < p.n; u += blockDim.x) p.memo.dcost[1u << u] = p.q->leaf[u];
+    }
     unsigned int nbar = 0;                 // grid barriers passed (thread 0)
     const unsigned int gen = p.q->gen;
     const int n = p.n;

@@ -553,7 +553,12 @@ __global__ void __launch_bounds__(kBlock) k_enum(const __grid_constant__ Params<
 // test of the block); the min is kept in f64 / mask registers (costs >= 0, so
 // the f64 order is the bit order of the Key, reading R7).  Singletons read the
 // leaf cost.  Counts valid pairs and non-singleton probes.
-template <bool HANG, typename M>
+//
+// The singletons' slots hold their leaf costs (written by every CTA of the
+// kernel before its first level), so every probe is one branch-free load.
+// COUNT: count the non-singleton probes pair by pair (else the caller uses
+// mc_probes_closed).
+template <bool HANG, typename M, bool COUNT = true>
 __device__ __forceinline__ void mc_span(const SQ<M>& q, M S, M lo, M R, M D, M sub, unsigned long long j,
                                         unsigned long long b, unsigned int step, double cS, M C, const M* hang,
                                         Key& best, unsigned long long& nvalid, unsigned long long& nprobe) {
@@ -573,10 +578,9 @@ __device__ __forceinline__ void mc_span(const SQ<M>& q, M S, M lo, M R, M D, M s
                 for (M T = X & C; T; T &= T - 1) X |= hang[ctz(T)];
             A[u] = X;
             const M Y = S ^ X;
-            const bool xs = (X & (X - 1)) != 0, ys = (Y & (Y - 1)) != 0;
-            ca[u] = ok[u] ? (xs ? mc[X] : q.leaf[ctz(X)]) : 0.0;
-            cb[u] = ok[u] ? (ys ? mc[Y] : q.leaf[ctz(Y)]) : 0.0;
-            np += ok[u] ? (unsigned int)xs + (unsigned int)ys : 0u;
+            ca[u] = ok[u] ? mc[X] : 0.0;
+            cb[u] = ok[u] ? mc[Y] : 0.0;
+            if (COUNT) np += ok[u] ? (unsigned int)((X & (X - 1)) != 0) + (unsigned int)((Y & (Y - 1)) != 0) : 0u;
             sub = ((sub | ~R) + D) & R;
         }
 #pragma unroll
@@ -593,6 +597,20 @@ __device__ __forceinline__ void mc_span(const SQ<M>& q, M S, M lo, M R, M D, M s
     nvalid += nv;
     nprobe += np;
     best = Key{(unsigned long long)__double_as_longlong(bc), (unsigned long long)bl};
+}
+
+// Non-singleton probes of the one-block candidates j in [a, b) of a set whose
+// lowest vertex is lo and R = S \ {lo}, r = |R|: two per pair, less the
+// singleton sides -- lb = {lo} at j = 0, and rb = {v} at j = 2^r - 1 - 2^t.
+__device__ __forceinline__ unsigned long long mc_probes_closed(unsigned long long a, unsigned long long b, int r) {
+    if (b <= a) return 0;
+    unsigned long long singles = a == 0 ? 1 : 0;
+    const unsigned long long full = (1ull << r) - 1;
+    for (int t = 0; t < r; t++) {
+        const unsigned long long j = full - (1ull << t);
+        singles += (j >= a && j < b) ? 1 : 0;
+    }
+    return 2 * (b - a) - singles;
 }
 
 // ------------------------------------------------------------ k_eval
@@ -665,8 +683,10 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
         const M lo = lowbit(S), R = S ^ lo;    // the probes of lb and rb are the CCP test (R20)
         sink.flush();
         unsigned long long nv = 0;
-        mc_span<false, M>(q, S, lo, R, lowbit(R), deposit<M>(j0, R), j0, j1, 1u, sink.cS, (M)0, nullptr, sink.best, nv,
-                          sink.nprobe);
+        unsigned long long np0 = 0;
+        mc_span<false, M, false>(q, S, lo, R, lowbit(R), deposit<M>(j0, R), j0, j1, 1u, sink.cS, (M)0, nullptr,
+                                 sink.best, nv, np0);
+        sink.nprobe += mc_probes_closed(j0, j1, popc(R));
         nccp += nv;
         return;
     }
@@ -1215,9 +1235,11 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                 if (j < b) {
                     const M da = a ? deposit<M>(a, R) : (M)0;      // deposit(a + lane), as a masked add
                     const M sub = ((da | ~R) + deposit<M>(lane, R)) & R;
-                    mc_span<false, M>(q, S, lo, R, D, sub, j, b, 32u, sink.cS, (M)0, nullptr, sink.best, sink.nvalid,
-                                      sink.nprobe);
+                    unsigned long long np0 = 0;
+                    mc_span<false, M, false>(q, S, lo, R, D, sub, j, b, 32u, sink.cS, (M)0, nullptr, sink.best,
+                                             sink.nvalid, np0);
                 }
+                if (lane == 0) sink.nprobe += mc_probes_closed(a, b, popc(R));
                 nccp += sink.nvalid;
             } else if (CLS == CLS_GENERAL && q.mc && kind == KIND_BLOCKS) {
                 eval_blocks_hang<M>(q, S, a, b, a == 0 && b == w, sink, s_ccc[threadIdx.x >> 5], lblk, hnb);
