@@ -56,6 +56,15 @@ template <typename M> __device__ __forceinline__ M deposit(uint64_t j, M R) {
     return out;
 }
 
+// deposit(j, R) for a small j (lane offsets, strides): walks R's elements
+// while j has bits left -- at most log2(j) + 1 steps and no bit search
+template <typename M> __device__ __forceinline__ M deposit_lo(unsigned int j, M R) {
+    M out = 0;
+    for (M T = R; j && T; T &= T - 1, j >>= 1)
+        if (j & 1u) out |= T & (M)(0 - T);
+    return out;
+}
+
 // ---------------------------------------------------------------- hashing
 // Murmur3 finalisers ("fast Murmur3 hashing")
 __device__ __forceinline__ uint32_t fmix(uint32_t h) {

@@ -1039,7 +1039,7 @@ __device__ __forceinline__ void eval_blocks_ccc(const SQ<M>& q, M S, int kind, u
         const bool complete = !q.dpsub && induced_degree_sum(q, Bm) == bsz * (bsz - 1);
         const unsigned long long a0 = (a > base ? a - base : 0), a1 = (b - base < wb ? b - base : wb);
         const M lo = lowbit(Bm), R = Bm ^ lo;
-        const M D32 = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
+        const M D32 = popc(R) > 5 ? deposit_lo<M>(32u, R) : (M)0;
         M sub = a0 + lane < a1 ? deposit<M>(a0 + lane, R) : (M)0;
         for (unsigned long long j0 = a0; j0 < a1; j0 += 32) {
             const unsigned long long j = j0 + lane;
@@ -1149,12 +1149,12 @@ __device__ __forceinline__ void eval_blocks_hang(const SQ<M>& q, M S, unsigned l
             hang[v] = grow(q, bitm<M>(v), ext | bitm<M>(v));
         }
         __syncwarp();
-        const M lo = lowbit(Bm), R = Bm ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
+        const M lo = lowbit(Bm), R = Bm ^ lo, D = popc(R) > 5 ? deposit_lo<M>(32u, R) : (M)0;
         const unsigned long long j = a0 + lane;
         if (j < a1) {
             // deposit(a0 + lane) = deposit(a0) (+) deposit(lane) in R's domain
             const M da = a0 ? deposit<M>(a0, R) : (M)0;
-            const M sub = ((da | ~R) + deposit<M>(lane, R)) & R;
+            const M sub = ((da | ~R) + deposit_lo<M>(lane, R)) & R;
             mc_span<true, M>(q, S, lo, R, D, sub, j, a1, 32u, sink.cS, C, hang, sink.best, sink.nvalid, sink.nprobe);
         }
         base += wb;
@@ -1217,7 +1217,7 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                 // sides differ in the lowest elements of S, so one warp's probes
                 // fall into few memo lines; +32 in the deposited domain is a
                 // masked add (carries skip the bits outside R)
-                const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;   // (<= 32 pairs: one round)
+                const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit_lo<M>(32u, R) : (M)0;   // (<= 32 pairs: one round)
                 unsigned long long j = a + lane;
                 M sub = j < b ? deposit<M>(j, R) : 0;
                 for (; j < b; j += 32) {
@@ -1230,11 +1230,11 @@ __device__ void heavy_phase(const Params<M>& p, int k, unsigned long long item, 
                 // one block S (or every set, DPSUB ablation): S_left = lb, and
                 // the probes of lb and rb are the CCP test (reading R20); lanes
                 // interleaved as for complete sets
-                const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit<M>(32, R) : (M)0;
+                const M lo = lowbit(S), R = S ^ lo, D = popc(R) > 5 ? deposit_lo<M>(32u, R) : (M)0;
                 const unsigned long long j = a + lane;
                 if (j < b) {
                     const M da = a ? deposit<M>(a, R) : (M)0;      // deposit(a + lane), as a masked add
-                    const M sub = ((da | ~R) + deposit<M>(lane, R)) & R;
+                    const M sub = ((da | ~R) + deposit_lo<M>(lane, R)) & R;
                     unsigned long long np0 = 0;
                     mc_span<false, M, false>(q, S, lo, R, D, sub, j, b, 32u, sink.cS, (M)0, nullptr, sink.best,
                                              sink.nvalid, np0);
