@@ -163,7 +163,8 @@ __device__ __forceinline__ bool connected(const SQ<M>& q, M S) {
 // instead of a BFS (Alg. connected).  Singletons are connected.
 constexpr unsigned long long kMemoAbsent = ~0ull;
 __device__ __forceinline__ bool memo_present(double c) {
-    return (unsigned long long)__double_as_longlong(c) != kMemoAbsent;
+    // (the high word decides: a cost, >= 0 or +inf, never has an all-ones one)
+    return __double2hiint(c) != -1;
 }
 template <typename M>
 __device__ __forceinline__ bool conn_sub(const SQ<M>& q, M X) {

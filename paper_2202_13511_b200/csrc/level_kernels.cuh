@@ -566,13 +566,15 @@ __device__ __forceinline__ void mc_span(const SQ<M>& q, M S, M lo, M R, M D, M s
     double bc = __longlong_as_double((long long)best.c);
     M bl = (M)best.l;
     unsigned int nv = 0, np = 0;
-    for (; j < b; j += 4ull * step) {
+    // (32-bit counters: the bitmask memo has n <= 24, so a set has < 2^23 pairs)
+    const unsigned int b32 = (unsigned int)b;
+    for (unsigned int j32 = (unsigned int)j; j32 < b32; j32 += 4u * step) {
         M A[4];
         double ca[4], cb[4];
         bool ok[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-            ok[u] = j + (unsigned long long)step * u < b;
+            ok[u] = j32 + step * u < b32;
             M X = lo | sub;
             if (HANG)
                 for (M T = X & C; T; T &= T - 1) X |= hang[ctz(T)];
