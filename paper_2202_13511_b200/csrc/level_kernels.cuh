@@ -166,6 +166,9 @@ template <typename M> struct Params {
     // warp whose claim holds their first pair (no cross-warp merge); larger
     // sets are cut at the claim boundaries and merged
     unsigned long long heavy_whole;
+    // tree list kernel: the next level is generated from this one (sparse
+    // expansion) when expand_fac x sets x (n - k) candidates <= C(n, k+1) ranks
+    double expand_fac;
     // general graphs on the bitmask memo: the cost array was filled with
     // kMemoAbsent at staging, so connectivity checks may probe it (reading R20)
     int memo_conn;

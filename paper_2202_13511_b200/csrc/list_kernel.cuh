@@ -273,16 +273,17 @@ __global__ void __launch_bounds__(kBlock, 2) k_dp_list(const __grid_constant__ P
             // thread) * (n - k) candidates over up to 32 lanes per set) below
             // the per-thread share of the ranks
             const unsigned long long T = (unsigned long long)gridDim.x * blockDim.x;
-            expand = CLS == CLS_TREE && whole && 4ull * N * (unsigned long long)(p.n - k) <= C1 &&
+            const double cand = p.expand_fac * (double)N * (double)(p.n - k);   // weighted candidates
+            const unsigned long long seg_grow = ((N + gridDim.x - 1) / gridDim.x + 1) * (unsigned long long)(p.n - k);
+            expand = CLS == CLS_TREE && whole && cand <= (double)C1 && seg_grow * gridDim.x <= p.list_cap &&
                      2ull * ((32ull * N + T - 1) / T) * (unsigned long long)(p.n - k) <= 32ull * ((C1 + T - 1) / T);
             // dense tree levels (one thread per set): the evaluation walk itself
             // generates level k+1 (emit_children), no rank scan
-            const unsigned long long seg_grow = ((N + gridDim.x - 1) / gridDim.x + 1) * (unsigned long long)(p.n - k);
             // (only where the candidates are few next to the ranks: the rank scan
             // writes the next list in colex order, which the star levels' probes
             // need for locality -- measured 1.42 vs 1.59 ms on star-25)
             fused_grow = CLS == CLS_TREE && whole && k >= 3 && 2ull * N > T && seg_grow * gridDim.x <= p.list_cap &&
-                         4ull * N * (unsigned long long)(p.n - k) <= C1;
+                         cand <= (double)C1;
             if (fused_grow) expand = false;
             seg_next = (expand || fused_grow) ? seg_grow : (unsigned long long)blockDim.x * list_rpt(C1);
             if (blockIdx.x == 0 && threadIdx.x == 0) p.desc[k + 1].seg = (unsigned int)seg_next;

@@ -613,6 +613,7 @@ static Params<M> make_params(mpdp_ctx* c, int shard = 0) {
     p.light_max = light_max_general();
     p.memo_conn = c->memo_conn ? 1 : 0;
     p.heavy_whole = getenv("MPDP_DEBUG_HEAVY_WHOLE") ? strtoull(getenv("MPDP_DEBUG_HEAVY_WHOLE"), nullptr, 10) : 2048;
+    p.expand_fac = getenv("MPDP_DEBUG_EXPAND_FAC") ? atof(getenv("MPDP_DEBUG_EXPAND_FAC")) : 0.1;
     p.clique_split_w = getenv("MPDP_DEBUG_CLIQUE_SPLIT") ? strtoull(getenv("MPDP_DEBUG_CLIQUE_SPLIT"), nullptr, 10) : 4096;
     p.clique_set_cost = getenv("MPDP_DEBUG_CLIQUE_SETCOST") ? atof(getenv("MPDP_DEBUG_CLIQUE_SETCOST")) : kCliqueSetCost;
     p.clique_split_fac = getenv("MPDP_DEBUG_CLIQUE_SPLITFAC") ? atof(getenv("MPDP_DEBUG_CLIQUE_SPLITFAC")) : 1.0;
