@@ -222,6 +222,57 @@ def l2_copy_gbs(torch, dev, mb=24, reps=50):
     return 2 * (mb << 20) * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
 
 
+def plan_cost_recomputed(g, r):
+    """The returned plan's C_out by the documented recurrence (card(L x R) =
+    card(L) card(R) x the selectivities of the crossing edges in edge-id
+    order, reading R17), after checking it is a cross-product-free tree over
+    all relations; None if it is not.  A plan checker, not the oracle."""
+    adj = {}
+    for i, (u, v) in enumerate(g.edges):
+        adj.setdefault(u, []).append((v, i))
+        adj.setdefault(v, []).append((u, i))
+    rels, card, cost = {}, {}, {}
+    for i, nd in enumerate(r.nodes):
+        if nd.relation >= 0:
+            rels[i], card[i], cost[i] = {nd.relation}, g.card[nd.relation], 0.0
+            continue
+        if not (nd.left < i and nd.right < i) or rels[nd.left] & rels[nd.right]:
+            return None
+        cross = sorted(e for x in rels[nd.left] for (u, e) in adj.get(x, []) if u in rels[nd.right])
+        if not cross:
+            return None
+        c = card[nd.left] * card[nd.right]
+        for e in cross:
+            c = c * g.sel[e]
+        rels[i], card[i] = rels[nd.left] | rels[nd.right], c
+        cost[i] = (cost[nd.left] + cost[nd.right]) + c
+    root = len(r.nodes) - 1
+    return cost[root] if rels.get(root) == set(range(g.n)) else None
+
+
+def config5_results(ctx, steps=3):
+    """BASELINE config 5: IDP2 / UnionDP with the GPU MPDP inner DP on the
+    1000-relation snowflake (seed 0), host wall time of the public call (every
+    inner DP on the GPU), the plan checked by recomputing its cost."""
+    g = W.snowflake(1000, 0)
+    runs = [("IDP2 k=25", lambda: ctx.mpdp_optimize(g, algo="IDP2_MPDP", k=25)),
+            ("UnionDP k=25 t=15", lambda: ctx.mpdp_optimize_uniondp(g, k=25, t=15)),
+            ("UnionDP k=25 t=25", lambda: ctx.mpdp_optimize_uniondp(g, k=25, t=25))]
+    out = []
+    for label, run in runs:
+        run()
+        ts = []
+        for _ in range(steps):
+            t = time.perf_counter()
+            r = run()
+            ts.append((time.perf_counter() - t) * 1e3)
+        rc = plan_cost_recomputed(g, r)
+        out.append({"workload": f"snowflake-1000 {label}", "ms": statistics.median(ts), "inner_calls": r.inner_calls,
+                    "pairs": r.pairs_evaluated, "plan_cost": r.cost, "plan_valid": rc is not None,
+                    "cost_recomputed_match": rc == r.cost, "timer": "host wall of mpdp_optimize"})
+    return out
+
+
 def config_results(ctx, flush, stream, torch, mpdp, traffic_all, sm_hz, peak, steps=5):
     """BASELINE configs 1, 2, 4 and the chain / cycle shapes north_star names:
     device time of the staged launch (L2 flushed), pairs/s, the kernel's
@@ -448,7 +499,7 @@ def run_ours(args):
                     "ms_per_step": 1e3 * e2e_s / args.steps},
             "gpu_launches": launches}
     if others:
-        line["configs"] = others
+        line["configs"] = others + config5_results(ctx)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, o = cpu_baseline(graphs[0])
         line["cpu_baseline"] = cb
