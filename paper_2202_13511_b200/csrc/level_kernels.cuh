@@ -696,29 +696,31 @@ __device__ void eval_range(const SQ<M>& q, M S, int k, int kind, unsigned long l
         return;
     }
     if constexpr (Sink::kChk) if (q.mc) {  // reading R20: S_left = grow(lb, S \ rb) is connected
-        sink.flush();                          // iff lb is, so the sink's probes are the CCP test
-        sink.chk = true;
+        sink.flush();                          // iff lb is, so the pair's probes are the CCP test;
+        unsigned long long nv = 0;             // S_left from the hanging parts (eval_blocks_hang)
+        M hv[MaxN<M>::value];
         unsigned long long base = 0;
         for (int bi = 0; bi < nb && base < j1; bi++) {
             const M Bm = blk[bi];
             const unsigned long long wb = (1ull << (popc(Bm) - 1)) - 1;
             if (base + wb > j0) {
                 const unsigned long long a0 = (j0 > base ? j0 - base : 0), a1 = (j1 - base < wb ? j1 - base : wb);
-                const M lo = lowbit(Bm), R = Bm ^ lo;
-                M sub = deposit<M>(a0, R);
-                for (unsigned long long j = a0; j < a1; j++) {
-                    const M lb = lo | sub;
-                    sub = (sub - R) & R;
-                    const M A = grow(q, lb, S & ~(Bm ^ lb));
-                    sink.add(A, S ^ A);
+                const M ext = S & ~Bm;
+                M C = 0;                       // vertices of B with neighbours outside B
+                for (M T = Bm; T; T &= T - 1) {
+                    const int u = ctz(T);
+                    if (q.adj[u] & ext) {
+                        C |= lowbit(T);
+                        hv[u] = grow(q, bitm<M>(u), ext | bitm<M>(u));
+                    }
                 }
+                const M lo = lowbit(Bm), R = Bm ^ lo;
+                mc_span<true, M>(q, S, lo, R, lowbit(R), deposit<M>(a0, R), a0, a1, 1u, sink.cS, C, hv, sink.best,
+                                 nv, sink.nprobe);
             }
             base += wb;
         }
-        sink.flush();
-        sink.chk = false;
-        nccp += sink.nvalid;
-        sink.nvalid = 0;
+        nccp += nv;
         return;
     }
     unsigned long long base = 0;
