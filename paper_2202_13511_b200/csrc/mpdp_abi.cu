@@ -135,6 +135,7 @@ struct mpdp_ctx {
 
     // staged query
     int n = 0, cls = CLS_TREE;
+    unsigned long long m = 0;             // edges of the staged query
     bool wide = false;                    // 64-bit masks
     bool staged = false;
     std::vector<unsigned long long> binom;
@@ -884,6 +885,15 @@ static bool small_eligible(const mpdp_ctx* c) {
     // general graphs gain nothing or lose (clique-9 59 vs 62 us, cycle-12 and
     // random-12 several times slower: Find-Blocks and the pair counts need the
     // whole GPU), so only tree queries take this path
+    // With memo-probe connectivity in shared memory (reading R20) general
+    // graphs with few independent cycles or n <= 10 now gain too (B200:
+    // cycle-12 0.244 -> 0.145 ms, cycle-13 0.270 -> 0.188, random-10 0.338 ->
+    // 0.246) while denser ones still lose (random-12 0.46 -> 0.72, random-13
+    // 0.46 -> 2.48 ms: their pairs need the whole GPU).
+    if (c->cls == CLS_GENERAL) {
+        if (const char* e = getenv("MPDP_DEBUG_SMALL_GENERAL")) return atoi(e) != 0;   // experiments only
+        return n <= 10 || c->m + 1 <= (unsigned long long)n + 4;     // cyclomatic number <= 4
+    }
     return c->cls == CLS_TREE;
 }
 
@@ -1881,6 +1891,7 @@ mpdp_status mpdp_stage(mpdp_ctx* c, const mpdp_query_graph* g) {
     c->n = n;
     c->wide = n > 32 || (c->flags & MPDP_FLAG_FORCE_WIDE_MASKS);
     const unsigned long long m = g->n_edges;
+    c->m = m;
     if (n >= 3 && m == (unsigned long long)n * (n - 1) / 2) c->cls = CLS_CLIQUE;
     else if (m == (unsigned long long)(n - 1)) c->cls = CLS_TREE;
     else c->cls = CLS_GENERAL;

@@ -142,6 +142,12 @@ __device__ __forceinline__ void small_body(const QueryDev<uint32_t>* qd, ResultD
         r->t_level[2] = globaltimer_ns();
     }
     __syncthreads();
+    if (CLS == CLS_GENERAL) {              // reading R20 on the shared-memory memo: every slot
+        for (unsigned int S = threadIdx.x; S < NS; S += blockDim.x)   // starts absent
+            cost[S] = __longlong_as_double((long long)kMemoAbsent);
+        if (threadIdx.x == 0) q.mc = cost;
+        __syncthreads();
+    }
     for (int v = threadIdx.x; v < n; v += blockDim.x) {      // level 1
         cost[1u << v] = q.leaf[v];
         card[1u << v] = q.card[v];
