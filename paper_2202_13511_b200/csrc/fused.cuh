@@ -677,6 +677,8 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
             M S0 = 0;
             unsigned int lflag = 0, hflag = 0, kinds = 0;   // kinds: 2 bits per rank (set_kind once)
             M cuts[kFusedRanksPerThread];      // general graphs: cut vertices of each rank's set (R21)
+            M blk0[kHeavyBlk];                 // the blocks of rank slot 0's set (most levels: one rank
+            int nb0 = -1;                      // per thread), reused by the heavy-list write
             Tri mine = {0, 0, 0};
             if (r0 < r_hi) {
                 S0 = unrank_colex32(bin, n, k, r0);
@@ -687,7 +689,9 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                         if (connected_cls<M, CLS>(q, S, k)) {
                             unsigned long long w;
                             cuts[i] = 0;
-                            const int kind = set_kind<M, CLS>(q, S, k, w, nullptr, nullptr, &cuts[i]);
+                            const int kind = (CLS == CLS_GENERAL && i == 0)
+                                                 ? set_kind<M, CLS>(q, S, k, w, blk0, &nb0, &cuts[i])
+                                                 : set_kind<M, CLS>(q, S, k, w, nullptr, nullptr, &cuts[i]);
                             kinds |= (unsigned int)kind << (2 * i);
                             // (general graphs: only sets without CCP checks,
                             // or with few candidates, are evaluated by one thread)
@@ -775,7 +779,16 @@ __global__ void __launch_bounds__(kBlock, CLS == CLS_TREE ? 3 : 2) k_dp_fused(co
                             M blk[kHeavyBlk];
                             int nb = 0;
                             const int kind = (int)((kinds >> (2 * i)) & 3u);
-                            w = kind_pairs<M, CLS>(q, S, k, kind, blk, &nb, cuts[i]);
+                            if (i == 0 && kind == KIND_BLOCKS && nb0 >= 0 && nb0 <= kHeavyBlk && !q.dpsub) {
+                                nb = nb0;              // found by the classification above
+                                w = 0;
+                                for (int b = 0; b < nb; b++) {
+                                    blk[b] = blk0[b];
+                                    w += (1ull << (popc(blk0[b]) - 1)) - 1;
+                                }
+                            } else {
+                                w = kind_pairs<M, CLS>(q, S, k, kind, blk, &nb, cuts[i]);
+                            }
                             if (hi < p.heavy_cap) {
                                 p.hinfo[hi] = (unsigned int)kind | ((unsigned int)nb << 2);
                                 for (int b = 0; b < nb && b < kHeavyBlk; b++) p.hblk[hi * kHeavyBlk + b] = blk[b];
